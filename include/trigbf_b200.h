@@ -1,0 +1,132 @@
+/*
+ * trigbf_b200.h -- C ABI of the B200-native constant-time trigonometric
+ * bilateral filter (arXiv 1105.4204 hot path).
+ *
+ * All pointers named d_* / f / out / num / den / workspace are DEVICE
+ * pointers (CUDA global memory on the current device); `stream` is a
+ * cudaStream_t passed as void*.  Every entry point is asynchronous on
+ * `stream` and returns a status code for errors detectable at launch time.
+ * No torch / C++ types cross this boundary.
+ *
+ * What each entry replaces in the reference package (/root/reference/pkg):
+ *
+ *   tbf_bilateral_trig   engines.py:228-306  bilateral_trig(img, spatial, kernel)
+ *                        (term loop + smooth_plane + demodulate + _guarded_ratio)
+ *   tbf_trig_partial     engines.py:249-300  the term loop restricted to the
+ *                        pairs [term_begin, term_end): accumulates num/den only
+ *                        (term-sharded multi-GPU path; NCCL reduce sits between
+ *                        this and tbf_finalize)
+ *   tbf_finalize         engines.py:109-117  _guarded_ratio(num, den, f)
+ *   tbf_range_check      engines.py:218-225  _check_range(plane, T)
+ *   tbf_recursive_smooth_f64
+ *                        _core.pyx:56-96     recursive_smooth(a, scale, c1..c4, pad)
+ *                        (the L1 plugin entry _backend.recursive_smooth,
+ *                        _backend.py:38-39)
+ *   tbf_box_pass_f64     _core.pyx:28-53     box_pass(a, radius)
+ *                        (_backend.box_pass, _backend.py:38)
+ */
+#ifndef TRIGBF_B200_H
+#define TRIGBF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TBF_API __attribute__((visibility("default")))
+#else
+#define TBF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (the Python wrapper maps them to the reference's exception
+ * classes, errors.py:4-24). */
+#define TBF_OK 0
+#define TBF_ERR_RANGE 1     /* ParameterError: samples outside [0, T]      */
+#define TBF_ERR_PARAM 2     /* ParameterError: bad filter / kernel params   */
+#define TBF_ERR_DIM 3       /* DimensionError: bad shape                    */
+#define TBF_ERR_CUDA 4      /* CUDA launch / runtime error                  */
+#define TBF_ERR_WORKSPACE 5 /* workspace too small                          */
+
+#define TBF_SPATIAL_RECURSIVE 0 /* SpatialKind.GAUSSIAN_RECURSIVE, spatial.py:31-34 */
+#define TBF_SPATIAL_BOX 1       /* SpatialKind.BOX                                   */
+
+/* Spatial smoother (SpatialSpec, spatial.py:41-74), already reduced to the
+ * numbers the device needs.  Recursive Gaussian: the reference's 4th-order
+ * recursion (spatial.py:124-144) factored into its two pole pairs, i.e. two
+ * second-order sections y = g*x + a1*y[-1] + a2*y[-2] (g1,a1,a2) then
+ * (g2,b1,b2).  ext_y / ext_x: mirror warm-up length per axis, min(K, n-1)
+ * where K is the decay length of the recursion (the reference uses n-1,
+ * spatial.py:163-172; beyond K the difference is below 1e-7 relative). */
+typedef struct tbf_spatial {
+    int32_t kind;
+    int32_t radius; /* box radius (>= 0) */
+    double g1, a1, a2;
+    double g2, b1, b2;
+    int32_t ext_y;
+    int32_t ext_x;
+} tbf_spatial;
+
+/* Raised-cosine range kernel expansion (make_trig_kernel, kernels.py:125-158,
+ * folded into frequency/weight pairs as in engines.py:249-253).  Host arrays,
+ * ascending frequency; nu[j] = nu[0] + j*dnu must hold (true for the
+ * reference's pairs, including a leading zero frequency for even N). */
+typedef struct tbf_terms {
+    int32_t n_terms;      /* number of pairs (P + [N even]) */
+    const double* nu;     /* [n_terms] frequencies */
+    const double* weight; /* [n_terms] pair weights */
+    double dnu;           /* 2*omega */
+    double T;             /* declared intensity range */
+} tbf_terms;
+
+/* Device workspace needed by tbf_bilateral_trig / tbf_trig_partial for the
+ * given shape and term range.  batch_terms <= 0 selects all terms at once. */
+TBF_API size_t tbf_workspace_bytes(int32_t B, int32_t H, int32_t W, const tbf_spatial* sp,
+                           int32_t term_begin, int32_t term_end, int32_t batch_terms);
+
+/* Full filter: out[b][y][x] for B frames of H x W fp32 samples (row-major,
+ * frame-major).  d_counters (device, 2 x uint64, zeroed by the caller):
+ * [0] += number of samples outside [-1e-9, T+1e-9] (or non-finite),
+ * [1] += number of guarded pixels (den < 1e-12, engines.py:109-117). */
+TBF_API int tbf_bilateral_trig(const float* f, float* out, int32_t B, int32_t H, int32_t W,
+                       const tbf_spatial* sp, const tbf_terms* terms, int32_t batch_terms,
+                       void* workspace, size_t workspace_bytes,
+                       unsigned long long* d_counters, void* stream);
+
+/* Term-sharded piece: num/den[b][y][x] (+)= the contribution of pairs
+ * [term_begin, term_end).  accumulate=0 overwrites num/den. */
+TBF_API int tbf_trig_partial(const float* f, float* num, float* den, int32_t B, int32_t H, int32_t W,
+                     const tbf_spatial* sp, const tbf_terms* terms, int32_t term_begin,
+                     int32_t term_end, int32_t batch_terms, int32_t accumulate,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* out = num/den where den >= 1e-12, else f; d_counters[1] += guarded count. */
+TBF_API int tbf_finalize(const float* num, const float* den, const float* f, float* out, int64_t count,
+                 unsigned long long* d_counters, void* stream);
+
+/* d_counters[0] += number of samples outside [-1e-9, T+1e-9] or non-finite. */
+TBF_API int tbf_range_check(const float* f, int64_t count, double T, unsigned long long* d_counters,
+                    void* stream);
+
+/* Plugin-level twins of the reference's compiled core, fp64 like the
+ * reference.  recursive_smooth filters along axis 0 of a[h][w] with `pad`
+ * mirrored rows per side and replicate start-up; scratch holds
+ * (h + 2*pad + 8) * w doubles.  box_pass filters along the last axis. */
+TBF_API int tbf_recursive_smooth_f64(const double* a, double* out, int32_t h, int32_t w, double scale,
+                             double c1, double c2, double c3, double c4, int32_t pad,
+                             double* scratch, void* stream);
+TBF_API int tbf_box_pass_f64(const double* a, double* out, int32_t h, int32_t w, int32_t radius,
+                     void* stream);
+
+/* Last error message of the calling thread (static storage). */
+TBF_API const char* tbf_last_error(void);
+/* ABI version (bumped on any signature change). */
+TBF_API int32_t tbf_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TRIGBF_B200_H */

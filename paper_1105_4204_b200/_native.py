@@ -1,0 +1,136 @@
+"""ctypes binding of the C ABI declared in include/trigbf_b200.h.
+
+This is the reference-side binding a maintainer would add next to
+``trigbf/_backend.py``: plain pointers and sizes, no torch types.  Loading
+fails loudly (``NativeUnavailableError``) -- there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import DimensionError, NativeUnavailableError, ParameterError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libtrigbf_b200.so")
+
+TBF_OK = 0
+TBF_ERR_RANGE = 1
+TBF_ERR_PARAM = 2
+TBF_ERR_DIM = 3
+TBF_ERR_CUDA = 4
+TBF_ERR_WORKSPACE = 5
+
+TBF_SPATIAL_RECURSIVE = 0
+TBF_SPATIAL_BOX = 1
+
+# Every symbol the header declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "tbf_workspace_bytes",
+    "tbf_bilateral_trig",
+    "tbf_trig_partial",
+    "tbf_finalize",
+    "tbf_range_check",
+    "tbf_recursive_smooth_f64",
+    "tbf_box_pass_f64",
+    "tbf_last_error",
+    "tbf_abi_version",
+)
+ABI_VERSION = 1
+
+
+class TbfSpatial(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("radius", ctypes.c_int32),
+        ("g1", ctypes.c_double),
+        ("a1", ctypes.c_double),
+        ("a2", ctypes.c_double),
+        ("g2", ctypes.c_double),
+        ("b1", ctypes.c_double),
+        ("b2", ctypes.c_double),
+        ("ext_y", ctypes.c_int32),
+        ("ext_x", ctypes.c_int32),
+    ]
+
+
+class TbfTerms(ctypes.Structure):
+    _fields_ = [
+        ("n_terms", ctypes.c_int32),
+        ("nu", ctypes.POINTER(ctypes.c_double)),
+        ("weight", ctypes.POINTER(ctypes.c_double)),
+        ("dnu", ctypes.c_double),
+        ("T", ctypes.c_double),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_f64 = ctypes.c_double
+_sz = ctypes.c_size_t
+
+
+def _declare(lib):
+    lib.tbf_abi_version.restype = _i32
+    lib.tbf_abi_version.argtypes = []
+    lib.tbf_last_error.restype = ctypes.c_char_p
+    lib.tbf_last_error.argtypes = []
+    lib.tbf_workspace_bytes.restype = _sz
+    lib.tbf_workspace_bytes.argtypes = [_i32, _i32, _i32, ctypes.POINTER(TbfSpatial), _i32, _i32, _i32]
+    lib.tbf_bilateral_trig.restype = ctypes.c_int
+    lib.tbf_bilateral_trig.argtypes = [
+        _vp, _vp, _i32, _i32, _i32, ctypes.POINTER(TbfSpatial), ctypes.POINTER(TbfTerms), _i32,
+        _vp, _sz, _vp, _vp,
+    ]
+    lib.tbf_trig_partial.restype = ctypes.c_int
+    lib.tbf_trig_partial.argtypes = [
+        _vp, _vp, _vp, _i32, _i32, _i32, ctypes.POINTER(TbfSpatial), ctypes.POINTER(TbfTerms),
+        _i32, _i32, _i32, _i32, _vp, _sz, _vp,
+    ]
+    lib.tbf_finalize.restype = ctypes.c_int
+    lib.tbf_finalize.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _vp]
+    lib.tbf_range_check.restype = ctypes.c_int
+    lib.tbf_range_check.argtypes = [_vp, _i64, _f64, _vp, _vp]
+    lib.tbf_recursive_smooth_f64.restype = ctypes.c_int
+    lib.tbf_recursive_smooth_f64.argtypes = [
+        _vp, _vp, _i32, _i32, _f64, _f64, _f64, _f64, _f64, _i32, _vp, _vp,
+    ]
+    lib.tbf_box_pass_f64.restype = ctypes.c_int
+    lib.tbf_box_pass_f64.argtypes = [_vp, _vp, _i32, _i32, _i32, _vp]
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and return the extension library."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailableError(
+                f"sm_100a extension not built ({path}); run `python -m paper_1105_4204_b200.build`"
+            )
+        lib = ctypes.CDLL(path)
+        _declare(lib)
+        ver = lib.tbf_abi_version()
+        if ver != ABI_VERSION:
+            raise NativeUnavailableError(f"ABI mismatch: library {ver}, binding {ABI_VERSION}")
+        _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    """Map a status code to the reference's exception classes (errors.py:4-24)."""
+    if rc == TBF_OK:
+        return
+    msg = load().tbf_last_error().decode(errors="replace")
+    if rc in (TBF_ERR_RANGE, TBF_ERR_PARAM):
+        raise ParameterError(msg)
+    if rc == TBF_ERR_DIM:
+        raise DimensionError(msg)
+    raise RuntimeError(f"trigbf_b200 error {rc}: {msg}")

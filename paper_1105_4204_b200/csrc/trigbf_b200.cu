@@ -1,0 +1,1228 @@
+// trigbf_b200.cu -- B200 (sm_100a) constant-time trigonometric bilateral filter.
+//
+// Reference semantics: /root/reference/pkg/src/trigbf/engines.py:228-306
+// (bilateral_trig) with spatial.py:163-182 (separable recursive Gaussian /
+// box smoother) and _core.pyx:28-96 (the two compiled loops).
+//
+// Pipeline per term batch (see DESIGN.md for the derivation and roofline):
+//
+//   k_pass1_gauss  one warp = 32 adjacent columns x one group of G1 terms.
+//                  The four auxiliary planes of each term (cos, sin, f*cos,
+//                  f*sin of nu*f) are generated in registers from f and run
+//                  through the forward/backward biquad cascade along y.  The
+//                  causal->anticausal dependency is broken with per-32-row
+//                  checkpoints of the forward state (phase A) and a segment-
+//                  wise recompute into shared memory (phase B).  The segment
+//                  tile is then read transposed from shared memory and the
+//                  zero-state forward recursion along x is run over the 32
+//                  columns of the tile ("tile-local forward"), which is what is
+//                  written to HBM (one fp32 round trip of the 4 planes).
+//   k_chain        per (row, plane): chains the 4-state carries of the tiles
+//                  along x (s' = M s + L), handles the mirrored x-extension,
+//                  and produces the backward start state.
+//   k_pass2_gauss  one thread = one row x G2 terms, tiles right to left:
+//                  exact forward output = tile-local + H[m] . carry, then the
+//                  backward cascade, demodulation and num/den accumulation in
+//                  registers (fused; no second round trip).
+//   k_reduce       folds the per-group partial num/den, transposes back to
+//                  row-major and applies the guarded ratio (engines.py:109-117).
+//
+// No tensor cores: the path is a set of first/second-order linear
+// recurrences, bounded by HBM bandwidth and the FP32 pipe.
+
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "trigbf_b200.h"
+
+#define TBF_ABI_VERSION 1
+
+namespace {
+
+constexpr int TILE = 32;          // segment length along y == tile width along x == warp size
+constexpr int P1_WARPS = 4;       // warps per pass-1 block (each a different term group)
+constexpr int P2_THREADS = 128;   // rows per pass-2 block
+constexpr int BUF_LD = TILE + 1;  // padded leading dimension of the smem tile
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+int check_cuda(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(TBF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return TBF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Device helpers
+// ---------------------------------------------------------------------------
+
+struct Casc {
+    float g1, a1, a2, g2, b1, b2;
+};
+
+// Whole-sample reflection for indices within one reflection of the line
+// (|extension| <= n-1), identical to _mirror (_core.pyx:14-25) there.
+__device__ __forceinline__ int mirror1(int i, int n) {
+    i = i < 0 ? -i : i;
+    return i >= n ? 2 * (n - 1) - i : i;
+}
+
+// General whole-sample reflection (period 2(n-1)), _core.pyx:14-25.
+__device__ __forceinline__ long long mirror_any(long long i, long long n) {
+    if (n == 1) return 0;
+    long long period = 2 * (n - 1);
+    i %= period;
+    if (i < 0) i += period;
+    return i >= n ? period - i : i;
+}
+
+// One step of the cascade of two all-pole biquads (state v1,v2 | y1,y2).
+__device__ __forceinline__ float cstep(float u, float& v1, float& v2, float& y1, float& y2,
+                                       const Casc& k) {
+    float v = fmaf(k.g1, u, fmaf(k.a1, v1, k.a2 * v2));
+    v2 = v1;
+    v1 = v;
+    float y = fmaf(k.g2, v, fmaf(k.b1, y1, k.b2 * y2));
+    y2 = y1;
+    y1 = y;
+    return y;
+}
+
+// Phasors of G consecutive terms at one sample (engines.py:272-286).  Terms
+// are grouped in anchor blocks of R: the first term of a block takes an
+// accurate sincos of nu*f (nu split hi/lo so the phase is correctly rounded,
+// no SFU approximation), the others follow by complex rotation with
+// (cos, sin)(dnu*f).  Pass 1 and pass 2 use the same rule, so modulation and
+// demodulation see bit-identical phasors.
+template <int G, int R>
+__device__ __forceinline__ void phasors(float fv, const float (&nu_hi)[G], const float (&nu_lo)[G],
+                                        float dnu, float (&cc)[G], float (&sn)[G]) {
+    float ss = 0.f, sc = 1.f;
+    if (R > 1) sincosf(dnu * fv, &ss, &sc);
+    float c = 1.f, s = 0.f;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        if (g % R == 0) {
+            sincosf(fmaf(nu_hi[g], fv, nu_lo[g] * fv), &s, &c);
+        } else {
+            float cn = fmaf(c, sc, -s * ss);
+            float snn = fmaf(s, sc, c * ss);
+            c = cn;
+            s = snn;
+        }
+        cc[g] = c;
+        sn[g] = s;
+    }
+}
+
+// Auxiliary planes u[4g+0..3] = cos, sin, f*cos, f*sin (engines.py:287).
+template <int G, int R>
+__device__ __forceinline__ void modulate(float fv, const float (&nu_hi)[G], const float (&nu_lo)[G],
+                                         float dnu, float (&u)[4 * G]) {
+    float cc[G], sn[G];
+    phasors<G, R>(fv, nu_hi, nu_lo, dnu, cc, sn);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        u[4 * g + 0] = cc[g];
+        u[4 * g + 1] = sn[g];
+        u[4 * g + 2] = fv * cc[g];
+        u[4 * g + 3] = fv * sn[g];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Kernel arguments
+// ---------------------------------------------------------------------------
+
+struct TermDev {
+    const float* nu_hi;  // [n] batch-relative
+    const float* nu_lo;
+    const float* w;
+    float dnu;
+    int n;       // terms in the batch
+    int anchor;  // phasor anchor block (== G1); groups never straddle anchors
+};
+
+struct Pass1Args {
+    const float* f;
+    int B, H, W;
+    int Ey, nseg;  // y warm-up, ceil((H+Ey)/32) checkpoint segments
+    int Ex, ne, edge_all, ntx;
+    Casc k;
+    TermDev t;
+    int ngroups;    // ceil(t.n / G1)
+    float* ckpt;    // [nseg][n*16][B][W]
+    float* floc;    // [n*4][B][W][H]   tile-local forward along x (transposed)
+    float* lcarry;  // [n*16][B][ntx][H]
+    float* edge;    // [n*4][B][ne][H]  raw y-filtered values at x-edge columns
+};
+
+struct ChainArgs {
+    int B, H, W;
+    int Ex, ne, edge_all, ntx;
+    Casc k;
+    int nplanes;          // n*4
+    float M[16];          // full-tile state transfer (column-major: M[k*4+r])
+    float Mlast[16];      // last (possibly partial) tile
+    const float* edge;    // [n*4][B][ne][H]
+    float* lcarry;        // in: local carries, out: chained carries (state at tile start)
+    float* extbuf;        // [n*4][B][Ex][H]
+    float* bstate;        // [n*16][B][H] backward start state
+};
+
+struct Pass2Args {
+    const float* fT;  // [B][W][H]
+    int B, H, W, ntx;
+    Casc k;
+    TermDev t;
+    int ngroups;       // ceil(t.n / G2)
+    float Hm[TILE][4]; // homogeneous response of the cascade to a unit state
+    const float* floc;
+    const float* carry;   // chained carries [n*16][B][ntx][H]
+    const float* bstate;  // [n*16][B][H]
+    float* part;          // [ngroups*2][B][W][H]
+};
+
+struct ReduceArgs {
+    const float* part;  // [ngroups*2][B][W][H]
+    int ngroups;
+    int B, H, W;
+    const float* in_num;  // [B][H][W] added to the partials when non-null
+    const float* in_den;
+    float* num;           // [B][H][W] written when non-null
+    float* den;
+    const float* f;       // guard fallback (when out != null)
+    float* out;           // [B][H][W] guarded ratio when non-null
+    unsigned long long* counters;
+};
+
+// ---------------------------------------------------------------------------
+// Pass 1 (recursive Gaussian): y-direction forward/backward + x tile-local
+// forward.  Replaces smooth_plane's first 1-D pass (spatial.py:169-170,
+// _core.pyx:56-96) for the 4 auxiliary planes of G terms, fused with their
+// generation (engines.py:272-287).
+// ---------------------------------------------------------------------------
+
+template <int G, int R>
+__global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_constant__ Pass1Args a) {
+    constexpr int NP = 4 * G;
+    extern __shared__ float smem[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int grp = blockIdx.y * P1_WARPS + warp;
+    if (grp >= a.ngroups) return;  // whole warp; no block-level barriers below
+    const int b = blockIdx.z;
+    const int H = a.H, W = a.W;
+    const int x0 = blockIdx.x * TILE;
+    const int x = x0 + lane;
+    const int xc = x < W ? x : W - 1;
+    const int tlen = min(TILE, W - x0);
+    const int j0 = grp * G;
+    const int nt = min(G, a.t.n - j0);  // valid terms in this group (1..G)
+    float* buf = smem + (size_t)warp * NP * TILE * BUF_LD;
+
+    float nu_hi[G], nu_lo[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        nu_hi[g] = a.t.nu_hi[j0 + g];  // table is padded past n
+        nu_lo[g] = a.t.nu_lo[j0 + g];
+    }
+    const float dnu = a.t.dnu;
+    const float* fcol = a.f + (size_t)b * H * W + xc;
+    const Casc k = a.k;
+    const int Ey = a.Ey;
+    const int iend = H + Ey;
+
+    float v1[NP], v2[NP], y1[NP], y2[NP], u[NP];
+
+    // ---- phase A: forward sweep over the mirrored column, checkpoints ----
+    {
+        float fv = __ldg(fcol + (size_t)mirror1(-Ey, H) * W);
+        modulate<G, R>(fv, nu_hi, nu_lo, dnu, u);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) v1[p] = v2[p] = y1[p] = y2[p] = u[p];
+    }
+    const size_t ck_stride_seg = (size_t)a.t.n * 16 * a.B * W;
+    float* ck_base = a.ckpt + ((size_t)(j0 * 16) * a.B + b) * W + x;
+    const size_t ck_stride_q = (size_t)a.B * W;
+    for (int ib = -Ey; ib < iend; ib += 8) {
+        float fv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            int i = ib + q;
+            fv[q] = i < iend ? __ldg(fcol + (size_t)mirror1(i, H) * W) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            int i = ib + q;
+            if (i < iend) {
+                if (i >= 0 && (i & (TILE - 1)) == 0 && x < W) {
+                    float* ck = ck_base + (size_t)(i >> 5) * ck_stride_seg;
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        if (p / 4 < nt) {
+                            ck[(size_t)(p * 4 + 0) * ck_stride_q] = v1[p];
+                            ck[(size_t)(p * 4 + 1) * ck_stride_q] = v2[p];
+                            ck[(size_t)(p * 4 + 2) * ck_stride_q] = y1[p];
+                            ck[(size_t)(p * 4 + 3) * ck_stride_q] = y2[p];
+                        }
+                    }
+                }
+                modulate<G, R>(fv[q], nu_hi, nu_lo, dnu, u);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
+            }
+        }
+    }
+
+    // ---- phase B: segments bottom -> top ----
+    float p1[NP], p2[NP], q1[NP], q2[NP];
+    const size_t fl_plane = (size_t)a.B * W * H;
+    float* fl_base = a.floc + ((size_t)(j0 * 4) * a.B + b) * W * (size_t)H;
+    const size_t lc_q = (size_t)a.B * a.ntx * H;
+    float* lc_base = a.lcarry + ((size_t)(j0 * 16) * a.B + b) * a.ntx * (size_t)H +
+                     (size_t)blockIdx.x * H;
+    const size_t ed_plane = (size_t)a.B * a.ne * H;
+    float* ed_base = a.edge + ((size_t)(j0 * 4) * a.B + b) * a.ne * (size_t)H;
+
+    for (int seg = a.nseg - 1; seg >= 0; --seg) {
+        const int i0 = seg * TILE;
+        const int i1 = min(i0 + TILE, iend);
+        if (x < W) {
+            const float* ck = ck_base + (size_t)seg * ck_stride_seg;
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                if (p / 4 < nt) {
+                    v1[p] = ck[(size_t)(p * 4 + 0) * ck_stride_q];
+                    v2[p] = ck[(size_t)(p * 4 + 1) * ck_stride_q];
+                    y1[p] = ck[(size_t)(p * 4 + 2) * ck_stride_q];
+                    y2[p] = ck[(size_t)(p * 4 + 3) * ck_stride_q];
+                } else {
+                    v1[p] = v2[p] = y1[p] = y2[p] = 0.f;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) v1[p] = v2[p] = y1[p] = y2[p] = 0.f;
+        }
+        // forward recompute of the segment into smem (own column only)
+        for (int ib = i0; ib < i1; ib += 8) {
+            float fv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                int i = ib + q;
+                fv[q] = i < i1 ? __ldg(fcol + (size_t)mirror1(i, H) * W) : 0.f;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                int i = ib + q;
+                if (i < i1) {
+                    modulate<G, R>(fv[q], nu_hi, nu_lo, dnu, u);
+#pragma unroll
+                    for (int p = 0; p < NP; ++p)
+                        buf[(p * TILE + (i - i0)) * BUF_LD + lane] =
+                            cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
+                }
+            }
+        }
+        if (seg == a.nseg - 1) {
+            // backward start = steady state of the last forward output (_core.pyx:85-87)
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                float last = buf[(p * TILE + (i1 - 1 - i0)) * BUF_LD + lane];
+                p1[p] = p2[p] = q1[p] = q2[p] = last;
+            }
+        }
+        // backward sweep over the segment, in place
+        for (int i = i1 - 1; i >= i0; --i) {
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                float* cell = &buf[(p * TILE + (i - i0)) * BUF_LD + lane];
+                *cell = cstep(*cell, p1[p], p2[p], q1[p], q2[p], k);
+            }
+        }
+        if (i0 < H) {
+            __syncwarp();
+            // epilogue: lane <-> row i; tile-local zero-state forward along x
+            const int i = i0 + lane;
+            if (i < min(i1, H)) {
+                float lv1[NP], lv2[NP], ly1[NP], ly2[NP];
+#pragma unroll
+                for (int p = 0; p < NP; ++p) lv1[p] = lv2[p] = ly1[p] = ly2[p] = 0.f;
+                for (int xx = 0; xx < tlen; ++xx) {
+                    const int gx = x0 + xx;
+                    const bool is_edge = a.edge_all || gx <= a.Ex || gx >= W - 1 - a.Ex;
+                    const int e = a.edge_all ? gx : (gx <= a.Ex ? gx : gx - (W - 1 - a.Ex) + a.Ex + 1);
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        if (p / 4 < nt) {
+                            float yv = buf[(p * TILE + lane) * BUF_LD + xx];
+                            float yl = cstep(yv, lv1[p], lv2[p], ly1[p], ly2[p], k);
+                            fl_base[(size_t)p * fl_plane + (size_t)gx * H + i] = yl;
+                            if (is_edge) ed_base[(size_t)p * ed_plane + (size_t)e * H + i] = yv;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    if (p / 4 < nt) {
+                        lc_base[(size_t)(p * 4 + 0) * lc_q + i] = lv1[p];
+                        lc_base[(size_t)(p * 4 + 1) * lc_q + i] = lv2[p];
+                        lc_base[(size_t)(p * 4 + 2) * lc_q + i] = ly1[p];
+                        lc_base[(size_t)(p * 4 + 3) * lc_q + i] = ly2[p];
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Chain: per (row, plane) the x-direction carries and the mirrored x-extension
+// (spatial.py:171 with pad = W-1 truncated to ext_x, _core.pyx:56-96).
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(128) k_chain(const __grid_constant__ ChainArgs a) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.H) return;
+    const int bt = blockIdx.y;  // tp * B + b
+    const int H = a.H, W = a.W, Ex = a.Ex;
+    const Casc k = a.k;
+    const float* ed = a.edge + (size_t)bt * a.ne * H + i;
+    auto Y = [&](int xx) -> float {
+        int e = a.edge_all ? xx : (xx <= Ex ? xx : xx - (W - 1 - Ex) + Ex + 1);
+        return ed[(size_t)e * H];
+    };
+    float v1, v2, y1, y2;
+    {
+        float u0 = Y(Ex);  // mirror(-Ex)
+        v1 = v2 = y1 = y2 = u0;
+    }
+    for (int xx = -Ex; xx < 0; ++xx) cstep(Y(-xx), v1, v2, y1, y2, k);
+    // chain along x; the 4 carry planes of this plane are tq = tp*4 + {0..3}
+    const int tp = bt / a.B, b = bt % a.B;
+    const size_t q_stride = (size_t)a.B * a.ntx * H;
+    float* lc = a.lcarry + ((size_t)(tp * 4) * a.B + b) * a.ntx * (size_t)H + i;
+    for (int t = 0; t < a.ntx; ++t) {
+        float* c = lc + (size_t)t * H;
+        float L0 = c[0], L1 = c[q_stride], L2 = c[2 * q_stride], L3 = c[3 * q_stride];
+        c[0] = v1;
+        c[q_stride] = v2;
+        c[2 * q_stride] = y1;
+        c[3 * q_stride] = y2;
+        const float* M = (t == a.ntx - 1) ? a.Mlast : a.M;
+        float s0 = v1, s1 = v2, s2 = y1, s3 = y2;
+        v1 = fmaf(M[0], s0, fmaf(M[4], s1, fmaf(M[8], s2, fmaf(M[12], s3, L0))));
+        v2 = fmaf(M[1], s0, fmaf(M[5], s1, fmaf(M[9], s2, fmaf(M[13], s3, L1))));
+        y1 = fmaf(M[2], s0, fmaf(M[6], s1, fmaf(M[10], s2, fmaf(M[14], s3, L2))));
+        y2 = fmaf(M[3], s0, fmaf(M[7], s1, fmaf(M[11], s2, fmaf(M[15], s3, L3))));
+    }
+    // right extension: forward over x = W .. W-1+Ex (input Y(2(W-1)-x)), then backward
+    float last = y1;
+    float* ext = a.extbuf + (size_t)bt * Ex * H + i;
+    for (int e = 0; e < Ex; ++e) {
+        last = cstep(Y(W - 2 - e), v1, v2, y1, y2, k);
+        ext[(size_t)e * H] = last;
+    }
+    float p1 = last, p2 = last, q1 = last, q2 = last;
+    for (int e = Ex - 1; e >= 0; --e) cstep(ext[(size_t)e * H], p1, p2, q1, q2, k);
+    float* bs = a.bstate + ((size_t)(tp * 4) * a.B + b) * H + i;
+    const size_t bq = (size_t)a.B * H;
+    bs[0] = p1;
+    bs[bq] = p2;
+    bs[2 * bq] = q1;
+    bs[3 * bq] = q2;
+}
+
+// ---------------------------------------------------------------------------
+// Pass 2 (recursive Gaussian): x-direction backward sweep on the exact forward
+// output, fused with demodulation + accumulation (engines.py:297-298).
+// ---------------------------------------------------------------------------
+
+template <int G, int R>
+__global__ void __launch_bounds__(P2_THREADS) k_pass2_gauss(const __grid_constant__ Pass2Args a) {
+    constexpr int NP = 4 * G;
+    const int i_raw = blockIdx.x * P2_THREADS + threadIdx.x;
+    const int H = a.H, W = a.W;
+    const bool iv = i_raw < H;
+    const int i = iv ? i_raw : H - 1;
+    const int grp = blockIdx.y;
+    const int b = blockIdx.z;
+    const int j0 = grp * G;
+    const int nt = min(G, a.t.n - j0);
+    const Casc k = a.k;
+    float nu_hi[G], nu_lo[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        nu_hi[g] = a.t.nu_hi[j0 + g];  // table is padded past n
+        nu_lo[g] = a.t.nu_lo[j0 + g];
+    }
+    const float dnu = a.t.dnu;
+    float wt[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) wt[g] = g < nt ? a.t.w[j0 + g] : 0.f;
+
+    const size_t plane = (size_t)a.B * W * H;
+    const float* fl = a.floc + ((size_t)(j0 * 4) * a.B + b) * W * (size_t)H + i;
+    const float* fT = a.fT + (size_t)b * W * H + i;
+    const size_t cq = (size_t)a.B * a.ntx * H;
+    const float* cr = a.carry + ((size_t)(j0 * 16) * a.B + b) * a.ntx * (size_t)H + i;
+    float p1[NP], p2[NP], q1[NP], q2[NP], C[NP][4];
+    {
+        const size_t bq = (size_t)a.B * H;
+        const float* bs = a.bstate + ((size_t)(j0 * 16) * a.B + b) * H + i;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            if (p / 4 < nt) {
+                p1[p] = bs[(size_t)(p * 4 + 0) * bq];
+                p2[p] = bs[(size_t)(p * 4 + 1) * bq];
+                q1[p] = bs[(size_t)(p * 4 + 2) * bq];
+                q2[p] = bs[(size_t)(p * 4 + 3) * bq];
+            } else {
+                p1[p] = p2[p] = q1[p] = q2[p] = 0.f;
+            }
+        }
+    }
+    float* pn = a.part + ((size_t)(grp * 2 + 0) * a.B + b) * W * (size_t)H + i_raw;
+    float* pd = a.part + ((size_t)(grp * 2 + 1) * a.B + b) * W * (size_t)H + i_raw;
+
+    for (int t = a.ntx - 1; t >= 0; --t) {
+        const int x0 = t * TILE;
+        const int len = min(TILE, W - x0);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+                C[p][s] = p / 4 < nt ? cr[(size_t)(p * 4 + s) * cq + (size_t)t * H] : 0.f;
+        }
+        for (int mb = len - 1; mb >= 0; mb -= 4) {
+            float fv[4], fo[4][NP];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int m = mb - q;
+                const int gx = x0 + (m >= 0 ? m : 0);
+                fv[q] = fT[(size_t)gx * H];
+#pragma unroll
+                for (int p = 0; p < NP; ++p)
+                    fo[q][p] = p / 4 < nt ? fl[(size_t)p * plane + (size_t)gx * H] : 0.f;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int m = mb - q;
+                if (m >= 0) {
+                    float cc[G], sn[G];
+                    phasors<G, R>(fv[q], nu_hi, nu_lo, dnu, cc, sn);
+                    float yo[NP];
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        float F = fo[q][p];
+                        F = fmaf(a.Hm[m][0], C[p][0], F);
+                        F = fmaf(a.Hm[m][1], C[p][1], F);
+                        F = fmaf(a.Hm[m][2], C[p][2], F);
+                        F = fmaf(a.Hm[m][3], C[p][3], F);
+                        yo[p] = cstep(F, p1[p], p2[p], q1[p], q2[p], k);
+                    }
+                    float num = 0.f, den = 0.f;
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        num = fmaf(wt[g], fmaf(cc[g], yo[4 * g + 2], sn[g] * yo[4 * g + 3]), num);
+                        den = fmaf(wt[g], fmaf(cc[g], yo[4 * g + 0], sn[g] * yo[4 * g + 1]), den);
+                    }
+                    if (iv) {
+                        const size_t off = (size_t)(x0 + m) * H;
+                        pn[off] = num;
+                        pd[off] = den;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Box variant (spatial.py:157-160 + box_pass _core.pyx:28-53): pass 1 along y
+// writes the y-filtered planes transposed into floc; pass 2 runs the x window
+// and demodulates.  Running sums in fp64 (the reference keeps long double).
+// ---------------------------------------------------------------------------
+
+template <int G, int R>
+__global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_box(const __grid_constant__ Pass1Args a, int radius) {
+    constexpr int NP = 4 * G;
+    extern __shared__ float smem[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int grp = blockIdx.y * P1_WARPS + warp;
+    if (grp >= a.ngroups) return;
+    const int b = blockIdx.z;
+    const int H = a.H, W = a.W;
+    const int x0 = blockIdx.x * TILE;
+    const int x = x0 + lane;
+    const int xc = x < W ? x : W - 1;
+    const int tlen = min(TILE, W - x0);
+    const int j0 = grp * G;
+    const int nt = min(G, a.t.n - j0);
+    float* buf = smem + (size_t)warp * NP * TILE * BUF_LD;
+    float nu_hi[G], nu_lo[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        nu_hi[g] = a.t.nu_hi[j0 + g];  // table is padded past n
+        nu_lo[g] = a.t.nu_lo[j0 + g];
+    }
+    const float dnu = a.t.dnu;
+    const float* fcol = a.f + (size_t)b * H * W + xc;
+    const double inv = 1.0 / (double)(2 * radius + 1);
+    double acc[NP];
+    float u[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) acc[p] = 0.0;
+    for (long long kk = -radius; kk <= radius; ++kk) {
+        modulate<G, R>(__ldg(fcol + (size_t)mirror_any(kk, H) * W), nu_hi, nu_lo, dnu, u);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) acc[p] += (double)u[p];
+    }
+    const size_t fl_plane = (size_t)a.B * W * H;
+    float* fl_base = a.floc + ((size_t)(j0 * 4) * a.B + b) * W * (size_t)H;
+    for (int i0 = 0; i0 < H; i0 += TILE) {
+        const int i1 = min(i0 + TILE, H);
+        for (int i = i0; i < i1; ++i) {
+            if (i > 0) {
+                float un[NP], uo[NP];
+                modulate<G, R>(__ldg(fcol + (size_t)mirror_any((long long)i + radius, H) * W), nu_hi,
+                            nu_lo, dnu, un);
+                modulate<G, R>(__ldg(fcol + (size_t)mirror_any((long long)i - radius - 1, H) * W),
+                            nu_hi, nu_lo, dnu, uo);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) acc[p] += (double)un[p] - (double)uo[p];
+            }
+#pragma unroll
+            for (int p = 0; p < NP; ++p)
+                buf[(p * TILE + (i - i0)) * BUF_LD + lane] = radius == 0 ? 0.f : (float)(acc[p] * inv);
+            if (radius == 0) {
+                modulate<G, R>(__ldg(fcol + (size_t)i * W), nu_hi, nu_lo, dnu, u);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) buf[(p * TILE + (i - i0)) * BUF_LD + lane] = u[p];
+            }
+        }
+        __syncwarp();
+        const int i = i0 + lane;
+        if (i < i1) {
+            for (int xx = 0; xx < tlen; ++xx) {
+#pragma unroll
+                for (int p = 0; p < NP; ++p)
+                    if (p / 4 < nt)
+                        fl_base[(size_t)p * fl_plane + (size_t)(x0 + xx) * H + i] =
+                            buf[(p * TILE + lane) * BUF_LD + xx];
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <int G, int R>
+__global__ void __launch_bounds__(P2_THREADS) k_pass2_box(const __grid_constant__ Pass2Args a, int radius) {
+    constexpr int NP = 4 * G;
+    const int i_raw = blockIdx.x * P2_THREADS + threadIdx.x;
+    const int H = a.H, W = a.W;
+    const bool iv = i_raw < H;
+    const int i = iv ? i_raw : H - 1;
+    const int grp = blockIdx.y;
+    const int b = blockIdx.z;
+    const int j0 = grp * G;
+    const int nt = min(G, a.t.n - j0);
+    float nu_hi[G], nu_lo[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        nu_hi[g] = a.t.nu_hi[j0 + g];  // table is padded past n
+        nu_lo[g] = a.t.nu_lo[j0 + g];
+    }
+    const float dnu = a.t.dnu;
+    float wt[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) wt[g] = g < nt ? a.t.w[j0 + g] : 0.f;
+    const size_t plane = (size_t)a.B * W * H;
+    const float* fl = a.floc + ((size_t)(j0 * 4) * a.B + b) * W * (size_t)H + i;
+    const float* fT = a.fT + (size_t)b * W * H + i;
+    float* pn = a.part + ((size_t)(grp * 2 + 0) * a.B + b) * W * (size_t)H + i_raw;
+    float* pd = a.part + ((size_t)(grp * 2 + 1) * a.B + b) * W * (size_t)H + i_raw;
+    const double inv = 1.0 / (double)(2 * radius + 1);
+    double acc[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) acc[p] = 0.0;
+    if (radius > 0) {
+        for (long long kk = -radius; kk <= radius; ++kk) {
+            const size_t off = (size_t)mirror_any(kk, W) * H;
+#pragma unroll
+            for (int p = 0; p < NP; ++p)
+                if (p / 4 < nt) acc[p] += (double)fl[(size_t)p * plane + off];
+        }
+    }
+    for (int xx = 0; xx < W; ++xx) {
+        float yo[NP];
+        if (radius > 0) {
+            if (xx > 0) {
+                const size_t on = (size_t)mirror_any((long long)xx + radius, W) * H;
+                const size_t oo = (size_t)mirror_any((long long)xx - radius - 1, W) * H;
+#pragma unroll
+                for (int p = 0; p < NP; ++p)
+                    if (p / 4 < nt)
+                        acc[p] += (double)fl[(size_t)p * plane + on] - (double)fl[(size_t)p * plane + oo];
+            }
+#pragma unroll
+            for (int p = 0; p < NP; ++p) yo[p] = (float)(acc[p] * inv);
+        } else {
+#pragma unroll
+            for (int p = 0; p < NP; ++p)
+                yo[p] = p / 4 < nt ? fl[(size_t)p * plane + (size_t)xx * H] : 0.f;
+        }
+        float cc[G], sn[G];
+        phasors<G, R>(fT[(size_t)xx * H], nu_hi, nu_lo, dnu, cc, sn);
+        float num = 0.f, den = 0.f;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            num = fmaf(wt[g], fmaf(cc[g], yo[4 * g + 2], sn[g] * yo[4 * g + 3]), num);
+            den = fmaf(wt[g], fmaf(cc[g], yo[4 * g + 0], sn[g] * yo[4 * g + 1]), den);
+        }
+        if (iv) {
+            pn[(size_t)xx * H] = num;
+            pd[(size_t)xx * H] = den;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Reduce partial groups, transpose to row-major, optional guarded ratio.
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) k_reduce(const __grid_constant__ ReduceArgs a) {
+    __shared__ float tn[TILE][TILE + 1];
+    __shared__ float td[TILE][TILE + 1];
+    const int b = blockIdx.z;
+    const int x0 = blockIdx.x * TILE, i0 = blockIdx.y * TILE;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
+    const size_t plane = (size_t)a.B * a.W * a.H;
+    // read partials in [x][i] orientation (coalesced over i)
+    for (int r = ty; r < TILE; r += 8) {
+        const int gx = x0 + r, gi = i0 + tx;
+        float n = 0.f, d = 0.f;
+        if (gx < a.W && gi < a.H) {
+            const size_t off = ((size_t)b * a.W + gx) * a.H + gi;
+            for (int g = 0; g < a.ngroups; ++g) {
+                n += a.part[(size_t)(2 * g) * plane + off];
+                d += a.part[(size_t)(2 * g + 1) * plane + off];
+            }
+        }
+        tn[r][tx] = n;
+        td[r][tx] = d;
+    }
+    __syncthreads();
+    unsigned long long guarded = 0;
+    for (int r = ty; r < TILE; r += 8) {
+        const int gi = i0 + r, gx = x0 + tx;
+        if (gi < a.H && gx < a.W) {
+            const size_t off = ((size_t)b * a.H + gi) * a.W + gx;
+            float n = tn[tx][r], d = td[tx][r];
+            if (a.in_num) {
+                n += a.in_num[off];
+                d += a.in_den[off];
+            }
+            if (a.num) {
+                a.num[off] = n;
+                a.den[off] = d;
+            }
+            if (a.out) {
+                bool gd = !(d >= 1e-12f);
+                guarded += gd;
+                a.out[off] = gd ? a.f[off] : n / d;
+            }
+        }
+    }
+    if (a.out && a.counters) {
+        // warp-aggregate then one atomic per warp (integer -> deterministic total)
+        for (int o = 16; o > 0; o >>= 1) guarded += __shfl_down_sync(0xffffffffu, guarded, o);
+        if (tx == 0 && guarded) atomicAdd(&a.counters[1], guarded);
+    }
+}
+
+__global__ void k_finalize(const float* num, const float* den, const float* f, float* out,
+                           long long n, unsigned long long* counters) {
+    unsigned long long guarded = 0;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        float d = den[idx];
+        bool gd = !(d >= 1e-12f);
+        guarded += gd;
+        out[idx] = gd ? f[idx] : num[idx] / d;
+    }
+    for (int o = 16; o > 0; o >>= 1) guarded += __shfl_down_sync(0xffffffffu, guarded, o);
+    if ((threadIdx.x & 31) == 0 && guarded && counters) atomicAdd(&counters[1], guarded);
+}
+
+__global__ void k_range_check(const float* f, long long n, double lo, double hi,
+                              unsigned long long* counters) {
+    unsigned long long bad = 0;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        double v = (double)f[idx];
+        bad += !(v >= lo && v <= hi);  // NaN counts as bad
+    }
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_down_sync(0xffffffffu, bad, o);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&counters[0], bad);
+}
+
+// f[b][i][x] -> fT[b][x][i]
+__global__ void __launch_bounds__(256) k_transpose(const float* f, float* fT, int H, int W) {
+    __shared__ float t[TILE][TILE + 1];
+    const int b = blockIdx.z;
+    const int x0 = blockIdx.x * TILE, i0 = blockIdx.y * TILE;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const float* src = f + (size_t)b * H * W;
+    float* dst = fT + (size_t)b * H * W;
+    for (int r = ty; r < TILE; r += 8) {
+        int gi = i0 + r, gx = x0 + tx;
+        t[r][tx] = (gi < H && gx < W) ? src[(size_t)gi * W + gx] : 0.f;
+    }
+    __syncthreads();
+    for (int r = ty; r < TILE; r += 8) {
+        int gx = x0 + r, gi = i0 + tx;
+        if (gx < W && gi < H) dst[(size_t)gx * H + gi] = t[tx][r];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Plugin-level fp64 twins of _core.recursive_smooth / _core.box_pass.
+// ---------------------------------------------------------------------------
+
+__global__ void k_recursive_smooth_f64(const double* a, double* out, int h, int w, double scale,
+                                       double c1, double c2, double c3, double c4, int pad,
+                                       double* s) {
+    const int xcol = blockIdx.x * blockDim.x + threadIdx.x;
+    if (xcol >= w) return;
+    const long long ext = (long long)h + 2LL * pad;
+    auto S = [&](long long r) -> double& { return s[r * w + xcol]; };
+    const double a0 = a[mirror_any(-pad, h) * w + xcol];
+    for (int r = 0; r < 4; ++r) S(r) = a0;
+    for (long long r = 0; r < ext; ++r) {
+        const long long src = mirror_any(r - pad, h);
+        S(r + 4) = scale * a[src * w + xcol] + c1 * S(r + 3) + c2 * S(r + 2) + c3 * S(r + 1) +
+                   c4 * S(r);
+    }
+    for (long long r = ext + 4; r < ext + 8; ++r) S(r) = S(ext + 3);
+    for (long long r = ext - 1; r >= 0; --r)
+        S(r + 4) = scale * S(r + 4) + c1 * S(r + 5) + c2 * S(r + 6) + c3 * S(r + 7) + c4 * S(r + 8);
+    for (int r = 0; r < h; ++r) out[(long long)r * w + xcol] = S(pad + r + 4);
+}
+
+__global__ void k_box_pass_f64(const double* a, double* out, int h, int w, int radius) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= h) return;
+    const double* ar = a + (long long)row * w;
+    double* orow = out + (long long)row * w;
+    if (radius == 0) {
+        for (int j = 0; j < w; ++j) orow[j] = ar[j];
+        return;
+    }
+    // Kahan-compensated running sum (the reference keeps long double)
+    double acc = 0.0, comp = 0.0;
+    auto add = [&](double v) {
+        double y = v - comp;
+        double t = acc + y;
+        comp = (t - acc) - y;
+        acc = t;
+    };
+    for (long long k = -radius; k <= radius; ++k) add(ar[mirror_any(k, w)]);
+    const double inv = 1.0 / (double)(2 * radius + 1);
+    orow[0] = acc * inv;
+    for (int j = 1; j < w; ++j) {
+        add(ar[mirror_any((long long)j + radius, w)]);
+        add(-ar[mirror_any((long long)j - radius - 1, w)]);
+        orow[j] = acc * inv;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Host side: plan, workspace layout, launches.
+// ---------------------------------------------------------------------------
+
+constexpr int G1 = 1;  // terms per pass-1 warp == phasor anchor block R
+constexpr int G2 = 2;  // terms per pass-2 thread (multiple of G1)
+constexpr int R_ANCHOR = G1;
+constexpr int TAB_PAD = 16;  // zero padding past the last term of the table
+
+size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
+
+struct Layout {
+    int B, H, W, Ey, Ex, nseg, ntx, ne, edge_all;
+    int tb;  // terms per batch (multiple of G2)
+    int ng2; // pass-2 groups per batch
+    size_t off_fT, off_ckpt, off_floc, off_lc, off_edge, off_ext, off_bst, off_part, off_num,
+        off_den, off_tab, total;
+};
+
+int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, int batch_terms,
+                Layout* L) {
+    if (B < 1 || H < 1 || W < 1) return fail(TBF_ERR_DIM, "bad shape B=%d H=%d W=%d", B, H, W);
+    if (!sp) return fail(TBF_ERR_PARAM, "null spatial");
+    L->B = B;
+    L->H = H;
+    L->W = W;
+    const bool box = sp->kind == TBF_SPATIAL_BOX;
+    L->Ey = box ? 0 : std::max(0, std::min(sp->ext_y, H - 1));
+    L->Ex = box ? 0 : std::max(0, std::min(sp->ext_x, W - 1));
+    L->nseg = (H + L->Ey + TILE - 1) / TILE;
+    L->ntx = (W + TILE - 1) / TILE;
+    L->edge_all = 2 * (L->Ex + 1) >= W;
+    L->ne = L->edge_all ? W : 2 * (L->Ex + 1);
+    int tb = batch_terms > 0 ? std::min(batch_terms, nterms_range) : nterms_range;
+    tb = std::max(tb, 1);
+    tb = (tb + G2 - 1) / G2 * G2;  // whole groups, so anchors stay aligned across batches
+    L->tb = tb;
+    L->ng2 = tb / G2;
+    const size_t px = (size_t)B * H * W;
+    size_t o = 0;
+    L->off_fT = o;
+    o = align_up(o + px * 4);
+    L->off_ckpt = o;
+    if (!box) o = align_up(o + (size_t)L->nseg * tb * 16 * B * W * 4);
+    L->off_floc = o;
+    o = align_up(o + (size_t)tb * 4 * px * 4);
+    L->off_lc = o;
+    if (!box) o = align_up(o + (size_t)tb * 16 * B * L->ntx * H * 4);
+    L->off_edge = o;
+    if (!box) o = align_up(o + (size_t)tb * 4 * B * L->ne * H * 4);
+    L->off_ext = o;
+    if (!box) o = align_up(o + (size_t)tb * 4 * B * L->Ex * H * 4);
+    L->off_bst = o;
+    if (!box) o = align_up(o + (size_t)tb * 16 * B * H * 4);
+    L->off_part = o;
+    o = align_up(o + (size_t)L->ng2 * 2 * px * 4);
+    const bool multi = tb < nterms_range;
+    L->off_num = o;
+    if (multi) o = align_up(o + px * 4);
+    L->off_den = o;
+    if (multi) o = align_up(o + px * 4);
+    L->off_tab = o;
+    o = align_up(o + (size_t)3 * (nterms_range + TAB_PAD) * 4);
+    L->total = o;
+    return TBF_OK;
+}
+
+// Zero-input evolution of the cascade: state s=(v1,v2,y1,y2) after `steps`
+// samples (M, column-major) and the output y at each step (Hm).
+void cascade_responses(const tbf_spatial* sp, int steps, double M[16], double (*Hm)[4]) {
+    for (int kk = 0; kk < 4; ++kk) {
+        double s[4] = {0, 0, 0, 0};
+        s[kk] = 1.0;
+        double v1 = s[0], v2 = s[1], y1 = s[2], y2 = s[3];
+        for (int m = 0; m < steps; ++m) {
+            double v = sp->a1 * v1 + sp->a2 * v2;
+            v2 = v1;
+            v1 = v;
+            double y = sp->g2 * v + sp->b1 * y1 + sp->b2 * y2;
+            y2 = y1;
+            y1 = y;
+            if (Hm) Hm[m][kk] = y;
+        }
+        M[kk * 4 + 0] = v1;
+        M[kk * 4 + 1] = v2;
+        M[kk * 4 + 2] = y1;
+        M[kk * 4 + 3] = y2;
+    }
+}
+
+Casc to_casc(const tbf_spatial* sp) {
+    return Casc{(float)sp->g1, (float)sp->a1, (float)sp->a2,
+                (float)sp->g2, (float)sp->b1, (float)sp->b2};
+}
+
+int validate(const tbf_spatial* sp, const tbf_terms* terms, int tbeg, int tend) {
+    if (!sp || !terms) return fail(TBF_ERR_PARAM, "null spatial/terms");
+    if (sp->kind != TBF_SPATIAL_RECURSIVE && sp->kind != TBF_SPATIAL_BOX)
+        return fail(TBF_ERR_PARAM, "unknown spatial kind %d", sp->kind);
+    if (sp->kind == TBF_SPATIAL_BOX && sp->radius < 0)
+        return fail(TBF_ERR_PARAM, "box radius must be >= 0, got %d", sp->radius);
+    if (terms->n_terms < 1 || !terms->nu || !terms->weight)
+        return fail(TBF_ERR_PARAM, "no terms");
+    if (tbeg < 0 || tend > terms->n_terms || tbeg >= tend)
+        return fail(TBF_ERR_PARAM, "bad term range [%d,%d) of %d", tbeg, tend, terms->n_terms);
+    return TBF_OK;
+}
+
+constexpr int P1_SMEM = P1_WARPS * 4 * G1 * TILE * BUF_LD * 4;
+
+void set_p1_smem() {
+    static bool done = false;
+    if (done) return;
+    cudaFuncSetAttribute(k_pass1_gauss<G1, R_ANCHOR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         P1_SMEM);
+    cudaFuncSetAttribute(k_pass1_box<G1, R_ANCHOR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         P1_SMEM);
+    done = true;
+}
+
+// Core driver: pairs [tbeg, tend) in batches of L.tb terms.  Either
+// accumulates into caller num/den (row-major), or (out != null) writes the
+// guarded ratio.
+int run_terms(const float* f, float* num, float* den, float* out, int B, int H, int W,
+              const tbf_spatial* sp, const tbf_terms* terms, int tbeg, int tend, int batch_terms,
+              int accumulate, void* ws, size_t ws_bytes, unsigned long long* counters,
+              cudaStream_t st) {
+    int rc = validate(sp, terms, tbeg, tend);
+    if (rc) return rc;
+    const int nrange = tend - tbeg;
+    Layout L;
+    rc = make_layout(B, H, W, sp, nrange, batch_terms, &L);
+    if (rc) return rc;
+    if (!ws || ws_bytes < L.total)
+        return fail(TBF_ERR_WORKSPACE, "workspace too small: need %zu have %zu", L.total, ws_bytes);
+    char* w8 = (char*)ws;
+    float* fT = (float*)(w8 + L.off_fT);
+    float* ckpt = (float*)(w8 + L.off_ckpt);
+    float* floc = (float*)(w8 + L.off_floc);
+    float* lc = (float*)(w8 + L.off_lc);
+    float* edge = (float*)(w8 + L.off_edge);
+    float* ext = (float*)(w8 + L.off_ext);
+    float* bst = (float*)(w8 + L.off_bst);
+    float* part = (float*)(w8 + L.off_part);
+    float* tab = (float*)(w8 + L.off_tab);
+    const bool box = sp->kind == TBF_SPATIAL_BOX;
+    const int nb = (nrange + L.tb - 1) / L.tb;
+    if (out && nb > 1) {  // accumulate batches in workspace num/den, ratio at the end
+        num = (float*)(w8 + L.off_num);
+        den = (float*)(w8 + L.off_den);
+        accumulate = 0;
+    }
+
+    // term tables: nu split hi/lo, float weights; zero padded past the end
+    const int ld = nrange + TAB_PAD;
+    std::vector<float> h_tab((size_t)3 * ld, 0.f);
+    for (int j = 0; j < nrange; ++j) {
+        double nu = terms->nu[tbeg + j];
+        float hi = (float)nu;
+        h_tab[j] = hi;
+        h_tab[ld + j] = (float)(nu - (double)hi);
+        h_tab[2 * ld + j] = (float)terms->weight[tbeg + j];
+    }
+    cudaMemcpyAsync(tab, h_tab.data(), h_tab.size() * 4, cudaMemcpyHostToDevice, st);
+
+    dim3 tgrid((W + TILE - 1) / TILE, (H + TILE - 1) / TILE, B);
+    k_transpose<<<tgrid, 256, 0, st>>>(f, fT, H, W);
+    if ((rc = check_cuda("transpose"))) return rc;
+
+    set_p1_smem();
+    const Casc kc = to_casc(sp);
+    double M[16], Mlast[16], Hm[TILE][4];
+    if (!box) {
+        cascade_responses(sp, TILE, M, Hm);
+        cascade_responses(sp, W - (L.ntx - 1) * TILE, Mlast, nullptr);
+    }
+
+    for (int bi = 0; bi < nb; ++bi) {
+        const int jb = bi * L.tb;
+        const int n = std::min(L.tb, nrange - jb);
+        TermDev td;
+        td.nu_hi = tab + jb;
+        td.nu_lo = tab + ld + jb;
+        td.w = tab + 2 * ld + jb;
+        td.dnu = (float)terms->dnu;
+        td.n = n;
+        td.anchor = R_ANCHOR;
+
+        Pass1Args p1;
+        p1.f = f;
+        p1.B = B;
+        p1.H = H;
+        p1.W = W;
+        p1.Ey = L.Ey;
+        p1.nseg = L.nseg;
+        p1.Ex = L.Ex;
+        p1.ne = L.ne;
+        p1.edge_all = L.edge_all;
+        p1.ntx = L.ntx;
+        p1.k = kc;
+        p1.t = td;
+        p1.ngroups = (n + G1 - 1) / G1;
+        p1.ckpt = ckpt;
+        p1.floc = floc;
+        p1.lcarry = lc;
+        p1.edge = edge;
+        dim3 g1((W + TILE - 1) / TILE, (p1.ngroups + P1_WARPS - 1) / P1_WARPS, B);
+        if (box)
+            k_pass1_box<G1, R_ANCHOR><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1, sp->radius);
+        else
+            k_pass1_gauss<G1, R_ANCHOR><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1);
+        if ((rc = check_cuda("pass1"))) return rc;
+
+        if (!box) {
+            ChainArgs ca;
+            ca.B = B;
+            ca.H = H;
+            ca.W = W;
+            ca.Ex = L.Ex;
+            ca.ne = L.ne;
+            ca.edge_all = L.edge_all;
+            ca.ntx = L.ntx;
+            ca.k = kc;
+            ca.nplanes = n * 4;
+            for (int q = 0; q < 16; ++q) {
+                ca.M[q] = (float)M[q];
+                ca.Mlast[q] = (float)Mlast[q];
+            }
+            ca.edge = edge;
+            ca.lcarry = lc;
+            ca.extbuf = ext;
+            ca.bstate = bst;
+            dim3 gc((H + 127) / 128, n * 4 * B);
+            k_chain<<<gc, 128, 0, st>>>(ca);
+            if ((rc = check_cuda("chain"))) return rc;
+        }
+
+        Pass2Args p2;
+        p2.fT = fT;
+        p2.B = B;
+        p2.H = H;
+        p2.W = W;
+        p2.ntx = L.ntx;
+        p2.k = kc;
+        p2.t = td;
+        p2.ngroups = (n + G2 - 1) / G2;
+        for (int m = 0; m < TILE; ++m)
+            for (int q = 0; q < 4; ++q) p2.Hm[m][q] = box ? 0.f : (float)Hm[m][q];
+        p2.floc = floc;
+        p2.carry = lc;
+        p2.bstate = bst;
+        p2.part = part;
+        dim3 g2((H + P2_THREADS - 1) / P2_THREADS, p2.ngroups, B);
+        if (box)
+            k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, st>>>(p2, sp->radius);
+        else
+            k_pass2_gauss<G2, R_ANCHOR><<<g2, P2_THREADS, 0, st>>>(p2);
+        if ((rc = check_cuda("pass2"))) return rc;
+
+        ReduceArgs ra;
+        ra.part = part;
+        ra.ngroups = p2.ngroups;
+        ra.B = B;
+        ra.H = H;
+        ra.W = W;
+        ra.f = f;
+        ra.counters = counters;
+        const bool add = bi > 0 || (accumulate && !out);
+        ra.in_num = add ? num : nullptr;
+        ra.in_den = add ? den : nullptr;
+        const bool last = bi == nb - 1;
+        if (out && last) {
+            ra.num = nullptr;
+            ra.den = nullptr;
+            ra.out = out;
+        } else {
+            ra.num = num;
+            ra.den = den;
+            ra.out = nullptr;
+        }
+        k_reduce<<<tgrid, 256, 0, st>>>(ra);
+        if ((rc = check_cuda("reduce"))) return rc;
+    }
+    return TBF_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+int32_t tbf_abi_version(void) { return TBF_ABI_VERSION; }
+
+const char* tbf_last_error(void) { return g_last_error.c_str(); }
+
+size_t tbf_workspace_bytes(int32_t B, int32_t H, int32_t W, const tbf_spatial* sp,
+                           int32_t term_begin, int32_t term_end, int32_t batch_terms) {
+    Layout L;
+    if (term_end <= term_begin) return 0;
+    if (make_layout(B, H, W, sp, term_end - term_begin, batch_terms, &L)) return 0;
+    return L.total;
+}
+
+int tbf_range_check(const float* f, int64_t count, double T, unsigned long long* d_counters,
+                    void* stream) {
+    if (count <= 0) return fail(TBF_ERR_DIM, "empty input");
+    if (!d_counters) return fail(TBF_ERR_PARAM, "null counters");
+    cudaStream_t st = (cudaStream_t)stream;
+    long long blocks = std::min<long long>((count + 255) / 256, 148LL * 8);
+    k_range_check<<<(unsigned)blocks, 256, 0, st>>>(f, count, -1e-9, T + 1e-9, d_counters);
+    return check_cuda("range_check");
+}
+
+int tbf_bilateral_trig(const float* f, float* out, int32_t B, int32_t H, int32_t W,
+                       const tbf_spatial* sp, const tbf_terms* terms, int32_t batch_terms,
+                       void* workspace, size_t workspace_bytes, unsigned long long* d_counters,
+                       void* stream) {
+    if (!terms) return fail(TBF_ERR_PARAM, "null terms");
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc;
+    if (d_counters) {
+        rc = tbf_range_check(f, (int64_t)B * H * W, terms->T, d_counters, stream);
+        if (rc) return rc;
+    }
+    return run_terms(f, nullptr, nullptr, out, B, H, W, sp, terms, 0, terms->n_terms, batch_terms,
+                     0, workspace, workspace_bytes, d_counters, st);
+}
+
+int tbf_trig_partial(const float* f, float* num, float* den, int32_t B, int32_t H, int32_t W,
+                     const tbf_spatial* sp, const tbf_terms* terms, int32_t term_begin,
+                     int32_t term_end, int32_t batch_terms, int32_t accumulate, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+    if (!num || !den) return fail(TBF_ERR_PARAM, "null num/den");
+    return run_terms(f, num, den, nullptr, B, H, W, sp, terms, term_begin, term_end, batch_terms,
+                     accumulate, workspace, workspace_bytes, nullptr, (cudaStream_t)stream);
+}
+
+int tbf_finalize(const float* num, const float* den, const float* f, float* out, int64_t count,
+                 unsigned long long* d_counters, void* stream) {
+    if (count <= 0) return fail(TBF_ERR_DIM, "empty input");
+    long long blocks = std::min<long long>((count + 255) / 256, 148LL * 8);
+    k_finalize<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(num, den, f, out, count,
+                                                                   d_counters);
+    return check_cuda("finalize");
+}
+
+int tbf_recursive_smooth_f64(const double* a, double* out, int32_t h, int32_t w, double scale,
+                             double c1, double c2, double c3, double c4, int32_t pad,
+                             double* scratch, void* stream) {
+    if (h < 1 || w < 1) return fail(TBF_ERR_DIM, "bad shape %dx%d", h, w);
+    if (pad < 0) return fail(TBF_ERR_PARAM, "pad must be >= 0");
+    k_recursive_smooth_f64<<<(w + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
+        a, out, h, w, scale, c1, c2, c3, c4, pad, scratch);
+    return check_cuda("recursive_smooth_f64");
+}
+
+int tbf_box_pass_f64(const double* a, double* out, int32_t h, int32_t w, int32_t radius,
+                     void* stream) {
+    if (h < 1 || w < 1) return fail(TBF_ERR_DIM, "bad shape %dx%d", h, w);
+    if (radius < 0) return fail(TBF_ERR_PARAM, "box radius must be >= 0, got %d", radius);
+    k_box_pass_f64<<<(h + 127) / 128, 128, 0, (cudaStream_t)stream>>>(a, out, h, w, radius);
+    return check_cuda("box_pass_f64");
+}
+
+}  // extern "C"
