@@ -1,0 +1,434 @@
+"""Benchmark: output Mpixel/s of the B200 trigonometric bilateral filter.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl mine|reference]
+
+One JSON line on rank 0.  A step is one full
+``bilateral_trig`` over the configuration's input (range check, all terms,
+guarded ratio) with the input resident in HBM; L2 is flushed before every
+timed step (a 512 MiB write, 4x the 126 MB L2) outside the step's events.
+
+Configs (BASELINE.json, workloads.CONFIGS): default 2 (configs[1], 2048^2,
+sigma_s=8, sigma_r=20, N=66).  Multi-GPU: configs 1-3 run replicas (weak
+scaling), config 4 splits its 64 frames across ranks, config 5 splits the
+frequency terms and sums num/den with an NCCL reduce (strong scaling).
+
+--impl reference times the reference's own CPU implementation (the trigbf
+package built from /root/reference into oracle/_ref, compiled core) on the
+host cores, on a bounded crop of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1105_4204_b200 import workloads  # noqa: E402
+from paper_1105_4204_b200.kernels import make_trig_kernel, term_pairs  # noqa: E402
+
+METRIC = "output Mpixel/s at fixed (sigma_s, sigma_r, N); achieved HBM GB/s vs B200 peak"
+UNIT = "Mpixel/s"
+REF_PATH = os.path.join(ROOT, "oracle", "_ref")
+
+
+def algorithmic_bytes_per_px(pairs) -> int:
+    """8 + 32 P + 8 z bytes per output pixel."""
+    z = 1 if pairs.has_zero else 0
+    p = pairs.count - z
+    return 8 + 32 * p + 8 * z
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/tbf_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+        return False
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        try:
+            with open(self.path) as fh:
+                for line in fh:
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        busy = [v for v in sm if smax and v > 0.3 * max(smax)] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# reference (CPU) arm
+# ---------------------------------------------------------------------------
+
+def _ref_module():
+    if os.path.isdir(os.path.join(REF_PATH, "trigbf")):
+        if REF_PATH not in sys.path:
+            sys.path.insert(0, REF_PATH)
+        import trigbf
+
+        return trigbf, "reference"
+    from oracle import trigbf_oracle
+
+    return trigbf_oracle, "port"
+
+
+def _ref_crop_job(args):
+    cfg_id, side, seed_off, workers = args
+    cfg = workloads.CONFIGS[cfg_id]
+    trigbf, kind = _ref_module()
+    f = workloads.frame(cfg, 0)
+    y0 = (seed_off * 97) % max(1, cfg.height - side + 1)
+    x0 = (seed_off * 131) % max(1, cfg.width - side + 1)
+    crop = np.ascontiguousarray(f[y0:y0 + side, x0:x0 + side], dtype=np.float64)
+    t = time.perf_counter()
+    if kind == "reference":
+        k = trigbf.make_trig_kernel(cfg.sigma_r, cfg.T)
+        trigbf.bilateral_trig(trigbf.Image(crop.shape[1], crop.shape[0], 1, crop[None]),
+                              trigbf.SpatialSpec.gaussian_recursive(cfg.sigma_s), k, workers=workers)
+    else:
+        trigbf.bilateral_trig(crop, "gauss-recursive", cfg.sigma_s,
+                              trigbf.make_trig_kernel(cfg.sigma_r, cfg.T))
+    return crop.size, time.perf_counter() - t
+
+
+def reference_sample(cfg_id: int, budget_s: float, procs: int):
+    """Time the reference on crops of the workload with `procs` processes
+    (workers=1 each) -- about `budget_s` seconds of CPU work.  Returns
+    (Mpx/s, description, kind, cores)."""
+    from concurrent.futures import ProcessPoolExecutor
+
+    cfg = workloads.CONFIGS[cfg_id]
+    _, kind = _ref_module()
+    n_terms = term_pairs(make_trig_kernel(cfg.sigma_r, cfg.T)).spatial_passes
+    # calibrate: reference ~ 30 ns per pixel per spatial pass (compiled core)
+    per_px = 30e-9 * n_terms * (1.0 if kind == "reference" else 6.0)
+    side = int(math.sqrt(max(64 * 64, budget_s / per_px)))
+    side = max(64, min(side, cfg.height, cfg.width, 2048))
+    jobs = [(cfg_id, side, i, 1) for i in range(procs)]
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(max_workers=procs) as pool:
+        res = list(pool.map(_ref_crop_job, jobs))
+    wall = time.perf_counter() - t0
+    px = sum(r[0] for r in res)
+    desc = (f"{procs} x {side}x{side} crop(s) of config {cfg_id} (sigma_s={cfg.sigma_s}, "
+            f"sigma_r={cfg.sigma_r}, N={make_trig_kernel(cfg.sigma_r, cfg.T).N}), one process "
+            f"per core, workers=1 each; per-pixel cost is size-independent (O(1) filter)")
+    return px / wall / 1e6, desc, kind, procs
+
+
+def run_reference_arm(args, rank: int):
+    if rank != 0:
+        return
+    cfg = workloads.CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    steps, warmup = args.steps, args.warmup
+    budget = max(2.0, 150.0 / max(1, steps + warmup))
+    vals = []
+    desc = kind = None
+    for i in range(warmup + steps):
+        v, desc, kind, used = reference_sample(args.config, budget, cores)
+        if i >= warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
+        "ms_per_step": cfg.pixels / (value * 1e6) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "shape": [cfg.frames, cfg.height, cfg.width],
+                   "sigma_s": cfg.sigma_s, "sigma_r": cfg.sigma_r,
+                   "N": make_trig_kernel(cfg.sigma_r, cfg.T).N},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU baseline work")
+    ap.add_argument("--flush-mb", type=int, default=512)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1105_4204_b200 as tb
+    from paper_1105_4204_b200 import _native
+    from paper_1105_4204_b200.distributed import frame_range, term_range
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    cfg = workloads.CONFIGS[args.config]
+    kernel = make_trig_kernel(cfg.sigma_r, cfg.T)
+    pairs = term_pairs(kernel)
+    spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
+
+    # ---- partition ----
+    mode = "replica"
+    f0, f1 = 0, cfg.frames
+    t0, t1 = 0, pairs.count
+    if world > 1 and args.config == 4:
+        mode = "frames"
+        f0, f1 = frame_range(cfg.frames, world, rank)
+    elif world > 1 and args.config == 5:
+        mode = "terms"
+        t0, t1 = term_range(pairs.count, pairs.has_zero, world, rank)
+    host = np.empty((f1 - f0, cfg.height, cfg.width), dtype=np.float32)
+    for i in range(f0, f1):
+        host[i - f0] = workloads.frame(cfg, i)
+    f = torch.from_numpy(host).to(dev)
+    px_rank = f.numel()
+    px_job = cfg.pixels * (world if mode == "replica" else 1)
+
+    if mode == "terms":
+        plan = tb.TrigFilter(tuple(f.shape), spec, kernel, term_range=(t0, t1)) if t1 > t0 else None
+        fin = plan if plan is not None else tb.TrigFilter(tuple(f.shape), spec, kernel)
+        num = torch.zeros_like(f)
+        den = torch.zeros_like(f)
+        out = torch.empty_like(f)
+
+        def step():
+            fin.range_check(f)
+            if plan is not None:
+                plan.partial(f, num, den, accumulate=False)
+            else:
+                num.zero_()
+                den.zero_()
+            dist.reduce(num, dst=0)
+            dist.reduce(den, dst=0)
+            if rank == 0:
+                fin.finalize(num, den, f, out)
+        counters_plan = fin
+    else:
+        plan = tb.TrigFilter(tuple(f.shape), spec, kernel)
+        out = torch.empty_like(f)
+
+        def step():
+            plan(f, out)
+        counters_plan = plan
+
+    flush = torch.empty(args.flush_mb * (1 << 20) // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    bad, guarded = counters_plan.read_counters()
+
+    # ---- timed region ----
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize(dev)
+        wall0 = time.perf_counter()
+        with _native.KernelProfiler() as prof:
+            for i in range(args.steps):
+                flush.zero_()
+                evs[i][0].record(stream)
+                step()
+                evs[i][1].record(stream)
+            torch.cuda.synchronize(dev)
+        barrier()
+        wall = time.perf_counter() - wall0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    t_rank = sum(step_ms) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_rank], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_job = float(tt.item())
+    else:
+        t_job = t_rank
+    bad2, guarded2 = counters_plan.read_counters()
+    if bad or bad2:
+        raise SystemExit(f"range violations in benchmark input: {bad + bad2}")
+
+    value = px_job * args.steps / t_job / 1e6
+    ms_per_step = t_job / args.steps * 1e3
+
+    # ---- roofline: dominant kernel, live per-kernel event timing ----
+    peak, peak_kind = measured_peaks()
+    kt = prof.result
+    dom = max(kt, key=lambda k: kt[k][0]) if kt else None
+    nz = pairs.count - (1 if pairs.has_zero else 0)
+    n_shard = t1 - t0
+    nz_shard = n_shard - (1 if (pairs.has_zero and t0 == 0 and n_shard > 0) else 0)
+    z_shard = n_shard - nz_shard
+    round_trip = 16 * nz_shard + 4 * z_shard  # one write (pass1) or one read (pass2) of the planes
+    alg_kernel = {"pass1": (4 + round_trip) * px_rank, "pass2": (4 + round_trip) * px_rank,
+                  "reduce": 8 * px_rank, "transpose": 8 * px_rank, "range_check": 4 * px_rank,
+                  "finalize": 12 * px_rank, "chain": 0}
+    roofline = None
+    if dom is not None:
+        ms_total, launches = kt[dom]
+        avg_s = ms_total / launches / 1e3
+        per_launch = alg_kernel.get(dom, 0) * args.steps / launches
+        ach = per_launch / avg_s / 1e9
+        roofline = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
+                    "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / peak, 4),
+                    "traffic": None, "algorithmic_bytes_per_launch": per_launch,
+                    "avg_launch_ms": round(avg_s * 1e3, 4)}
+        prof_path = os.path.join(ROOT, "profiles", f"ncu_traffic_cfg{args.config}.json")
+        if os.path.exists(prof_path):
+            try:
+                with open(prof_path) as fh:
+                    tr = json.load(fh)
+                roofline["traffic"] = tr.get(dom)
+            except Exception:
+                pass
+    alg_step = algorithmic_bytes_per_px(pairs) * cfg.pixels * (world if mode == "replica" else 1)
+    pipe_ach = alg_step / (t_job / args.steps) / 1e9
+    pipeline = {"bound": "hbm", "achieved": round(pipe_ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(pipe_ach / peak, 4),
+                "algorithmic_bytes_per_step": alg_step,
+                "model": "8 + 32P + 8z bytes/px (SURVEY.md 8(d))"}
+    kernel_share = {k: {"ms_per_step": round(v[0] / args.steps, 4), "launches": v[1],
+                        "share": round(v[0] / max(1e-9, sum(x[0] for x in kt.values())), 4)}
+                    for k, v in kt.items()}
+    launches_total = sum(v[1] for v in kt.values())
+
+    # ---- e2e through the public API with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e and mode != "terms":
+        pin_in = torch.from_numpy(host).pin_memory()
+        e2e_times = []
+        res = None
+        for i in range(args.warmup + args.steps):
+            torch.cuda.synchronize(dev)
+            t = time.perf_counter()
+            res = tb.bilateral_trig(pin_in, spec, kernel)  # H2D, filter, D2H (+ range check)
+            e2e_times.append(time.perf_counter() - t)
+        tt = sum(e2e_times[args.warmup:])
+        if world > 1:
+            x = torch.tensor([tt], dtype=torch.float64, device=dev)
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+            tt = float(x.item())
+        e2e = {"value": px_job * args.steps / tt / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": int(host.nbytes), "d2h_bytes_per_step": int(res.numel() * 4)}
+        del pin_in
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, desc, kind, cores = reference_sample(args.config, args.cpu_budget, os.cpu_count() or 1)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc}
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": repr(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True,
+            "scaling": "weak" if mode == "replica" else "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "shape": [cfg.frames, cfg.height, cfg.width],
+                       "sigma_s": cfg.sigma_s, "sigma_r": cfg.sigma_r, "T": cfg.T,
+                       "N": kernel.N, "terms": pairs.count, "spatial_passes": pairs.spatial_passes,
+                       "spatial": "gauss-recursive", "parallelism": f"{mode}x{world}",
+                       "l2": f"flushed before each timed step ({args.flush_mb} MiB write, outside the step events)"},
+            "roofline": roofline,
+            "pipeline_roofline": pipeline,
+            "kernels": kernel_share,
+            "gpu_launches": launches_total,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "wall_s_timed_region": round(wall, 4),
+            "guarded_pixels_per_step": guarded2 // max(1, args.steps),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -120,6 +120,15 @@ TBF_API int tbf_recursive_smooth_f64(const double* a, double* out, int32_t h, in
 TBF_API int tbf_box_pass_f64(const double* a, double* out, int32_t h, int32_t w, int32_t radius,
                      void* stream);
 
+/* Per-kernel timing for measurement: when enabled, CUDA events are recorded
+ * on the launch stream around every kernel; collect synchronizes them and
+ * returns summed milliseconds and launch counts per kernel kind (arrays of
+ * tbf_profile_kinds() entries, names from tbf_kernel_name), then resets. */
+TBF_API int tbf_profile_enable(int32_t on);
+TBF_API int32_t tbf_profile_kinds(void);
+TBF_API const char* tbf_kernel_name(int32_t kind);
+TBF_API int tbf_profile_collect(double* ms, long long* launches, int32_t n);
+
 /* Last error message of the calling thread (static storage). */
 TBF_API const char* tbf_last_error(void);
 /* ABI version (bumped on any signature change). */

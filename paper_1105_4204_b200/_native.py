@@ -37,6 +37,10 @@ EXPORTS = (
     "tbf_box_pass_f64",
     "tbf_last_error",
     "tbf_abi_version",
+    "tbf_profile_enable",
+    "tbf_profile_kinds",
+    "tbf_kernel_name",
+    "tbf_profile_collect",
 )
 ABI_VERSION = 1
 
@@ -101,6 +105,14 @@ def _declare(lib):
     lib.tbf_recursive_smooth_f64.argtypes = [
         _vp, _vp, _i32, _i32, _f64, _f64, _f64, _f64, _f64, _i32, _vp, _vp,
     ]
+    lib.tbf_profile_enable.restype = ctypes.c_int
+    lib.tbf_profile_enable.argtypes = [_i32]
+    lib.tbf_profile_kinds.restype = _i32
+    lib.tbf_profile_kinds.argtypes = []
+    lib.tbf_kernel_name.restype = ctypes.c_char_p
+    lib.tbf_kernel_name.argtypes = [_i32]
+    lib.tbf_profile_collect.restype = ctypes.c_int
+    lib.tbf_profile_collect.argtypes = [ctypes.POINTER(_f64), ctypes.POINTER(ctypes.c_longlong), _i32]
     lib.tbf_box_pass_f64.restype = ctypes.c_int
     lib.tbf_box_pass_f64.argtypes = [_vp, _vp, _i32, _i32, _i32, _vp]
 
@@ -134,3 +146,29 @@ def check(rc: int) -> None:
     if rc == TBF_ERR_DIM:
         raise DimensionError(msg)
     raise RuntimeError(f"trigbf_b200 error {rc}: {msg}")
+
+
+class KernelProfiler:
+    """Context manager: per-kernel device time of every launch inside it,
+    measured with CUDA events on the launch stream by the library."""
+
+    def __enter__(self):
+        lib = load()
+        self.lib = lib
+        n = lib.tbf_profile_kinds()
+        self.n = n
+        self.names = [lib.tbf_kernel_name(k).decode() for k in range(n)]
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_longlong * n)()
+        lib.tbf_profile_collect(ms, cnt, n)  # drop anything stale
+        lib.tbf_profile_enable(1)
+        self.result = {}
+        return self
+
+    def __exit__(self, *exc):
+        self.lib.tbf_profile_enable(0)
+        ms = (ctypes.c_double * self.n)()
+        cnt = (ctypes.c_longlong * self.n)()
+        check(self.lib.tbf_profile_collect(ms, cnt, self.n))
+        self.result = {self.names[k]: (float(ms[k]), int(cnt[k])) for k in range(self.n) if cnt[k]}
+        return False

@@ -37,6 +37,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -69,6 +70,54 @@ int check_cuda(const char* what) {
     if (e != cudaSuccess) return fail(TBF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
     return TBF_OK;
 }
+
+// Optional per-kernel timing: CUDA events recorded on the launch stream around
+// every launch (tbf_profile_enable / tbf_profile_collect).
+enum KernelKind {
+    KK_TRANSPOSE = 0, KK_RANGE, KK_PASS1, KK_CHAIN, KK_PASS2, KK_REDUCE, KK_FINALIZE, KK_COUNT
+};
+const char* const kKernelNames[KK_COUNT] = {"transpose", "range_check", "pass1", "chain",
+                                            "pass2", "reduce", "finalize"};
+
+struct ProfRec {
+    int kind;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_ev_pool;
+
+cudaEvent_t ev_get() {
+    if (!g_ev_pool.empty()) {
+        cudaEvent_t e = g_ev_pool.back();
+        g_ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct Prof {
+    int kind;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    Prof(int k, cudaStream_t s) : kind(k), st(s) {
+        std::lock_guard<std::mutex> g(g_prof_mu);
+        if (g_prof_on) {
+            a = ev_get();
+            cudaEventRecord(a, st);
+        }
+    }
+    ~Prof() {
+        if (!a) return;
+        std::lock_guard<std::mutex> g(g_prof_mu);
+        cudaEvent_t b = ev_get();
+        cudaEventRecord(b, st);
+        g_prof.push_back({kind, a, b});
+    }
+};
 
 // ---------------------------------------------------------------------------
 // Device helpers
@@ -1024,7 +1073,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
     cudaMemcpyAsync(tab, h_tab.data(), h_tab.size() * 4, cudaMemcpyHostToDevice, st);
 
     dim3 tgrid((W + TILE - 1) / TILE, (H + TILE - 1) / TILE, B);
-    k_transpose<<<tgrid, 256, 0, st>>>(f, fT, H, W);
+    { Prof pr(KK_TRANSPOSE, st); k_transpose<<<tgrid, 256, 0, st>>>(f, fT, H, W); }
     if ((rc = check_cuda("transpose"))) return rc;
 
     set_p1_smem();
@@ -1065,10 +1114,13 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p1.lcarry = lc;
         p1.edge = edge;
         dim3 g1((W + TILE - 1) / TILE, (p1.ngroups + P1_WARPS - 1) / P1_WARPS, B);
-        if (box)
-            k_pass1_box<G1, R_ANCHOR><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1, sp->radius);
-        else
-            k_pass1_gauss<G1, R_ANCHOR><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1);
+        {
+            Prof pr(KK_PASS1, st);
+            if (box)
+                k_pass1_box<G1, R_ANCHOR><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1, sp->radius);
+            else
+                k_pass1_gauss<G1, R_ANCHOR><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1);
+        }
         if ((rc = check_cuda("pass1"))) return rc;
 
         if (!box) {
@@ -1091,7 +1143,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             ca.extbuf = ext;
             ca.bstate = bst;
             dim3 gc((H + 127) / 128, n * 4 * B);
-            k_chain<<<gc, 128, 0, st>>>(ca);
+            { Prof pr(KK_CHAIN, st); k_chain<<<gc, 128, 0, st>>>(ca); }
             if ((rc = check_cuda("chain"))) return rc;
         }
 
@@ -1111,10 +1163,13 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.bstate = bst;
         p2.part = part;
         dim3 g2((H + P2_THREADS - 1) / P2_THREADS, p2.ngroups, B);
-        if (box)
-            k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, st>>>(p2, sp->radius);
-        else
-            k_pass2_gauss<G2, R_ANCHOR><<<g2, P2_THREADS, 0, st>>>(p2);
+        {
+            Prof pr(KK_PASS2, st);
+            if (box)
+                k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, st>>>(p2, sp->radius);
+            else
+                k_pass2_gauss<G2, R_ANCHOR><<<g2, P2_THREADS, 0, st>>>(p2);
+        }
         if ((rc = check_cuda("pass2"))) return rc;
 
         ReduceArgs ra;
@@ -1138,7 +1193,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             ra.den = den;
             ra.out = nullptr;
         }
-        k_reduce<<<tgrid, 256, 0, st>>>(ra);
+        { Prof pr(KK_REDUCE, st); k_reduce<<<tgrid, 256, 0, st>>>(ra); }
         if ((rc = check_cuda("reduce"))) return rc;
     }
     return TBF_OK;
@@ -1153,6 +1208,40 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
 extern "C" {
 
 int32_t tbf_abi_version(void) { return TBF_ABI_VERSION; }
+
+int tbf_profile_enable(int32_t on) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    g_prof_on = on != 0;
+    return TBF_OK;
+}
+
+int32_t tbf_profile_kinds(void) { return KK_COUNT; }
+
+const char* tbf_kernel_name(int32_t kind) {
+    return (kind >= 0 && kind < KK_COUNT) ? kKernelNames[kind] : "";
+}
+
+int tbf_profile_collect(double* ms, long long* launches, int32_t n) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    for (int k = 0; k < n; ++k) {
+        ms[k] = 0.0;
+        launches[k] = 0;
+    }
+    int rc = TBF_OK;
+    for (auto& r : g_prof) {
+        float t = 0.f;
+        if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess)
+            rc = fail(TBF_ERR_CUDA, "profile event: %s", cudaGetErrorString(cudaGetLastError()));
+        if (r.kind < n) {
+            ms[r.kind] += t;
+            launches[r.kind] += 1;
+        }
+        g_ev_pool.push_back(r.a);
+        g_ev_pool.push_back(r.b);
+    }
+    g_prof.clear();
+    return rc;
+}
 
 const char* tbf_last_error(void) { return g_last_error.c_str(); }
 
@@ -1170,7 +1259,7 @@ int tbf_range_check(const float* f, int64_t count, double T, unsigned long long*
     if (!d_counters) return fail(TBF_ERR_PARAM, "null counters");
     cudaStream_t st = (cudaStream_t)stream;
     long long blocks = std::min<long long>((count + 255) / 256, 148LL * 8);
-    k_range_check<<<(unsigned)blocks, 256, 0, st>>>(f, count, -1e-9, T + 1e-9, d_counters);
+    { Prof pr(KK_RANGE, st); k_range_check<<<(unsigned)blocks, 256, 0, st>>>(f, count, -1e-9, T + 1e-9, d_counters); }
     return check_cuda("range_check");
 }
 
@@ -1202,8 +1291,11 @@ int tbf_finalize(const float* num, const float* den, const float* f, float* out,
                  unsigned long long* d_counters, void* stream) {
     if (count <= 0) return fail(TBF_ERR_DIM, "empty input");
     long long blocks = std::min<long long>((count + 255) / 256, 148LL * 8);
-    k_finalize<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(num, den, f, out, count,
-                                                                   d_counters);
+    {
+        Prof pr(KK_FINALIZE, (cudaStream_t)stream);
+        k_finalize<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(num, den, f, out, count,
+                                                                       d_counters);
+    }
     return check_cuda("finalize");
 }
 

@@ -219,9 +219,17 @@ _PLANS: dict = {}
 _MAX_PLANS = 4
 
 
+def _require_cuda():
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise NativeUnavailableError("no CUDA device: the B200 path has no CPU fallback")
+    _native.load()
+
+
 def get_plan(shape, spatial: SpatialSpec, kernel: TrigKernel, device=None) -> TrigFilter:
     """Cached plan (workspace reuse across calls with the same configuration)."""
     torch = _torch()
+    _require_cuda()
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     key = (str(dev), tuple(shape), spatial, kernel.N, kernel.omega, kernel.T)
     plan = _PLANS.get(key)
@@ -269,6 +277,7 @@ def bilateral_trig(img, spatial, kernel, *, workers: int = 1,
     torch = _torch()
     kernel = _check_kernel(kernel)
     spatial = _check_spatial(spatial)
+    _require_cuda()
     kind = "image"
     if isinstance(img, Image):
         if img.channels != 1:
@@ -287,7 +296,8 @@ def bilateral_trig(img, spatial, kernel, *, workers: int = 1,
             raise DimensionError(f"unsupported input type {type(img).__name__}")
         if t.dim() not in (2, 3):
             raise DimensionError(f"expected [H, W] or [B, H, W], got shape {tuple(t.shape)}")
-        f = t.to(device="cuda" if not t.is_cuda else t.device, dtype=torch.float32).contiguous()
+        f = t.to(device="cuda" if not t.is_cuda else t.device, dtype=torch.float32,
+                 non_blocking=bool(not t.is_cuda and t.is_pinned())).contiguous()
         shape = (1, *f.shape) if f.dim() == 2 else tuple(f.shape)
     if diagnostics is not None:
         diagnostics.degree = kernel.N
@@ -310,7 +320,10 @@ def bilateral_trig(img, spatial, kernel, *, workers: int = 1,
         return Image(img.width, img.height, 1, res)
     if kind == "cuda":
         return out.reshape(img.shape)
-    res = out.reshape(t.shape).cpu()
+    # device -> host into pinned memory when the caller's buffer was pinned
+    res = torch.empty(tuple(t.shape), dtype=torch.float32,
+                      pin_memory=(kind == "cpu" and t.is_pinned()))
+    res.copy_(out.reshape(t.shape))
     return res.numpy() if kind == "numpy" else res
 
 

@@ -1,0 +1,284 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+own outputs (golden vectors from oracle/_ref) and the float64 oracle.
+
+Tolerance (north_star): max abs error <= 1e-3 * T = 0.255 for fp32 against
+the reference's float64.  Ports of the reference's hot-path tests
+(test_engines.py, test_spatial.py, test_backends.py) use the same bound
+where the reference's 1e-8 is an fp64-only figure.
+"""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, TOL
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def tb():
+    import paper_1105_4204_b200 as tb
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return tb
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle import trigbf_oracle
+
+    return trigbf_oracle
+
+
+def _spec(tb, kind, param):
+    return tb.SpatialSpec.box(param) if kind == "box" else tb.SpatialSpec.gaussian_recursive(param)
+
+
+def _run(tb, f, kind, param, sigma_r, degree=None, **kw):
+    k = tb.make_trig_kernel(sigma_r, 255.0, degree=degree)
+    out = tb.bilateral_trig(torch.from_numpy(np.ascontiguousarray(f, dtype=np.float32)).cuda(),
+                            _spec(tb, kind, param), k, **kw)
+    return out.cpu().numpy().astype(np.float64)
+
+
+# ---------------------------------------------------------------------------
+# golden vectors from the real reference
+# ---------------------------------------------------------------------------
+
+def test_small_goldens(tb, small_cases):
+    worst = 0.0
+    for name, c in small_cases.items():
+        got = _run(tb, c["f"], c["kind"], c["param"], c["sigma_r"], c["degree"])
+        err = float(np.max(np.abs(got - c["out"])))
+        worst = max(worst, err)
+        assert err <= TOL, (name, err)
+    print(f"small goldens: worst max abs err {worst:.3g}")
+
+
+def test_image_roundtrip_matches_golden(tb, small_cases):
+    c = small_cases["rec_96x80_s3_r30"]
+    img = tb.Image(c["w"], c["h"], 1, c["f"].astype(np.float64)[None])
+    out = tb.bilateral_trig(img, tb.SpatialSpec.gaussian_recursive(3.0), tb.make_trig_kernel(30.0))
+    assert isinstance(out, tb.Image)
+    assert tb.error_stats(out, tb.Image(c["w"], c["h"], 1, c["out"][None])).max_abs <= TOL
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2, 3, 4, 5])
+def test_config_goldens(tb, cfg_id):
+    """Full-size configs: the device result at the sampled pixels of the
+    reference's own output (full runs for 1, 2, 4; margin-safe crops for 3, 5)."""
+    from paper_1105_4204_b200 import workloads
+
+    g = np.load(os.path.join(GOLDEN, f"config_{cfg_id}.npz"))
+    cfg = workloads.CONFIGS[cfg_id]
+    frames = sorted(set(g["frame"].tolist()))
+    k = tb.make_trig_kernel(cfg.sigma_r, cfg.T)
+    spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
+    worst = 0.0
+    for fi in frames:
+        f = torch.from_numpy(workloads.frame(cfg, fi)).cuda()
+        out = tb.bilateral_trig(f, spec, k)
+        sel = g["frame"] == fi
+        got = out[torch.from_numpy(g["y"][sel]).cuda(), torch.from_numpy(g["x"][sel]).cuda()]
+        err = float(np.max(np.abs(got.double().cpu().numpy() - g["value"][sel])))
+        worst = max(worst, err)
+        del out, f
+        torch.cuda.empty_cache()
+    print(f"config {cfg_id}: worst max abs err {worst:.3g} over {g['value'].size} sampled pixels")
+    assert worst <= TOL
+
+
+def test_batched_frames_equal_single_calls(tb):
+    """Config-4 style batch: frames are independent (batch == per-frame calls)."""
+    from paper_1105_4204_b200.workloads import rects_image
+
+    fs = np.stack([rects_image(72, 130, 5, seed=s) for s in (1, 2, 3)])
+    k = tb.make_trig_kernel(25.0)
+    spec = tb.SpatialSpec.gaussian_recursive(5.0)
+    batch = tb.bilateral_trig(torch.from_numpy(fs).cuda(), spec, k).cpu().numpy()
+    for i in range(3):
+        one = tb.bilateral_trig(torch.from_numpy(fs[i]).cuda(), spec, k).cpu().numpy()
+        assert np.array_equal(batch[i], one)
+
+
+# ---------------------------------------------------------------------------
+# ports of the reference's hot-path tests
+# ---------------------------------------------------------------------------
+
+def test_trig_equals_direct_box(tb, orc):
+    # test_engines.py:88-99 (trig == direct with the same raised cosine)
+    rng = np.random.default_rng(13)
+    for _ in range(2):
+        f = rng.integers(0, 256, (64, 64)).astype(np.float32)
+        for radius in (1, 3, 7):
+            for n_deg in (1, 2, 3, 4, 5, 6):
+                k = orc.make_trig_kernel(170.0, 255.0, degree=n_deg)
+                ref = orc.bilateral_direct(f.astype(np.float64), "box", radius, lambda s: orc.trig_eval(k, s))
+                got = _run(tb, f, "box", radius, 170.0, n_deg)
+                assert np.max(np.abs(got - ref)) <= TOL
+
+
+def test_constant_image_fixed_point(tb):
+    # test_engines.py:111-115
+    f = np.full((16, 16), 131.0, dtype=np.float32)
+    got = _run(tb, f, "gauss-recursive", 4.0, 80.0)
+    assert np.max(np.abs(got - 131.0)) < 1e-3
+
+
+def test_degree_zero_is_plain_spatial(tb, orc):
+    # test_engines.py:117-123
+    f = np.random.default_rng(15).integers(0, 256, (10, 20)).astype(np.float32)
+    got = _run(tb, f, "box", 2, 80.0, 0)
+    assert np.max(np.abs(got - orc.smooth_plane(f, "box", 2))) <= TOL
+    got = _run(tb, f, "gauss-recursive", 2.5, 80.0, 0)
+    assert np.max(np.abs(got - orc.smooth_plane(f, "gauss-recursive", 2.5))) <= TOL
+
+
+def test_out_of_range_rejected(tb):
+    # test_engines.py:127-131
+    f = np.array([[0.0, 100.0], [200.0, 300.0]], dtype=np.float32)
+    with pytest.raises(tb.ParameterError):
+        _run(tb, f, "box", 1, 80.0)
+    with pytest.raises(tb.ParameterError):
+        _run(tb, np.array([[0.0, np.nan]], dtype=np.float32), "box", 1, 80.0)
+
+
+def test_color_image_rejected(tb):
+    img = tb.Image(2, 2, 3, np.zeros((3, 2, 2)))
+    with pytest.raises(tb.DimensionError):
+        tb.bilateral_trig(img, tb.SpatialSpec.box(1), tb.make_trig_kernel(80.0))
+
+
+def test_diagnostics_pass_counts_and_guard(tb):
+    # test_engines.py:133-153
+    f = np.random.default_rng(16).integers(0, 256, (16, 16)).astype(np.float32)
+    for n_deg in range(0, 10):
+        diag = tb.EngineDiagnostics()
+        k = tb.make_trig_kernel(80.0, 255.0, degree=n_deg)
+        tb.bilateral_trig(torch.from_numpy(f).cuda(), tb.SpatialSpec.box(1), k, diagnostics=diag)
+        assert diag.spatial_passes == 2 * (n_deg + 1) - (1 if n_deg % 2 == 0 else 0)
+        assert diag.degree == n_deg
+    rng = np.random.default_rng(17)
+    for _ in range(5):
+        f = rng.integers(0, 256, (24, 24)).astype(np.float32)
+        n_deg = int(rng.integers(1, 7))
+        k = tb.make_trig_kernel(170.0, 255.0, degree=n_deg)
+        diag = tb.EngineDiagnostics()
+        tb.bilateral_trig(torch.from_numpy(f).cuda(), tb.SpatialSpec.box(2), k, diagnostics=diag)
+        assert diag.guarded_pixels == 0
+
+
+def test_range_preservation(tb):
+    # test_engines.py:155-165 (fp32 slack)
+    rng = np.random.default_rng(18)
+    for _ in range(20):
+        w, h = int(rng.integers(4, 20)), int(rng.integers(4, 20))
+        f = rng.integers(0, 256, (h, w)).astype(np.float32)
+        got = _run(tb, f, "box", int(rng.integers(1, 4)), 170.0, int(rng.integers(1, 6)))
+        assert got.min() >= f.min() - 1e-3 and got.max() <= f.max() + 1e-3
+
+
+def test_workers_and_repeats_bit_identical(tb):
+    # test_engines.py:167-184
+    f = np.random.default_rng(19).integers(0, 256, (30, 40)).astype(np.float32)
+    a = _run(tb, f, "gauss-recursive", 3.0, 60.0, workers=1)
+    b = _run(tb, f, "gauss-recursive", 3.0, 60.0, workers=4)
+    c = _run(tb, f, "gauss-recursive", 3.0, 60.0)
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+def test_edge_sharper_than_blur(tb, orc):
+    # test_engines.py:186-198
+    plane = np.where(np.arange(40) < 20, 0.0, 200.0)[None, :].repeat(40, axis=0).astype(np.float32)
+    got = _run(tb, plane, "box", 3, 30.0)
+    blur = orc.smooth_plane(plane, "box", 3)
+    assert np.max(np.abs(np.diff(got, axis=1))) >= 0.8 * 200.0
+    assert np.max(np.abs(np.diff(blur, axis=1))) < np.max(np.abs(np.diff(got, axis=1)))
+
+
+def test_term_batches_and_partials_match_full(tb):
+    """Splitting the terms into batches, or into shards summed with
+    tbf_trig_partial + tbf_finalize (the multi-GPU path), gives the same
+    result as one batch (up to fp32 reassociation of the num/den sums)."""
+    from paper_1105_4204_b200.distributed import term_range
+    from paper_1105_4204_b200.kernels import term_pairs
+
+    f = torch.from_numpy(np.random.default_rng(5).uniform(0, 255, (70, 90)).astype(np.float32)).cuda()
+    k = tb.make_trig_kernel(20.0)
+    spec = tb.SpatialSpec.gaussian_recursive(4.0)
+    full = tb.TrigFilter(tuple(f.shape), spec, k)(f)
+    batched = tb.TrigFilter(tuple(f.shape), spec, k, batch_terms=6)(f)
+    assert float((full - batched).abs().max()) < 1e-3
+    pairs = term_pairs(k)
+    num = torch.zeros_like(f)
+    den = torch.zeros_like(f)
+    for r in range(3):
+        t0, t1 = term_range(pairs.count, pairs.has_zero, 3, r)
+        n_ = torch.zeros_like(f)
+        d_ = torch.zeros_like(f)
+        tb.TrigFilter(tuple(f.shape), spec, k, term_range=(t0, t1)).partial(f, n_, d_)
+        num += n_
+        den += d_
+    out = torch.empty_like(f)
+    tb.TrigFilter(tuple(f.shape), spec, k).finalize(num, den, f, out)
+    assert float((full - out).abs().max()) < 1e-3
+
+
+def test_recursive_smooth_plugin_f64(tb, plugin_vectors):
+    # test_backends.py:30-40: compiled vs fallback < 1e-10 (fp64 device twin)
+    from paper_1105_4204_b200 import _native
+
+    lib = _native.load()
+    d = plugin_vectors
+    for i in range(4):
+        a = torch.from_numpy(d[f"plugin_rec{i}__a"]).cuda()
+        h, w = a.shape
+        out = torch.empty_like(a)
+        scratch = torch.empty((h + 2 * (h - 1) + 8) * w, dtype=torch.float64, device="cuda")
+        taps = [float(v) for v in d[f"plugin_rec{i}__taps"]]
+        _native.check(lib.tbf_recursive_smooth_f64(a.data_ptr(), out.data_ptr(), h, w, *taps, h - 1,
+                                                   scratch.data_ptr(), None))
+        torch.cuda.synchronize()
+        assert np.max(np.abs(out.cpu().numpy() - d[f"plugin_rec{i}__out"])) < 1e-10
+    for i in range(5):
+        a = torch.from_numpy(d[f"plugin_box{i}__a"]).cuda()
+        out = torch.empty_like(a)
+        _native.check(lib.tbf_box_pass_f64(a.data_ptr(), out.data_ptr(), a.shape[0], a.shape[1],
+                                           int(d[f"plugin_box{i}__radius"][0]), None))
+        torch.cuda.synchronize()
+        assert np.max(np.abs(out.cpu().numpy() - d[f"plugin_box{i}__out"])) < 1e-10
+
+
+def test_unit_dc_gain_and_linearity_properties(tb):
+    """Size-independent properties at a full config size: a constant image is
+    a fixed point, and the filter is invariant to adding a constant within
+    range is NOT expected (range kernel) -- so check the fixed point at
+    2048^2 plus symmetry under transposition."""
+    f = torch.full((2048, 2048), 77.0, device="cuda")
+    k = tb.make_trig_kernel(20.0)
+    out = tb.bilateral_trig(f, tb.SpatialSpec.gaussian_recursive(8.0), k)
+    assert float((out - 77.0).abs().max()) < 1e-2
+    g = torch.from_numpy(np.random.default_rng(3).uniform(0, 255, (200, 130)).astype(np.float32)).cuda()
+    a = tb.bilateral_trig(g, tb.SpatialSpec.gaussian_recursive(3.0), k)
+    b = tb.bilateral_trig(g.t().contiguous(), tb.SpatialSpec.gaussian_recursive(3.0), k).t()
+    assert float((a - b).abs().max()) < 1e-2
+
+
+def test_brute_force_error_reported(tb, orc):
+    """Error vs the brute-force Gaussian bilateral filter (reported, not gated;
+    the range-kernel approximation dominates)."""
+    from paper_1105_4204_b200 import workloads
+
+    cfg = workloads.CONFIGS[1]
+    f = workloads.frame(cfg, 0)[:128, :128]
+    got = _run(tb, f, "gauss-recursive", cfg.sigma_s, cfg.sigma_r)
+    brute = orc.bilateral_direct(f.astype(np.float64), "gauss-fir", cfg.sigma_s,
+                                 lambda s: orc.gaussian_eval(cfg.sigma_r, s))
+    e = np.abs(got - brute)
+    print(f"vs brute-force Gaussian BF (128^2 crop of cfg1): max {e.max():.3g} mean {e.mean():.3g}")
+    assert e.max() < 10.0
