@@ -49,7 +49,7 @@
 namespace {
 
 constexpr int TILE = 32;          // segment length along y == tile width along x == warp size
-constexpr int P1_WARPS = 4;       // warps per pass-1 block (each a different term group)
+constexpr int P1_WARPS = 2;       // warps per pass-1 block (each a different term group)
 constexpr int P2_THREADS = 128;   // rows per pass-2 block
 constexpr int BUF_LD = TILE + 1;  // padded leading dimension of the smem tile
 
@@ -123,8 +123,16 @@ struct Prof {
 // Device helpers
 // ---------------------------------------------------------------------------
 
+// Cascade of the two pole-pair sections in "pure" form: the section gains
+// g1, g2 are not applied per sample (v = u + a1 v1 + a2 v2; y = v + b1 y1 +
+// b2 y2: 4 FMA per sample instead of 6).  Each pure sweep therefore scales
+// its output by 1/g (g = g1*g2); the host folds the scale back in (pass-1
+// epilogue multiplies by gg = g^2, pass-2 weights carry g^2).
 struct Casc {
-    float g1, a1, a2, g2, b1, b2;
+    float a1, a2, b1, b2;
+    float ig1;  // 1/g1  (steady state of section 1 for unit input)
+    float ig;   // 1/g   (steady state of the cascade for unit input)
+    float gg;   // g^2   (undoes the two y sweeps)
 };
 
 // Whole-sample reflection for indices within one reflection of the line
@@ -143,34 +151,69 @@ __device__ __forceinline__ long long mirror_any(long long i, long long n) {
     return i >= n ? period - i : i;
 }
 
-// One step of the cascade of two all-pole biquads (state v1,v2 | y1,y2).
+// One pure cascade step (state v1,v2 | y1,y2); output scaled by 1/g.
 __device__ __forceinline__ float cstep(float u, float& v1, float& v2, float& y1, float& y2,
                                        const Casc& k) {
-    float v = fmaf(k.g1, u, fmaf(k.a1, v1, k.a2 * v2));
+    float v = fmaf(k.a1, v1, fmaf(k.a2, v2, u));
     v2 = v1;
     v1 = v;
-    float y = fmaf(k.g2, v, fmaf(k.b1, y1, k.b2 * y2));
+    float y = fmaf(k.b1, y1, fmaf(k.b2, y2, v));
     y2 = y1;
     y1 = y;
     return y;
 }
 
+// Steady state of the pure cascade for a constant input u (replicate
+// start-up of _core.pyx:75-78 / :85-87).
+__device__ __forceinline__ void csteady(float u, float& v1, float& v2, float& y1, float& y2,
+                                        const Casc& k) {
+    v1 = v2 = u * k.ig1;
+    y1 = y2 = u * k.ig;
+}
+
+// sin and cos of x for |x| < ~1e5 on the FMA pipe (no SFU, no slow-path
+// branch): Cody-Waite reduction by pi/2 in three parts (exact products inside
+// the FMAs), then the Cephes minimax polynomials on [-pi/4, pi/4] (about 1 ulp).
+// Arguments here are nu*f <= ~420 rad.
+__device__ __forceinline__ void sincos_fma(float x, float* sp, float* cp) {
+    const float q = rintf(x * 0.636619772367581343f);
+    const int qi = (int)q;
+    float r = fmaf(q, -1.5703125f, x);
+    r = fmaf(q, -4.837512969970703125e-4f, r);
+    r = fmaf(q, -7.54978995489188216e-8f, r);
+    const float r2 = r * r;
+    float ps = fmaf(r2, -1.9515295891e-4f, 8.3321608736e-3f);
+    ps = fmaf(r2, ps, -1.6666654611e-1f);
+    ps = fmaf(r2 * r, ps, r);
+    float pc = fmaf(r2, 2.443315711809948e-5f, -1.388731625493765e-3f);
+    pc = fmaf(r2, pc, 4.166664568298827e-2f);
+    pc = fmaf(r2, pc, -0.5f);
+    pc = fmaf(r2, pc, 1.0f);
+    const bool swap = qi & 1;
+    float sv = swap ? pc : ps;
+    float cv = swap ? ps : pc;
+    sv = __int_as_float(__float_as_int(sv) ^ ((qi & 2) << 30));
+    cv = __int_as_float(__float_as_int(cv) ^ (((qi + 1) & 2) << 30));
+    *sp = sv;
+    *cp = cv;
+}
+
 // Phasors of G consecutive terms at one sample (engines.py:272-286).  Terms
 // are grouped in anchor blocks of R: the first term of a block takes an
-// accurate sincos of nu*f (nu split hi/lo so the phase is correctly rounded,
-// no SFU approximation), the others follow by complex rotation with
-// (cos, sin)(dnu*f).  Pass 1 and pass 2 use the same rule, so modulation and
-// demodulation see bit-identical phasors.
+// accurate sincos of nu*f (nu split hi/lo so the phase is correctly rounded),
+// the others follow by complex rotation with (cos, sin)(dnu*f).  Pass 1 and
+// pass 2 use the same rule, so modulation and demodulation see bit-identical
+// phasors.
 template <int G, int R>
 __device__ __forceinline__ void phasors(float fv, const float (&nu_hi)[G], const float (&nu_lo)[G],
                                         float dnu, float (&cc)[G], float (&sn)[G]) {
     float ss = 0.f, sc = 1.f;
-    if (R > 1) sincosf(dnu * fv, &ss, &sc);
+    if (R > 1) sincos_fma(dnu * fv, &ss, &sc);
     float c = 1.f, s = 0.f;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         if (g % R == 0) {
-            sincosf(fmaf(nu_hi[g], fv, nu_lo[g] * fv), &s, &c);
+            sincos_fma(fmaf(nu_hi[g], fv, nu_lo[g] * fv), &s, &c);
         } else {
             float cn = fmaf(c, sc, -s * ss);
             float snn = fmaf(s, sc, c * ss);
@@ -244,6 +287,7 @@ struct Pass2Args {
     TermDev t;
     int ngroups;       // ceil(t.n / G2)
     float Hm[TILE][4]; // homogeneous response of the cascade to a unit state
+    float wscale;      // g^2: undoes the two pure x sweeps (1 for box)
     const float* floc;
     const float* carry;   // chained carries [n*16][B][ntx][H]
     const float* bstate;  // [n*16][B][H]
@@ -282,11 +326,14 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
     const int H = a.H, W = a.W;
     const int x0 = blockIdx.x * TILE;
     const int x = x0 + lane;
-    const int xc = x < W ? x : W - 1;
+    const bool xv = x < W;
+    const int xc = xv ? x : W - 1;
     const int tlen = min(TILE, W - x0);
     const int j0 = grp * G;
     const int nt = min(G, a.t.n - j0);  // valid terms in this group (1..G)
-    float* buf = smem + (size_t)warp * NP * TILE * BUF_LD;
+    float* const buf = smem + (size_t)warp * NP * TILE * BUF_LD;
+    float* const bl = buf + lane;           // own column (phases A/B)
+    float* const br = buf + lane * BUF_LD;  // own row (epilogue)
 
     float nu_hi[G], nu_lo[G];
 #pragma unroll
@@ -295,153 +342,180 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
         nu_lo[g] = a.t.nu_lo[j0 + g];
     }
     const float dnu = a.t.dnu;
-    const float* fcol = a.f + (size_t)b * H * W + xc;
     const Casc k = a.k;
     const int Ey = a.Ey;
     const int iend = H + Ey;
+    const float* const fcol = a.f + (size_t)b * H * W + xc;
+    const size_t ckq = (size_t)a.B * W;               // stride between state slots
+    const size_t cks = (size_t)a.t.n * 16 * ckq;      // stride between segments
+    float* const ck0 = a.ckpt + (size_t)(j0 * 16) * ckq + (size_t)b * W + xc;
 
     float v1[NP], v2[NP], y1[NP], y2[NP], u[NP];
 
     // ---- phase A: forward sweep over the mirrored column, checkpoints ----
     {
-        float fv = __ldg(fcol + (size_t)mirror1(-Ey, H) * W);
-        modulate<G, R>(fv, nu_hi, nu_lo, dnu, u);
+        modulate<G, R>(__ldg(fcol + (size_t)mirror1(-Ey, H) * W), nu_hi, nu_lo, dnu, u);
 #pragma unroll
-        for (int p = 0; p < NP; ++p) v1[p] = v2[p] = y1[p] = y2[p] = u[p];
+        for (int p = 0; p < NP; ++p) csteady(u[p], v1[p], v2[p], y1[p], y2[p], k);
     }
-    const size_t ck_stride_seg = (size_t)a.t.n * 16 * a.B * W;
-    float* ck_base = a.ckpt + ((size_t)(j0 * 16) * a.B + b) * W + x;
-    const size_t ck_stride_q = (size_t)a.B * W;
-    for (int ib = -Ey; ib < iend; ib += 8) {
+    for (int ib = -Ey; ib < 0; ib += 8) {  // left extension: rows Ey..1
         float fv[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            int i = ib + q;
-            fv[q] = i < iend ? __ldg(fcol + (size_t)mirror1(i, H) * W) : 0.f;
-        }
+        for (int q = 0; q < 8; ++q)
+            fv[q] = ib + q < 0 ? __ldg(fcol + (size_t)(-(ib + q)) * W) : 0.f;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            int i = ib + q;
-            if (i < iend) {
-                if (i >= 0 && (i & (TILE - 1)) == 0 && x < W) {
-                    float* ck = ck_base + (size_t)(i >> 5) * ck_stride_seg;
-#pragma unroll
-                    for (int p = 0; p < NP; ++p) {
-                        if (p / 4 < nt) {
-                            ck[(size_t)(p * 4 + 0) * ck_stride_q] = v1[p];
-                            ck[(size_t)(p * 4 + 1) * ck_stride_q] = v2[p];
-                            ck[(size_t)(p * 4 + 2) * ck_stride_q] = y1[p];
-                            ck[(size_t)(p * 4 + 3) * ck_stride_q] = y2[p];
-                        }
-                    }
-                }
+            if (ib + q < 0) {
                 modulate<G, R>(fv[q], nu_hi, nu_lo, dnu, u);
 #pragma unroll
                 for (int p = 0; p < NP; ++p) cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
             }
         }
     }
-
-    // ---- phase B: segments bottom -> top ----
-    float p1[NP], p2[NP], q1[NP], q2[NP];
-    const size_t fl_plane = (size_t)a.B * W * H;
-    float* fl_base = a.floc + ((size_t)(j0 * 4) * a.B + b) * W * (size_t)H;
-    const size_t lc_q = (size_t)a.B * a.ntx * H;
-    float* lc_base = a.lcarry + ((size_t)(j0 * 16) * a.B + b) * a.ntx * (size_t)H +
-                     (size_t)blockIdx.x * H;
-    const size_t ed_plane = (size_t)a.B * a.ne * H;
-    float* ed_base = a.edge + ((size_t)(j0 * 4) * a.B + b) * a.ne * (size_t)H;
-
-    for (int seg = a.nseg - 1; seg >= 0; --seg) {
+    for (int seg = 0; seg < a.nseg; ++seg) {
         const int i0 = seg * TILE;
-        const int i1 = min(i0 + TILE, iend);
-        if (x < W) {
-            const float* ck = ck_base + (size_t)seg * ck_stride_seg;
+        const int len = min(TILE, iend - i0);
+        const bool inner = i0 + TILE <= H;
+        if (xv) {
+            float* ck = ck0 + (size_t)seg * cks;
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
                 if (p / 4 < nt) {
-                    v1[p] = ck[(size_t)(p * 4 + 0) * ck_stride_q];
-                    v2[p] = ck[(size_t)(p * 4 + 1) * ck_stride_q];
-                    y1[p] = ck[(size_t)(p * 4 + 2) * ck_stride_q];
-                    y2[p] = ck[(size_t)(p * 4 + 3) * ck_stride_q];
-                } else {
-                    v1[p] = v2[p] = y1[p] = y2[p] = 0.f;
+                    ck[(size_t)(p * 4 + 0) * ckq] = v1[p];
+                    ck[(size_t)(p * 4 + 1) * ckq] = v2[p];
+                    ck[(size_t)(p * 4 + 2) * ckq] = y1[p];
+                    ck[(size_t)(p * 4 + 3) * ckq] = y2[p];
                 }
             }
-        } else {
-#pragma unroll
-            for (int p = 0; p < NP; ++p) v1[p] = v2[p] = y1[p] = y2[p] = 0.f;
         }
-        // forward recompute of the segment into smem (own column only)
-        for (int ib = i0; ib < i1; ib += 8) {
+        const float* fp = fcol + (size_t)i0 * W;
+        for (int r0 = 0; r0 < len; r0 += 8) {
             float fv[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                int i = ib + q;
-                fv[q] = i < i1 ? __ldg(fcol + (size_t)mirror1(i, H) * W) : 0.f;
+                const int r = r0 + q;
+                fv[q] = r < len ? __ldg(inner ? fp + (size_t)r * W
+                                              : fcol + (size_t)mirror1(i0 + r, H) * W)
+                                : 0.f;
             }
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                int i = ib + q;
-                if (i < i1) {
+                if (r0 + q < len) {
+                    modulate<G, R>(fv[q], nu_hi, nu_lo, dnu, u);
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
+                }
+            }
+        }
+    }
+
+    // ---- phase B: segments bottom -> top ----
+    float p1[NP], p2[NP], q1[NP], q2[NP];
+    const size_t flpl = (size_t)a.B * W * H;  // plane stride of floc
+    const size_t lcq = (size_t)a.B * a.ntx * H;
+    const size_t edpl = (size_t)a.B * a.ne * H;
+    for (int seg = a.nseg - 1; seg >= 0; --seg) {
+        const int i0 = seg * TILE;
+        const int len = min(TILE, iend - i0);
+        const bool inner = i0 + TILE <= H;
+        {
+            const float* ck = ck0 + (size_t)seg * cks;
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const bool ok = xv && p / 4 < nt;
+                v1[p] = ok ? ck[(size_t)(p * 4 + 0) * ckq] : 0.f;
+                v2[p] = ok ? ck[(size_t)(p * 4 + 1) * ckq] : 0.f;
+                y1[p] = ok ? ck[(size_t)(p * 4 + 2) * ckq] : 0.f;
+                y2[p] = ok ? ck[(size_t)(p * 4 + 3) * ckq] : 0.f;
+            }
+        }
+        // forward recompute of the segment into smem (own column only)
+        const float* fp = fcol + (size_t)i0 * W;
+        for (int r0 = 0; r0 < len; r0 += 8) {
+            float fv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int r = r0 + q;
+                fv[q] = r < len ? __ldg(inner ? fp + (size_t)r * W
+                                              : fcol + (size_t)mirror1(i0 + r, H) * W)
+                                : 0.f;
+            }
+            float* row = bl + r0 * BUF_LD;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (r0 + q < len) {
                     modulate<G, R>(fv[q], nu_hi, nu_lo, dnu, u);
 #pragma unroll
                     for (int p = 0; p < NP; ++p)
-                        buf[(p * TILE + (i - i0)) * BUF_LD + lane] =
-                            cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
+                        row[(p * TILE + q) * BUF_LD] = cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
                 }
             }
         }
         if (seg == a.nseg - 1) {
             // backward start = steady state of the last forward output (_core.pyx:85-87)
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                float last = buf[(p * TILE + (i1 - 1 - i0)) * BUF_LD + lane];
-                p1[p] = p2[p] = q1[p] = q2[p] = last;
-            }
+            for (int p = 0; p < NP; ++p)
+                csteady(bl[(p * TILE + len - 1) * BUF_LD], p1[p], p2[p], q1[p], q2[p], k);
         }
         // backward sweep over the segment, in place
-        for (int i = i1 - 1; i >= i0; --i) {
+        for (int r0 = len - 1; r0 >= 0; r0 -= 8) {
+            float* row = bl + r0 * BUF_LD;
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                float* cell = &buf[(p * TILE + (i - i0)) * BUF_LD + lane];
-                *cell = cstep(*cell, p1[p], p2[p], q1[p], q2[p], k);
-            }
-        }
-        if (i0 < H) {
-            __syncwarp();
-            // epilogue: lane <-> row i; tile-local zero-state forward along x
-            const int i = i0 + lane;
-            if (i < min(i1, H)) {
-                float lv1[NP], lv2[NP], ly1[NP], ly2[NP];
-#pragma unroll
-                for (int p = 0; p < NP; ++p) lv1[p] = lv2[p] = ly1[p] = ly2[p] = 0.f;
-                for (int xx = 0; xx < tlen; ++xx) {
-                    const int gx = x0 + xx;
-                    const bool is_edge = a.edge_all || gx <= a.Ex || gx >= W - 1 - a.Ex;
-                    const int e = a.edge_all ? gx : (gx <= a.Ex ? gx : gx - (W - 1 - a.Ex) + a.Ex + 1);
+            for (int q = 0; q < 8; ++q) {
+                if (r0 - q >= 0) {
 #pragma unroll
                     for (int p = 0; p < NP; ++p) {
-                        if (p / 4 < nt) {
-                            float yv = buf[(p * TILE + lane) * BUF_LD + xx];
-                            float yl = cstep(yv, lv1[p], lv2[p], ly1[p], ly2[p], k);
-                            fl_base[(size_t)p * fl_plane + (size_t)gx * H + i] = yl;
-                            if (is_edge) ed_base[(size_t)p * ed_plane + (size_t)e * H + i] = yv;
+                        float* cell = row + (p * TILE - q) * BUF_LD;
+                        *cell = cstep(*cell, p1[p], p2[p], q1[p], q2[p], k);
+                    }
+                }
+            }
+        }
+        if (i0 >= H) continue;  // extension segment: no output
+        __syncwarp();
+        // epilogue: lane <-> row i; tile-local zero-state forward along x
+        const int i = i0 + lane;
+        if (lane < min(len, H - i0)) {
+            float lv1[NP], lv2[NP], ly1[NP], ly2[NP];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) lv1[p] = lv2[p] = ly1[p] = ly2[p] = 0.f;
+            float* fl = a.floc + ((size_t)(j0 * 4) * a.B + b) * W * (size_t)H + (size_t)x0 * H + i;
+            const bool edge_tile = a.edge_all || x0 <= a.Ex || x0 + tlen - 1 >= W - 1 - a.Ex;
+            float* ed = a.edge + ((size_t)(j0 * 4) * a.B + b) * a.ne * (size_t)H + i;
+            for (int xb = 0; xb < tlen; xb += 8) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int xx = xb + q;
+                    if (xx < tlen) {
+                        const int gx = x0 + xx;
+                        const bool is_edge = edge_tile && (a.edge_all || gx <= a.Ex || gx >= W - 1 - a.Ex);
+                        const int e = a.edge_all ? gx : (gx <= a.Ex ? gx : gx - (W - 1 - a.Ex) + a.Ex + 1);
+#pragma unroll
+                        for (int p = 0; p < NP; ++p) {
+                            if (p / 4 < nt) {
+                                // undo the 1/g^2 of the two pure y sweeps
+                                const float yv = br[p * TILE * BUF_LD + xx] * k.gg;
+                                fl[(size_t)p * flpl + (size_t)xx * H] =
+                                    cstep(yv, lv1[p], lv2[p], ly1[p], ly2[p], k);
+                                if (is_edge) ed[(size_t)p * edpl + (size_t)e * H] = yv;
+                            }
                         }
                     }
                 }
+            }
+            float* lc = a.lcarry + ((size_t)(j0 * 16) * a.B + b) * a.ntx * (size_t)H +
+                        (size_t)blockIdx.x * H + i;
 #pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    if (p / 4 < nt) {
-                        lc_base[(size_t)(p * 4 + 0) * lc_q + i] = lv1[p];
-                        lc_base[(size_t)(p * 4 + 1) * lc_q + i] = lv2[p];
-                        lc_base[(size_t)(p * 4 + 2) * lc_q + i] = ly1[p];
-                        lc_base[(size_t)(p * 4 + 3) * lc_q + i] = ly2[p];
-                    }
+            for (int p = 0; p < NP; ++p) {
+                if (p / 4 < nt) {
+                    lc[(size_t)(p * 4 + 0) * lcq] = lv1[p];
+                    lc[(size_t)(p * 4 + 1) * lcq] = lv2[p];
+                    lc[(size_t)(p * 4 + 2) * lcq] = ly1[p];
+                    lc[(size_t)(p * 4 + 3) * lcq] = ly2[p];
                 }
             }
-            __syncwarp();
         }
+        __syncwarp();
     }
 }
 
@@ -457,43 +531,96 @@ __global__ void __launch_bounds__(128) k_chain(const __grid_constant__ ChainArgs
     const int H = a.H, W = a.W, Ex = a.Ex;
     const Casc k = a.k;
     const float* ed = a.edge + (size_t)bt * a.ne * H + i;
-    auto Y = [&](int xx) -> float {
-        int e = a.edge_all ? xx : (xx <= Ex ? xx : xx - (W - 1 - Ex) + Ex + 1);
-        return ed[(size_t)e * H];
+    auto eidx = [&](int xx) -> int {
+        return a.edge_all ? xx : (xx <= Ex ? xx : xx - (W - 1 - Ex) + Ex + 1);
     };
     float v1, v2, y1, y2;
-    {
-        float u0 = Y(Ex);  // mirror(-Ex)
-        v1 = v2 = y1 = y2 = u0;
+    csteady(ed[(size_t)eidx(Ex) * H], v1, v2, y1, y2, k);  // mirror(-Ex)
+    // left extension x = -Ex..-1 reads Y(-x); chunks of 8 loads in flight
+    for (int xb = -Ex; xb < 0; xb += 8) {
+        float u[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int xx = xb + q;
+            u[q] = xx < 0 ? ed[(size_t)eidx(-xx) * H] : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (xb + q < 0) cstep(u[q], v1, v2, y1, y2, k);
     }
-    for (int xx = -Ex; xx < 0; ++xx) cstep(Y(-xx), v1, v2, y1, y2, k);
-    // chain along x; the 4 carry planes of this plane are tq = tp*4 + {0..3}
+    // chain along x: C_t = state at tile start; s_{t+1} = M s_t + L_t
+    float M[16], Ml[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        M[q] = a.M[q];
+        Ml[q] = a.Mlast[q];
+    }
     const int tp = bt / a.B, b = bt % a.B;
     const size_t q_stride = (size_t)a.B * a.ntx * H;
     float* lc = a.lcarry + ((size_t)(tp * 4) * a.B + b) * a.ntx * (size_t)H + i;
-    for (int t = 0; t < a.ntx; ++t) {
-        float* c = lc + (size_t)t * H;
-        float L0 = c[0], L1 = c[q_stride], L2 = c[2 * q_stride], L3 = c[3 * q_stride];
-        c[0] = v1;
-        c[q_stride] = v2;
-        c[2 * q_stride] = y1;
-        c[3 * q_stride] = y2;
-        const float* M = (t == a.ntx - 1) ? a.Mlast : a.M;
-        float s0 = v1, s1 = v2, s2 = y1, s3 = y2;
-        v1 = fmaf(M[0], s0, fmaf(M[4], s1, fmaf(M[8], s2, fmaf(M[12], s3, L0))));
-        v2 = fmaf(M[1], s0, fmaf(M[5], s1, fmaf(M[9], s2, fmaf(M[13], s3, L1))));
-        y1 = fmaf(M[2], s0, fmaf(M[6], s1, fmaf(M[10], s2, fmaf(M[14], s3, L2))));
-        y2 = fmaf(M[3], s0, fmaf(M[7], s1, fmaf(M[11], s2, fmaf(M[15], s3, L3))));
+    for (int tb = 0; tb < a.ntx; tb += 8) {
+        float L[8][4];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int t = tb + q;
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                L[q][r] = t < a.ntx ? lc[(size_t)t * H + r * q_stride] : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int t = tb + q;
+            if (t < a.ntx) {
+                float* c = lc + (size_t)t * H;
+                c[0] = v1;
+                c[q_stride] = v2;
+                c[2 * q_stride] = y1;
+                c[3 * q_stride] = y2;
+                const bool last = t == a.ntx - 1;
+                float s0 = v1, s1 = v2, s2 = y1, s3 = y2;
+                float m[16];
+#pragma unroll
+                for (int r = 0; r < 16; ++r) m[r] = last ? Ml[r] : M[r];
+                v1 = fmaf(m[0], s0, fmaf(m[4], s1, fmaf(m[8], s2, fmaf(m[12], s3, L[q][0]))));
+                v2 = fmaf(m[1], s0, fmaf(m[5], s1, fmaf(m[9], s2, fmaf(m[13], s3, L[q][1]))));
+                y1 = fmaf(m[2], s0, fmaf(m[6], s1, fmaf(m[10], s2, fmaf(m[14], s3, L[q][2]))));
+                y2 = fmaf(m[3], s0, fmaf(m[7], s1, fmaf(m[11], s2, fmaf(m[15], s3, L[q][3]))));
+            }
+        }
     }
-    // right extension: forward over x = W .. W-1+Ex (input Y(2(W-1)-x)), then backward
+    // right extension: forward over x = W .. W-1+Ex (input Y(2(W-1)-x)), kept
+    // in scratch, then backward over it -> backward start state at x = W-1
     float last = y1;
     float* ext = a.extbuf + (size_t)bt * Ex * H + i;
-    for (int e = 0; e < Ex; ++e) {
-        last = cstep(Y(W - 2 - e), v1, v2, y1, y2, k);
-        ext[(size_t)e * H] = last;
+    for (int eb = 0; eb < Ex; eb += 8) {
+        float u[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = eb + q;
+            u[q] = e < Ex ? ed[(size_t)eidx(W - 2 - e) * H] : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = eb + q;
+            if (e < Ex) {
+                last = cstep(u[q], v1, v2, y1, y2, k);
+                ext[(size_t)e * H] = last;
+            }
+        }
     }
-    float p1 = last, p2 = last, q1 = last, q2 = last;
-    for (int e = Ex - 1; e >= 0; --e) cstep(ext[(size_t)e * H], p1, p2, q1, q2, k);
+    float p1, p2, q1, q2;
+    csteady(last, p1, p2, q1, q2, k);
+    for (int eb = Ex - 1; eb >= 0; eb -= 8) {
+        float u[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = eb - q;
+            u[q] = e >= 0 ? ext[(size_t)e * H] : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (eb - q >= 0) cstep(u[q], p1, p2, q1, q2, k);
+    }
     float* bs = a.bstate + ((size_t)(tp * 4) * a.B + b) * H + i;
     const size_t bq = (size_t)a.B * H;
     bs[0] = p1;
@@ -528,7 +655,7 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2_gauss(const __grid_constan
     const float dnu = a.t.dnu;
     float wt[G];
 #pragma unroll
-    for (int g = 0; g < G; ++g) wt[g] = g < nt ? a.t.w[j0 + g] : 0.f;
+    for (int g = 0; g < G; ++g) wt[g] = g < nt ? a.t.w[j0 + g] * a.wscale : 0.f;
 
     const size_t plane = (size_t)a.B * W * H;
     const float* fl = a.floc + ((size_t)(j0 * 4) * a.B + b) * W * (size_t)H + i;
@@ -869,14 +996,22 @@ __global__ void k_recursive_smooth_f64(const double* a, double* out, int h, int 
     auto S = [&](long long r) -> double& { return s[r * w + xcol]; };
     const double a0 = a[mirror_any(-pad, h) * w + xcol];
     for (int r = 0; r < 4; ++r) S(r) = a0;
+    // Left-to-right, separately rounded products and sums (no FMA contraction),
+    // i.e. the reference's own evaluation order -> bit-identical results.
+    auto dot5 = [&](double x0, double x1, double x2, double x3, double x4) {
+        double t = __dmul_rn(scale, x0);
+        t = __dadd_rn(t, __dmul_rn(c1, x1));
+        t = __dadd_rn(t, __dmul_rn(c2, x2));
+        t = __dadd_rn(t, __dmul_rn(c3, x3));
+        return __dadd_rn(t, __dmul_rn(c4, x4));
+    };
     for (long long r = 0; r < ext; ++r) {
         const long long src = mirror_any(r - pad, h);
-        S(r + 4) = scale * a[src * w + xcol] + c1 * S(r + 3) + c2 * S(r + 2) + c3 * S(r + 1) +
-                   c4 * S(r);
+        S(r + 4) = dot5(a[src * w + xcol], S(r + 3), S(r + 2), S(r + 1), S(r));
     }
     for (long long r = ext + 4; r < ext + 8; ++r) S(r) = S(ext + 3);
     for (long long r = ext - 1; r >= 0; --r)
-        S(r + 4) = scale * S(r + 4) + c1 * S(r + 5) + c2 * S(r + 6) + c3 * S(r + 7) + c4 * S(r + 8);
+        S(r + 4) = dot5(S(r + 4), S(r + 5), S(r + 6), S(r + 7), S(r + 8));
     for (int r = 0; r < h; ++r) out[(long long)r * w + xcol] = S(pad + r + 4);
 }
 
@@ -911,8 +1046,8 @@ __global__ void k_box_pass_f64(const double* a, double* out, int h, int w, int r
 // Host side: plan, workspace layout, launches.
 // ---------------------------------------------------------------------------
 
-constexpr int G1 = 1;  // terms per pass-1 warp == phasor anchor block R
-constexpr int G2 = 2;  // terms per pass-2 thread (multiple of G1)
+constexpr int G1 = 2;  // terms per pass-1 warp == phasor anchor block R
+constexpr int G2 = 4;  // terms per pass-2 thread (multiple of G1)
 constexpr int R_ANCHOR = G1;
 constexpr int TAB_PAD = 16;  // zero padding past the last term of the table
 
@@ -974,8 +1109,8 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     return TBF_OK;
 }
 
-// Zero-input evolution of the cascade: state s=(v1,v2,y1,y2) after `steps`
-// samples (M, column-major) and the output y at each step (Hm).
+// Zero-input evolution of the pure cascade: state s=(v1,v2,y1,y2) after
+// `steps` samples (M, column-major) and the output y at each step (Hm).
 void cascade_responses(const tbf_spatial* sp, int steps, double M[16], double (*Hm)[4]) {
     for (int kk = 0; kk < 4; ++kk) {
         double s[4] = {0, 0, 0, 0};
@@ -985,7 +1120,7 @@ void cascade_responses(const tbf_spatial* sp, int steps, double M[16], double (*
             double v = sp->a1 * v1 + sp->a2 * v2;
             v2 = v1;
             v1 = v;
-            double y = sp->g2 * v + sp->b1 * y1 + sp->b2 * y2;
+            double y = v + sp->b1 * y1 + sp->b2 * y2;
             y2 = y1;
             y1 = y;
             if (Hm) Hm[m][kk] = y;
@@ -998,8 +1133,9 @@ void cascade_responses(const tbf_spatial* sp, int steps, double M[16], double (*
 }
 
 Casc to_casc(const tbf_spatial* sp) {
-    return Casc{(float)sp->g1, (float)sp->a1, (float)sp->a2,
-                (float)sp->g2, (float)sp->b1, (float)sp->b2};
+    const double g = sp->g1 * sp->g2;
+    return Casc{(float)sp->a1, (float)sp->a2, (float)sp->b1, (float)sp->b2,
+                (float)(1.0 / sp->g1), (float)(1.0 / g), (float)(g * g)};
 }
 
 int validate(const tbf_spatial* sp, const tbf_terms* terms, int tbeg, int tend) {
@@ -1158,6 +1294,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.ngroups = (n + G2 - 1) / G2;
         for (int m = 0; m < TILE; ++m)
             for (int q = 0; q < 4; ++q) p2.Hm[m][q] = box ? 0.f : (float)Hm[m][q];
+        p2.wscale = box ? 1.f : (float)(sp->g1 * sp->g2 * sp->g1 * sp->g2);
         p2.floc = floc;
         p2.carry = lc;
         p2.bstate = bst;
