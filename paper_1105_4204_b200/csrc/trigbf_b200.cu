@@ -49,7 +49,7 @@
 namespace {
 
 constexpr int TILE = 32;          // segment length along y == tile width along x == warp size
-constexpr int P1_WARPS = 2;       // warps per pass-1 block (each a different term group)
+constexpr int P1_WARPS = 4;       // warps per pass-1 block (each a different term group)
 constexpr int P2_THREADS = 128;   // rows per pass-2 block
 constexpr int BUF_LD = TILE + 1;  // padded leading dimension of the smem tile
 
@@ -240,6 +240,42 @@ __device__ __forceinline__ void modulate(float fv, const float (&nu_hi)[G], cons
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Block helpers: NB consecutive samples of one line.  Phasors of all NB
+// samples are computed first (independent -> overlapped by the scheduler),
+// then the NB recurrence steps run.  Callers use NB = 8 for full blocks and
+// NB = 1 for remainders, so the hot loops are branch-free.
+// ---------------------------------------------------------------------------
+
+template <int G, int R, int NB>
+__device__ __forceinline__ void fwd_block(const float (&fv)[NB], const float (&nu_hi)[G],
+                                          const float (&nu_lo)[G], float dnu, const Casc& k,
+                                          float (&v1)[4 * G], float (&v2)[4 * G],
+                                          float (&y1)[4 * G], float (&y2)[4 * G],
+                                          float* out_row, int out_stride) {
+    float cc[NB][G], sn[NB][G];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) phasors<G, R>(fv[q], nu_hi, nu_lo, dnu, cc[q], sn[q]);
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const float u0 = cc[q][g], u1 = sn[q][g], u2 = fv[q] * cc[q][g], u3 = fv[q] * sn[q][g];
+            const float o0 = cstep(u0, v1[4 * g + 0], v2[4 * g + 0], y1[4 * g + 0], y2[4 * g + 0], k);
+            const float o1 = cstep(u1, v1[4 * g + 1], v2[4 * g + 1], y1[4 * g + 1], y2[4 * g + 1], k);
+            const float o2 = cstep(u2, v1[4 * g + 2], v2[4 * g + 2], y1[4 * g + 2], y2[4 * g + 2], k);
+            const float o3 = cstep(u3, v1[4 * g + 3], v2[4 * g + 3], y1[4 * g + 3], y2[4 * g + 3], k);
+            if (out_row) {
+                out_row[((4 * g + 0) * TILE + q) * out_stride] = o0;
+                out_row[((4 * g + 1) * TILE + q) * out_stride] = o1;
+                out_row[((4 * g + 2) * TILE + q) * out_stride] = o2;
+                out_row[((4 * g + 3) * TILE + q) * out_stride] = o3;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Kernel arguments
 // ---------------------------------------------------------------------------
@@ -288,6 +324,8 @@ struct Pass2Args {
     int ngroups;       // ceil(t.n / G2)
     float Hm[TILE][4]; // homogeneous response of the cascade to a unit state
     float wscale;      // g^2: undoes the two pure x sweeps (1 for box)
+    int tiles_per_chunk;  // x-chunking of rows (gauss); == ntx for one chunk
+    int warm_tiles;       // warm-up tiles of a chunk's backward sweep
     const float* floc;
     const float* carry;   // chained carries [n*16][B][ntx][H]
     const float* bstate;  // [n*16][B][H]
@@ -358,18 +396,17 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
 #pragma unroll
         for (int p = 0; p < NP; ++p) csteady(u[p], v1[p], v2[p], y1[p], y2[p], k);
     }
-    for (int ib = -Ey; ib < 0; ib += 8) {  // left extension: rows Ey..1
-        float fv[8];
+    {  // left extension: x = -Ey..-1 reads rows Ey..1
+        int ib = -Ey;
+        for (; ib + 8 <= 0; ib += 8) {
+            float fv[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-            fv[q] = ib + q < 0 ? __ldg(fcol + (size_t)(-(ib + q)) * W) : 0.f;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            if (ib + q < 0) {
-                modulate<G, R>(fv[q], nu_hi, nu_lo, dnu, u);
-#pragma unroll
-                for (int p = 0; p < NP; ++p) cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
-            }
+            for (int q = 0; q < 8; ++q) fv[q] = __ldg(fcol + (size_t)(-(ib + q)) * W);
+            fwd_block<G, R, 8>(fv, nu_hi, nu_lo, dnu, k, v1, v2, y1, y2, nullptr, 0);
+        }
+        for (; ib < 0; ++ib) {
+            float fv[1] = {__ldg(fcol + (size_t)(-ib) * W)};
+            fwd_block<G, R, 1>(fv, nu_hi, nu_lo, dnu, k, v1, v2, y1, y2, nullptr, 0);
         }
     }
     for (int seg = 0; seg < a.nseg; ++seg) {
@@ -388,23 +425,19 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
                 }
             }
         }
-        const float* fp = fcol + (size_t)i0 * W;
-        for (int r0 = 0; r0 < len; r0 += 8) {
-            float fv[8];
+        if (inner) {
+            const float* fp = fcol + (size_t)i0 * W;
+#pragma unroll 1
+            for (int r0 = 0; r0 < TILE; r0 += 8) {
+                float fv[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int r = r0 + q;
-                fv[q] = r < len ? __ldg(inner ? fp + (size_t)r * W
-                                              : fcol + (size_t)mirror1(i0 + r, H) * W)
-                                : 0.f;
+                for (int q = 0; q < 8; ++q) fv[q] = __ldg(fp + (size_t)(r0 + q) * W);
+                fwd_block<G, R, 8>(fv, nu_hi, nu_lo, dnu, k, v1, v2, y1, y2, nullptr, 0);
             }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                if (r0 + q < len) {
-                    modulate<G, R>(fv[q], nu_hi, nu_lo, dnu, u);
-#pragma unroll
-                    for (int p = 0; p < NP; ++p) cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
-                }
+        } else {
+            for (int r = 0; r < len; ++r) {
+                float fv[1] = {__ldg(fcol + (size_t)mirror1(i0 + r, H) * W)};
+                fwd_block<G, R, 1>(fv, nu_hi, nu_lo, dnu, k, v1, v2, y1, y2, nullptr, 0);
             }
         }
     }
@@ -430,25 +463,19 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
             }
         }
         // forward recompute of the segment into smem (own column only)
-        const float* fp = fcol + (size_t)i0 * W;
-        for (int r0 = 0; r0 < len; r0 += 8) {
-            float fv[8];
+        if (inner) {
+            const float* fp = fcol + (size_t)i0 * W;
+#pragma unroll 1
+            for (int r0 = 0; r0 < TILE; r0 += 8) {
+                float fv[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int r = r0 + q;
-                fv[q] = r < len ? __ldg(inner ? fp + (size_t)r * W
-                                              : fcol + (size_t)mirror1(i0 + r, H) * W)
-                                : 0.f;
+                for (int q = 0; q < 8; ++q) fv[q] = __ldg(fp + (size_t)(r0 + q) * W);
+                fwd_block<G, R, 8>(fv, nu_hi, nu_lo, dnu, k, v1, v2, y1, y2, bl + r0 * BUF_LD, BUF_LD);
             }
-            float* row = bl + r0 * BUF_LD;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                if (r0 + q < len) {
-                    modulate<G, R>(fv[q], nu_hi, nu_lo, dnu, u);
-#pragma unroll
-                    for (int p = 0; p < NP; ++p)
-                        row[(p * TILE + q) * BUF_LD] = cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
-                }
+        } else {
+            for (int r = 0; r < len; ++r) {
+                float fv[1] = {__ldg(fcol + (size_t)mirror1(i0 + r, H) * W)};
+                fwd_block<G, R, 1>(fv, nu_hi, nu_lo, dnu, k, v1, v2, y1, y2, bl + r * BUF_LD, BUF_LD);
             }
         }
         if (seg == a.nseg - 1) {
@@ -458,16 +485,27 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
                 csteady(bl[(p * TILE + len - 1) * BUF_LD], p1[p], p2[p], q1[p], q2[p], k);
         }
         // backward sweep over the segment, in place
-        for (int r0 = len - 1; r0 >= 0; r0 -= 8) {
-            float* row = bl + r0 * BUF_LD;
+        if (len == TILE) {
+#pragma unroll 1
+            for (int r0 = TILE - 1; r0 >= 0; r0 -= 8) {
+                float* row = bl + r0 * BUF_LD;
+                float in[8][NP];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                if (r0 - q >= 0) {
+                for (int q = 0; q < 8; ++q)
 #pragma unroll
-                    for (int p = 0; p < NP; ++p) {
-                        float* cell = row + (p * TILE - q) * BUF_LD;
-                        *cell = cstep(*cell, p1[p], p2[p], q1[p], q2[p], k);
-                    }
+                    for (int p = 0; p < NP; ++p) in[q][p] = row[(p * TILE - q) * BUF_LD];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+#pragma unroll
+                    for (int p = 0; p < NP; ++p)
+                        row[(p * TILE - q) * BUF_LD] = cstep(in[q][p], p1[p], p2[p], q1[p], q2[p], k);
+            }
+        } else {
+            for (int r = len - 1; r >= 0; --r) {
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    float* cell = bl + (p * TILE + r) * BUF_LD;
+                    *cell = cstep(*cell, p1[p], p2[p], q1[p], q2[p], k);
                 }
             }
         }
@@ -482,23 +520,39 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
             float* fl = a.floc + ((size_t)(j0 * 4) * a.B + b) * W * (size_t)H + (size_t)x0 * H + i;
             const bool edge_tile = a.edge_all || x0 <= a.Ex || x0 + tlen - 1 >= W - 1 - a.Ex;
             float* ed = a.edge + ((size_t)(j0 * 4) * a.B + b) * a.ne * (size_t)H + i;
-            for (int xb = 0; xb < tlen; xb += 8) {
+            if (tlen == TILE && !edge_tile) {
+                float* flp[NP];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int xx = xb + q;
-                    if (xx < tlen) {
-                        const int gx = x0 + xx;
-                        const bool is_edge = edge_tile && (a.edge_all || gx <= a.Ex || gx >= W - 1 - a.Ex);
-                        const int e = a.edge_all ? gx : (gx <= a.Ex ? gx : gx - (W - 1 - a.Ex) + a.Ex + 1);
+                for (int p = 0; p < NP; ++p) flp[p] = fl + (size_t)p * flpl;
+#pragma unroll 1
+                for (int xb = 0; xb < TILE; xb += 8) {
+                    float yv[8][NP];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+#pragma unroll
+                        for (int p = 0; p < NP; ++p) yv[q][p] = br[p * TILE * BUF_LD + xb + q] * k.gg;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
 #pragma unroll
                         for (int p = 0; p < NP; ++p) {
-                            if (p / 4 < nt) {
-                                // undo the 1/g^2 of the two pure y sweeps
-                                const float yv = br[p * TILE * BUF_LD + xx] * k.gg;
-                                fl[(size_t)p * flpl + (size_t)xx * H] =
-                                    cstep(yv, lv1[p], lv2[p], ly1[p], ly2[p], k);
-                                if (is_edge) ed[(size_t)p * edpl + (size_t)e * H] = yv;
-                            }
+                            const float o = cstep(yv[q][p], lv1[p], lv2[p], ly1[p], ly2[p], k);
+                            if (p / 4 < nt) flp[p][(size_t)(xb + q) * H] = o;
+                        }
+                    }
+                }
+            } else {
+                for (int xx = 0; xx < tlen; ++xx) {
+                    const int gx = x0 + xx;
+                    const bool is_edge = edge_tile && (a.edge_all || gx <= a.Ex || gx >= W - 1 - a.Ex);
+                    const int e = a.edge_all ? gx : (gx <= a.Ex ? gx : gx - (W - 1 - a.Ex) + a.Ex + 1);
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        if (p / 4 < nt) {
+                            // undo the 1/g^2 of the two pure y sweeps
+                            const float yv = br[p * TILE * BUF_LD + xx] * k.gg;
+                            fl[(size_t)p * flpl + (size_t)xx * H] =
+                                cstep(yv, lv1[p], lv2[p], ly1[p], ly2[p], k);
+                            if (is_edge) ed[(size_t)p * edpl + (size_t)e * H] = yv;
                         }
                     }
                 }
@@ -634,94 +688,67 @@ __global__ void __launch_bounds__(128) k_chain(const __grid_constant__ ChainArgs
 // output, fused with demodulation + accumulation (engines.py:297-298).
 // ---------------------------------------------------------------------------
 
-template <int G, int R>
-__global__ void __launch_bounds__(P2_THREADS) k_pass2_gauss(const __grid_constant__ Pass2Args a) {
+// One 32-column tile of pass 2, right to left.  OUT = false for warm-up tiles
+// (backward state only).  Steps are processed in blocks of 4: loads and
+// phasors of the 4 steps first, then the 4 recurrence steps (branch-free for
+// full tiles).
+template <int G, int R, bool OUT>
+__device__ __forceinline__ void pass2_tile(const Pass2Args& a, int t, const float* fl,
+                                           const float* fT, const float* cr, size_t plane,
+                                           size_t cq, int nt, const float (&nu_hi)[G],
+                                           const float (&nu_lo)[G], const float (&wt)[G],
+                                           float (&p1)[4 * G], float (&p2)[4 * G],
+                                           float (&q1)[4 * G], float (&q2)[4 * G], bool& init,
+                                           float* pn, float* pd, bool iv) {
     constexpr int NP = 4 * G;
-    const int i_raw = blockIdx.x * P2_THREADS + threadIdx.x;
     const int H = a.H, W = a.W;
-    const bool iv = i_raw < H;
-    const int i = iv ? i_raw : H - 1;
-    const int grp = blockIdx.y;
-    const int b = blockIdx.z;
-    const int j0 = grp * G;
-    const int nt = min(G, a.t.n - j0);
+    const int x0 = t * TILE;
+    const int len = min(TILE, W - x0);
     const Casc k = a.k;
-    float nu_hi[G], nu_lo[G];
+    float C[NP][4];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-        nu_hi[g] = a.t.nu_hi[j0 + g];  // table is padded past n
-        nu_lo[g] = a.t.nu_lo[j0 + g];
-    }
-    const float dnu = a.t.dnu;
-    float wt[G];
+    for (int p = 0; p < NP; ++p)
 #pragma unroll
-    for (int g = 0; g < G; ++g) wt[g] = g < nt ? a.t.w[j0 + g] * a.wscale : 0.f;
-
-    const size_t plane = (size_t)a.B * W * H;
-    const float* fl = a.floc + ((size_t)(j0 * 4) * a.B + b) * W * (size_t)H + i;
-    const float* fT = a.fT + (size_t)b * W * H + i;
-    const size_t cq = (size_t)a.B * a.ntx * H;
-    const float* cr = a.carry + ((size_t)(j0 * 16) * a.B + b) * a.ntx * (size_t)H + i;
-    float p1[NP], p2[NP], q1[NP], q2[NP], C[NP][4];
-    {
-        const size_t bq = (size_t)a.B * H;
-        const float* bs = a.bstate + ((size_t)(j0 * 16) * a.B + b) * H + i;
+        for (int s = 0; s < 4; ++s)
+            C[p][s] = p / 4 < nt ? cr[(size_t)(p * 4 + s) * cq + (size_t)t * H] : 0.f;
+#pragma unroll 1
+    for (int mb = len - 1; mb >= 0; mb -= 4) {
+        float fv[4], fo[4][NP];
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            if (p / 4 < nt) {
-                p1[p] = bs[(size_t)(p * 4 + 0) * bq];
-                p2[p] = bs[(size_t)(p * 4 + 1) * bq];
-                q1[p] = bs[(size_t)(p * 4 + 2) * bq];
-                q2[p] = bs[(size_t)(p * 4 + 3) * bq];
-            } else {
-                p1[p] = p2[p] = q1[p] = q2[p] = 0.f;
-            }
+        for (int q = 0; q < 4; ++q) {
+            const int m = max(mb - q, 0);
+            const size_t off = (size_t)(x0 + m) * H;
+            if (OUT) fv[q] = fT[off];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) fo[q][p] = p / 4 < nt ? fl[(size_t)p * plane + off] : 0.f;
         }
-    }
-    float* pn = a.part + ((size_t)(grp * 2 + 0) * a.B + b) * W * (size_t)H + i_raw;
-    float* pd = a.part + ((size_t)(grp * 2 + 1) * a.B + b) * W * (size_t)H + i_raw;
-
-    for (int t = a.ntx - 1; t >= 0; --t) {
-        const int x0 = t * TILE;
-        const int len = min(TILE, W - x0);
+        float cc[4][G], sn[4][G];
+        if (OUT) {
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-#pragma unroll
-            for (int s = 0; s < 4; ++s)
-                C[p][s] = p / 4 < nt ? cr[(size_t)(p * 4 + s) * cq + (size_t)t * H] : 0.f;
+            for (int q = 0; q < 4; ++q) phasors<G, R>(fv[q], nu_hi, nu_lo, a.t.dnu, cc[q], sn[q]);
         }
-        for (int mb = len - 1; mb >= 0; mb -= 4) {
-            float fv[4], fo[4][NP];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int m = mb - q;
-                const int gx = x0 + (m >= 0 ? m : 0);
-                fv[q] = fT[(size_t)gx * H];
+        for (int q = 0; q < 4; ++q) {
+            const int m = mb - q;
+            if (len == TILE || m >= 0) {  // full tiles: always true (mb = 31, 27, ...)
+                const float h0 = a.Hm[m][0], h1 = a.Hm[m][1], h2 = a.Hm[m][2], h3 = a.Hm[m][3];
+                float yo[NP];
 #pragma unroll
-                for (int p = 0; p < NP; ++p)
-                    fo[q][p] = p / 4 < nt ? fl[(size_t)p * plane + (size_t)gx * H] : 0.f;
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int m = mb - q;
-                if (m >= 0) {
-                    float cc[G], sn[G];
-                    phasors<G, R>(fv[q], nu_hi, nu_lo, dnu, cc, sn);
-                    float yo[NP];
-#pragma unroll
-                    for (int p = 0; p < NP; ++p) {
-                        float F = fo[q][p];
-                        F = fmaf(a.Hm[m][0], C[p][0], F);
-                        F = fmaf(a.Hm[m][1], C[p][1], F);
-                        F = fmaf(a.Hm[m][2], C[p][2], F);
-                        F = fmaf(a.Hm[m][3], C[p][3], F);
-                        yo[p] = cstep(F, p1[p], p2[p], q1[p], q2[p], k);
-                    }
+                for (int p = 0; p < NP; ++p) {
+                    float F = fmaf(h0, C[p][0], fo[q][p]);
+                    F = fmaf(h1, C[p][1], F);
+                    F = fmaf(h2, C[p][2], F);
+                    F = fmaf(h3, C[p][3], F);
+                    if (!init) csteady(F, p1[p], p2[p], q1[p], q2[p], k);
+                    yo[p] = cstep(F, p1[p], p2[p], q1[p], q2[p], k);
+                }
+                init = true;
+                if (OUT) {
                     float num = 0.f, den = 0.f;
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
-                        num = fmaf(wt[g], fmaf(cc[g], yo[4 * g + 2], sn[g] * yo[4 * g + 3]), num);
-                        den = fmaf(wt[g], fmaf(cc[g], yo[4 * g + 0], sn[g] * yo[4 * g + 1]), den);
+                        num = fmaf(wt[g], fmaf(cc[q][g], yo[4 * g + 2], sn[q][g] * yo[4 * g + 3]), num);
+                        den = fmaf(wt[g], fmaf(cc[q][g], yo[4 * g + 0], sn[q][g] * yo[4 * g + 1]), den);
                     }
                     if (iv) {
                         const size_t off = (size_t)(x0 + m) * H;
@@ -732,6 +759,71 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2_gauss(const __grid_constan
             }
         }
     }
+}
+
+// Pass 2 (recursive Gaussian): x-direction backward sweep on the exact forward
+// output (tile-local + H . carry), fused with demodulation + accumulation
+// (engines.py:297-298).  Rows may be split into x-chunks for parallelism:
+// a chunk that does not end at the right edge starts its backward sweep
+// warm_tiles tiles further right from a steady-state guess, which decays
+// below eps = 1e-7 within the decay length K <= 32*warm_tiles samples (the
+// same bound as the mirror truncation).
+template <int G, int R>
+__global__ void __launch_bounds__(P2_THREADS) k_pass2_gauss(const __grid_constant__ Pass2Args a) {
+    constexpr int NP = 4 * G;
+    const int nrb = (a.H + P2_THREADS - 1) / P2_THREADS;
+    const int chunk = blockIdx.x / nrb;
+    const int i_raw = (blockIdx.x % nrb) * P2_THREADS + threadIdx.x;
+    const int H = a.H, W = a.W;
+    const bool iv = i_raw < H;
+    const int i = iv ? i_raw : H - 1;
+    const int grp = blockIdx.y;
+    const int b = blockIdx.z;
+    const int j0 = grp * G;
+    const int nt = min(G, a.t.n - j0);
+    float nu_hi[G], nu_lo[G], wt[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        nu_hi[g] = a.t.nu_hi[j0 + g];  // table is padded past n
+        nu_lo[g] = a.t.nu_lo[j0 + g];
+        wt[g] = g < nt ? a.t.w[j0 + g] * a.wscale : 0.f;
+    }
+    const size_t plane = (size_t)a.B * W * H;
+    const float* fl = a.floc + ((size_t)(j0 * 4) * a.B + b) * W * (size_t)H + i;
+    const float* fT = a.fT + (size_t)b * W * H + i;
+    const size_t cq = (size_t)a.B * a.ntx * H;
+    const float* cr = a.carry + ((size_t)(j0 * 16) * a.B + b) * a.ntx * (size_t)H + i;
+    float* pn = a.part + ((size_t)(grp * 2 + 0) * a.B + b) * W * (size_t)H + i_raw;
+    float* pd = a.part + ((size_t)(grp * 2 + 1) * a.B + b) * W * (size_t)H + i_raw;
+
+    const int t_lo = chunk * a.tiles_per_chunk;
+    const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
+    float p1[NP], p2[NP], q1[NP], q2[NP];
+    bool init = false;
+    int t_start = t_hi - 1;
+    if (t_hi == a.ntx) {  // rightmost chunk: exact start state from the chain
+        const size_t bq = (size_t)a.B * H;
+        const float* bs = a.bstate + ((size_t)(j0 * 16) * a.B + b) * H + i;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const bool ok = p / 4 < nt;
+            p1[p] = ok ? bs[(size_t)(p * 4 + 0) * bq] : 0.f;
+            p2[p] = ok ? bs[(size_t)(p * 4 + 1) * bq] : 0.f;
+            q1[p] = ok ? bs[(size_t)(p * 4 + 2) * bq] : 0.f;
+            q2[p] = ok ? bs[(size_t)(p * 4 + 3) * bq] : 0.f;
+        }
+        init = true;
+    } else {
+        const int tw = min(a.ntx - 1, t_hi - 1 + a.warm_tiles);
+#pragma unroll 1
+        for (int t = tw; t >= t_hi; --t)
+            pass2_tile<G, R, false>(a, t, fl, fT, cr, plane, cq, nt, nu_hi, nu_lo, wt, p1, p2, q1,
+                                    q2, init, pn, pd, iv);
+    }
+#pragma unroll 1
+    for (int t = t_start; t >= t_lo; --t)
+        pass2_tile<G, R, true>(a, t, fl, fT, cr, plane, cq, nt, nu_hi, nu_lo, wt, p1, p2, q1, q2,
+                               init, pn, pd, iv);
 }
 
 // ---------------------------------------------------------------------------
@@ -1046,8 +1138,8 @@ __global__ void k_box_pass_f64(const double* a, double* out, int h, int w, int r
 // Host side: plan, workspace layout, launches.
 // ---------------------------------------------------------------------------
 
-constexpr int G1 = 2;  // terms per pass-1 warp == phasor anchor block R
-constexpr int G2 = 4;  // terms per pass-2 thread (multiple of G1)
+constexpr int G1 = 1;  // terms per pass-1 warp == phasor anchor block R
+constexpr int G2 = 2;  // terms per pass-2 thread (multiple of G1)
 constexpr int R_ANCHOR = G1;
 constexpr int TAB_PAD = 16;  // zero padding past the last term of the table
 
@@ -1299,7 +1391,22 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.carry = lc;
         p2.bstate = bst;
         p2.part = part;
-        dim3 g2((H + P2_THREADS - 1) / P2_THREADS, p2.ngroups, B);
+        // x-chunking of pass-2 rows when rows x groups cannot fill the GPU
+        const int nrb = (H + P2_THREADS - 1) / P2_THREADS;
+        int nchunk = 1;
+        p2.warm_tiles = (std::max(sp->ext_x, 1) + TILE - 1) / TILE;
+        if (!box) {
+            const long long threads = (long long)nrb * P2_THREADS * p2.ngroups * B;
+            const long long target = 148LL * 24 * 32;  // ~24 resident warps per SM
+            while (threads * nchunk < target && nchunk < 64) {
+                const int tpc = (L.ntx + 2 * nchunk - 1) / (2 * nchunk);
+                if (tpc < 2 * p2.warm_tiles) break;  // keep warm-up <= 50% of a chunk
+                nchunk *= 2;
+            }
+        }
+        p2.tiles_per_chunk = (L.ntx + nchunk - 1) / nchunk;
+        nchunk = (L.ntx + p2.tiles_per_chunk - 1) / p2.tiles_per_chunk;
+        dim3 g2(nrb * (box ? 1 : nchunk), p2.ngroups, B);
         {
             Prof pr(KK_PASS2, st);
             if (box)

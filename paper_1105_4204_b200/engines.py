@@ -142,14 +142,20 @@ class TrigFilter:
         budget = WORKSPACE_FRACTION * free
         if self.workspace_bytes(n) <= budget:
             return n
-        w2, w4 = self.workspace_bytes(2), self.workspace_bytes(4)
-        per = max(1, (w4 - w2) // 2)
-        base = w2 - 2 * per
-        tb = int((budget - base) // per) // 2 * 2
-        if tb < 2:
+        # workspace is affine in the batch size (the library rounds batches to
+        # whole pass-2 groups of 4 terms): fit the slope on multiples of 8
+        w8, w16 = self.workspace_bytes(8), self.workspace_bytes(16)
+        per = max(1, (w16 - w8) // 8)
+        base = w8 - 8 * per
+        tb = int((budget - base) // per) // 8 * 8
+        if tb < 8:
+            tb = 4 if self.workspace_bytes(4) <= budget else 0
+        if tb < 1:
             raise ParameterError(
-                f"image too large for device memory: needs {w2 / 2**30:.1f} GiB for 2 terms"
+                f"image too large for device memory: needs {w8 / 2**30:.1f} GiB for 8 terms"
             )
+        while tb > 4 and self.workspace_bytes(tb) > budget:
+            tb -= 4
         return min(tb, n)
 
     # -- calls ------------------------------------------------------------
