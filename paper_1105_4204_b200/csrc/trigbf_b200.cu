@@ -297,10 +297,13 @@ struct Pass1Args {
     Casc k;
     TermDev t;
     int ngroups;    // ceil(t.n / G1)
-    float* ckpt;    // [nseg][n*16][B][W]
-    float* floc;    // [n*4][B][W][H]   tile-local forward along x (transposed)
-    float* lcarry;  // [n*16][B][ntx][H]
-    float* edge;    // [n*4][B][ne][H]  raw y-filtered values at x-edge columns
+    // Gaussian layouts (float4 = the 4 planes of one term, or the 4 states
+    // (v1,v2,y1,y2) of one plane):
+    float* ckpt;    // float4 [nseg][n][B][W][4 planes]
+    float* floc;    // float4 [n][B][W][H]  tile-local forward along x (x-major)
+                    //   (box: planar [n*4][B][W][H] y-filtered values)
+    float* lcarry;  // float4 [n][B][ntx][H][4 planes]
+    float* edge;    // float4 [n][B][ne][H] y-filtered values at x-edge columns
 };
 
 struct ChainArgs {
@@ -310,10 +313,11 @@ struct ChainArgs {
     int nplanes;          // n*4
     float M[16];          // full-tile state transfer (column-major: M[k*4+r])
     float Mlast[16];      // last (possibly partial) tile
-    const float* edge;    // [n*4][B][ne][H]
+    int n;                // terms in the batch
+    const float* edge;    // float4 [n][B][ne][H]
     float* lcarry;        // in: local carries, out: chained carries (state at tile start)
-    float* extbuf;        // [n*4][B][Ex][H]
-    float* bstate;        // [n*16][B][H] backward start state
+    float* extbuf;        // float4 [n][B][Ex][H]
+    float* bstate;        // float4 [n][B][H][4 planes] backward start state
 };
 
 struct Pass2Args {
@@ -327,8 +331,8 @@ struct Pass2Args {
     int tiles_per_chunk;  // x-chunking of rows (gauss); == ntx for one chunk
     int warm_tiles;       // warm-up tiles of a chunk's backward sweep
     const float* floc;
-    const float* carry;   // chained carries [n*16][B][ntx][H]
-    const float* bstate;  // [n*16][B][H]
+    const float* carry;   // chained carries float4 [n][B][ntx][H][4]
+    const float* bstate;  // float4 [n][B][H][4]
     float* part;          // [ngroups*2][B][W][H]
 };
 
@@ -348,18 +352,40 @@ struct ReduceArgs {
 // ---------------------------------------------------------------------------
 // Pass 1 (recursive Gaussian): y-direction forward/backward + x tile-local
 // forward.  Replaces smooth_plane's first 1-D pass (spatial.py:169-170,
-// _core.pyx:56-96) for the 4 auxiliary planes of G terms, fused with their
-// generation (engines.py:272-287).
+// _core.pyx:56-96) for the 4 auxiliary planes of one term, fused with their
+// generation (engines.py:272-287).  One warp = 32 columns x 1 term.
 // ---------------------------------------------------------------------------
 
-template <int G, int R>
+__device__ __forceinline__ float4 f4(float a, float b, float c, float d) {
+    return make_float4(a, b, c, d);
+}
+
+// 8 samples of the forward sweep of one term (phasors first, then the 4
+// plane recurrences); optionally store outputs into the smem segment tile.
+template <bool STORE>
+__device__ __forceinline__ void p1_fwd8(const float (&fv)[8], float nu_hi, float nu_lo,
+                                        const Casc& k, float (&v1)[4], float (&v2)[4],
+                                        float (&y1)[4], float (&y2)[4], float* row) {
+    float cs[8], sn[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sincos_fma(fmaf(nu_hi, fv[q], nu_lo * fv[q]), &sn[q], &cs[q]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const float u[4] = {cs[q], sn[q], fv[q] * cs[q], fv[q] * sn[q]};
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const float o = cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
+            if (STORE) row[(p * TILE + q) * BUF_LD] = o;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_constant__ Pass1Args a) {
-    constexpr int NP = 4 * G;
     extern __shared__ float smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int grp = blockIdx.y * P1_WARPS + warp;
-    if (grp >= a.ngroups) return;  // whole warp; no block-level barriers below
+    const int term = blockIdx.y * P1_WARPS + warp;
+    if (term >= a.t.n) return;  // whole warp; no block-level barriers below
     const int b = blockIdx.z;
     const int H = a.H, W = a.W;
     const int x0 = blockIdx.x * TILE;
@@ -367,121 +393,142 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
     const bool xv = x < W;
     const int xc = xv ? x : W - 1;
     const int tlen = min(TILE, W - x0);
-    const int j0 = grp * G;
-    const int nt = min(G, a.t.n - j0);  // valid terms in this group (1..G)
-    float* const buf = smem + (size_t)warp * NP * TILE * BUF_LD;
+    float* const buf = smem + (size_t)warp * 4 * TILE * BUF_LD;
     float* const bl = buf + lane;           // own column (phases A/B)
     float* const br = buf + lane * BUF_LD;  // own row (epilogue)
-
-    float nu_hi[G], nu_lo[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        nu_hi[g] = a.t.nu_hi[j0 + g];  // table is padded past n
-        nu_lo[g] = a.t.nu_lo[j0 + g];
-    }
-    const float dnu = a.t.dnu;
+    const float nu_hi = a.t.nu_hi[term], nu_lo = a.t.nu_lo[term];
     const Casc k = a.k;
     const int Ey = a.Ey;
-    const int iend = H + Ey;
+    const int iend = H + Ey;  // forward runs over extended rows [-Ey, H+Ey)
     const float* const fcol = a.f + (size_t)b * H * W + xc;
-    const size_t ckq = (size_t)a.B * W;               // stride between state slots
-    const size_t cks = (size_t)a.t.n * 16 * ckq;      // stride between segments
-    float* const ck0 = a.ckpt + (size_t)(j0 * 16) * ckq + (size_t)b * W + xc;
+    auto fload = [&](int i) -> float {  // f at extended row i (mirrored), clamped
+        i = max(-Ey, min(i, iend - 1));
+        return __ldg(fcol + (size_t)mirror1(i, H) * W);
+    };
+    // checkpoints: float4 per plane, [seg][term][b][x][4]
+    float4* const ck0 = reinterpret_cast<float4*>(a.ckpt) +
+                        (((size_t)term * a.B + b) * W + xc) * 4;
+    const size_t cks = (size_t)a.t.n * a.B * W * 4;  // float4 stride between segments
 
-    float v1[NP], v2[NP], y1[NP], y2[NP], u[NP];
-
-    // ---- phase A: forward sweep over the mirrored column, checkpoints ----
+    float v1[4], v2[4], y1[4], y2[4];
     {
-        modulate<G, R>(__ldg(fcol + (size_t)mirror1(-Ey, H) * W), nu_hi, nu_lo, dnu, u);
+        const float f0 = fload(-Ey);
+        float s0, c0;
+        sincos_fma(fmaf(nu_hi, f0, nu_lo * f0), &s0, &c0);
+        const float u[4] = {c0, s0, f0 * c0, f0 * s0};
 #pragma unroll
-        for (int p = 0; p < NP; ++p) csteady(u[p], v1[p], v2[p], y1[p], y2[p], k);
+        for (int p = 0; p < 4; ++p) csteady(u[p], v1[p], v2[p], y1[p], y2[p], k);
     }
-    {  // left extension: x = -Ey..-1 reads rows Ey..1
-        int ib = -Ey;
-        for (; ib + 8 <= 0; ib += 8) {
-            float fv[8];
+
+    // ---- phase A: forward sweep, double-buffered 8-row blocks ----
+    auto step1 = [&](int i) {
+        const float fs = fload(i);
+        float s0, c0;
+        sincos_fma(fmaf(nu_hi, fs, nu_lo * fs), &s0, &c0);
+        const float u[4] = {c0, s0, fs * c0, fs * s0};
 #pragma unroll
-            for (int q = 0; q < 8; ++q) fv[q] = __ldg(fcol + (size_t)(-(ib + q)) * W);
-            fwd_block<G, R, 8>(fv, nu_hi, nu_lo, dnu, k, v1, v2, y1, y2, nullptr, 0);
-        }
-        for (; ib < 0; ++ib) {
-            float fv[1] = {__ldg(fcol + (size_t)(-ib) * W)};
-            fwd_block<G, R, 1>(fv, nu_hi, nu_lo, dnu, k, v1, v2, y1, y2, nullptr, 0);
-        }
-    }
-    for (int seg = 0; seg < a.nseg; ++seg) {
-        const int i0 = seg * TILE;
-        const int len = min(TILE, iend - i0);
-        const bool inner = i0 + TILE <= H;
-        if (xv) {
-            float* ck = ck0 + (size_t)seg * cks;
+        for (int p = 0; p < 4; ++p) cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
+    };
+    {
+        int i = -Ey;
+        for (; i < -Ey + (Ey & 7); ++i) step1(i);  // remainder of the left extension
+        float cur[8];
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                if (p / 4 < nt) {
-                    ck[(size_t)(p * 4 + 0) * ckq] = v1[p];
-                    ck[(size_t)(p * 4 + 1) * ckq] = v2[p];
-                    ck[(size_t)(p * 4 + 2) * ckq] = y1[p];
-                    ck[(size_t)(p * 4 + 3) * ckq] = y2[p];
-                }
-            }
-        }
-        if (inner) {
-            const float* fp = fcol + (size_t)i0 * W;
+        for (int q = 0; q < 8; ++q) cur[q] = fload(i + q);
 #pragma unroll 1
-            for (int r0 = 0; r0 < TILE; r0 += 8) {
-                float fv[8];
+        for (; i < 0; i += 8) {  // rest of the left extension, ends at row 0
+            float nx[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) fv[q] = __ldg(fp + (size_t)(r0 + q) * W);
-                fwd_block<G, R, 8>(fv, nu_hi, nu_lo, dnu, k, v1, v2, y1, y2, nullptr, 0);
+            for (int q = 0; q < 8; ++q) nx[q] = fload(i + 8 + q);
+            p1_fwd8<false>(cur, nu_hi, nu_lo, k, v1, v2, y1, y2, nullptr);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) cur[q] = nx[q];
+        }
+#pragma unroll 1
+        for (int seg = 0; seg < a.nseg; ++seg) {
+            const int i0 = seg * TILE;
+            const int len = min(TILE, iend - i0);
+            if (xv) {
+                float4* ck = ck0 + (size_t)seg * cks;
+#pragma unroll
+                for (int p = 0; p < 4; ++p) ck[p] = f4(v1[p], v2[p], y1[p], y2[p]);
             }
-        } else {
-            for (int r = 0; r < len; ++r) {
-                float fv[1] = {__ldg(fcol + (size_t)mirror1(i0 + r, H) * W)};
-                fwd_block<G, R, 1>(fv, nu_hi, nu_lo, dnu, k, v1, v2, y1, y2, nullptr, 0);
+            if (len == TILE) {
+#pragma unroll 1
+                for (int r0 = 0; r0 < TILE; r0 += 8) {
+                    float nx[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) nx[q] = fload(i0 + r0 + 8 + q);
+                    p1_fwd8<false>(cur, nu_hi, nu_lo, k, v1, v2, y1, y2, nullptr);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) cur[q] = nx[q];
+                }
+            } else {
+                for (int r = 0; r < len; ++r) step1(i0 + r);
             }
         }
     }
 
     // ---- phase B: segments bottom -> top ----
-    float p1[NP], p2[NP], q1[NP], q2[NP];
-    const size_t flpl = (size_t)a.B * W * H;  // plane stride of floc
-    const size_t lcq = (size_t)a.B * a.ntx * H;
-    const size_t edpl = (size_t)a.B * a.ne * H;
+    float p1[4], p2[4], q1[4], q2[4];
+    float4* const fl0 = reinterpret_cast<float4*>(a.floc) + ((size_t)term * a.B + b) * W * (size_t)H;
+    float4* const ed0 = reinterpret_cast<float4*>(a.edge) + ((size_t)term * a.B + b) * a.ne * (size_t)H;
+    float4* const lc0 = reinterpret_cast<float4*>(a.lcarry) +
+                        (((size_t)term * a.B + b) * a.ntx + blockIdx.x) * (size_t)H * 4;
+    float fnx[8];  // prefetch of the first block of the next segment (above)
+    {
+        const int i0 = (a.nseg - 1) * TILE;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) fnx[q] = fload(i0 + q);
+    }
     for (int seg = a.nseg - 1; seg >= 0; --seg) {
         const int i0 = seg * TILE;
         const int len = min(TILE, iend - i0);
-        const bool inner = i0 + TILE <= H;
         {
-            const float* ck = ck0 + (size_t)seg * cks;
+            const float4* ck = ck0 + (size_t)seg * cks;
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                const bool ok = xv && p / 4 < nt;
-                v1[p] = ok ? ck[(size_t)(p * 4 + 0) * ckq] : 0.f;
-                v2[p] = ok ? ck[(size_t)(p * 4 + 1) * ckq] : 0.f;
-                y1[p] = ok ? ck[(size_t)(p * 4 + 2) * ckq] : 0.f;
-                y2[p] = ok ? ck[(size_t)(p * 4 + 3) * ckq] : 0.f;
+            for (int p = 0; p < 4; ++p) {
+                const float4 c = xv ? ck[p] : f4(0.f, 0.f, 0.f, 0.f);
+                v1[p] = c.x;
+                v2[p] = c.y;
+                y1[p] = c.z;
+                y2[p] = c.w;
             }
         }
-        // forward recompute of the segment into smem (own column only)
-        if (inner) {
-            const float* fp = fcol + (size_t)i0 * W;
+        // forward recompute of the segment into smem (own column)
+        if (len == TILE) {
+            float fcur[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) fcur[q] = fnx[q];
 #pragma unroll 1
             for (int r0 = 0; r0 < TILE; r0 += 8) {
-                float fv[8];
+                float fn[8];
+                const int nr = r0 + 8 < TILE ? i0 + r0 + 8 : i0 - TILE;  // next block or next segment
 #pragma unroll
-                for (int q = 0; q < 8; ++q) fv[q] = __ldg(fp + (size_t)(r0 + q) * W);
-                fwd_block<G, R, 8>(fv, nu_hi, nu_lo, dnu, k, v1, v2, y1, y2, bl + r0 * BUF_LD, BUF_LD);
+                for (int q = 0; q < 8; ++q) fn[q] = fload(nr + q);
+                p1_fwd8<true>(fcur, nu_hi, nu_lo, k, v1, v2, y1, y2, bl + r0 * BUF_LD);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) fcur[q] = fn[q];
             }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) fnx[q] = fcur[q];
         } else {
             for (int r = 0; r < len; ++r) {
-                float fv[1] = {__ldg(fcol + (size_t)mirror1(i0 + r, H) * W)};
-                fwd_block<G, R, 1>(fv, nu_hi, nu_lo, dnu, k, v1, v2, y1, y2, bl + r * BUF_LD, BUF_LD);
+                const float fs = fload(i0 + r);
+                float s0, c0;
+                sincos_fma(fmaf(nu_hi, fs, nu_lo * fs), &s0, &c0);
+                const float u[4] = {c0, s0, fs * c0, fs * s0};
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+                    bl[(p * TILE + r) * BUF_LD] = cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
             }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) fnx[q] = fload(i0 - TILE + q);
         }
         if (seg == a.nseg - 1) {
             // backward start = steady state of the last forward output (_core.pyx:85-87)
 #pragma unroll
-            for (int p = 0; p < NP; ++p)
+            for (int p = 0; p < 4; ++p)
                 csteady(bl[(p * TILE + len - 1) * BUF_LD], p1[p], p2[p], q1[p], q2[p], k);
         }
         // backward sweep over the segment, in place
@@ -489,21 +536,21 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
 #pragma unroll 1
             for (int r0 = TILE - 1; r0 >= 0; r0 -= 8) {
                 float* row = bl + r0 * BUF_LD;
-                float in[8][NP];
+                float in[8][4];
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
 #pragma unroll
-                    for (int p = 0; p < NP; ++p) in[q][p] = row[(p * TILE - q) * BUF_LD];
+                    for (int p = 0; p < 4; ++p) in[q][p] = row[(p * TILE - q) * BUF_LD];
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
 #pragma unroll
-                    for (int p = 0; p < NP; ++p)
+                    for (int p = 0; p < 4; ++p)
                         row[(p * TILE - q) * BUF_LD] = cstep(in[q][p], p1[p], p2[p], q1[p], q2[p], k);
             }
         } else {
             for (int r = len - 1; r >= 0; --r) {
 #pragma unroll
-                for (int p = 0; p < NP; ++p) {
+                for (int p = 0; p < 4; ++p) {
                     float* cell = bl + (p * TILE + r) * BUF_LD;
                     *cell = cstep(*cell, p1[p], p2[p], q1[p], q2[p], k);
                 }
@@ -514,93 +561,92 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
         // epilogue: lane <-> row i; tile-local zero-state forward along x
         const int i = i0 + lane;
         if (lane < min(len, H - i0)) {
-            float lv1[NP], lv2[NP], ly1[NP], ly2[NP];
-#pragma unroll
-            for (int p = 0; p < NP; ++p) lv1[p] = lv2[p] = ly1[p] = ly2[p] = 0.f;
-            float* fl = a.floc + ((size_t)(j0 * 4) * a.B + b) * W * (size_t)H + (size_t)x0 * H + i;
+            float lv1[4] = {0.f, 0.f, 0.f, 0.f}, lv2[4] = {0.f, 0.f, 0.f, 0.f};
+            float ly1[4] = {0.f, 0.f, 0.f, 0.f}, ly2[4] = {0.f, 0.f, 0.f, 0.f};
+            float4* fl = fl0 + (size_t)x0 * H + i;
             const bool edge_tile = a.edge_all || x0 <= a.Ex || x0 + tlen - 1 >= W - 1 - a.Ex;
-            float* ed = a.edge + ((size_t)(j0 * 4) * a.B + b) * a.ne * (size_t)H + i;
             if (tlen == TILE && !edge_tile) {
-                float* flp[NP];
-#pragma unroll
-                for (int p = 0; p < NP; ++p) flp[p] = fl + (size_t)p * flpl;
 #pragma unroll 1
                 for (int xb = 0; xb < TILE; xb += 8) {
-                    float yv[8][NP];
+                    float yv[8][4];
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
 #pragma unroll
-                        for (int p = 0; p < NP; ++p) yv[q][p] = br[p * TILE * BUF_LD + xb + q] * k.gg;
+                        for (int p = 0; p < 4; ++p) yv[q][p] = br[p * TILE * BUF_LD + xb + q] * k.gg;
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
+                        float o[4];
 #pragma unroll
-                        for (int p = 0; p < NP; ++p) {
-                            const float o = cstep(yv[q][p], lv1[p], lv2[p], ly1[p], ly2[p], k);
-                            if (p / 4 < nt) flp[p][(size_t)(xb + q) * H] = o;
-                        }
+                        for (int p = 0; p < 4; ++p) o[p] = cstep(yv[q][p], lv1[p], lv2[p], ly1[p], ly2[p], k);
+                        fl[(size_t)(xb + q) * H] = f4(o[0], o[1], o[2], o[3]);
                     }
                 }
             } else {
                 for (int xx = 0; xx < tlen; ++xx) {
                     const int gx = x0 + xx;
-                    const bool is_edge = edge_tile && (a.edge_all || gx <= a.Ex || gx >= W - 1 - a.Ex);
-                    const int e = a.edge_all ? gx : (gx <= a.Ex ? gx : gx - (W - 1 - a.Ex) + a.Ex + 1);
+                    float yv[4], o[4];
 #pragma unroll
-                    for (int p = 0; p < NP; ++p) {
-                        if (p / 4 < nt) {
-                            // undo the 1/g^2 of the two pure y sweeps
-                            const float yv = br[p * TILE * BUF_LD + xx] * k.gg;
-                            fl[(size_t)p * flpl + (size_t)xx * H] =
-                                cstep(yv, lv1[p], lv2[p], ly1[p], ly2[p], k);
-                            if (is_edge) ed[(size_t)p * edpl + (size_t)e * H] = yv;
-                        }
+                    for (int p = 0; p < 4; ++p) {
+                        // undo the 1/g^2 of the two pure y sweeps
+                        yv[p] = br[p * TILE * BUF_LD + xx] * k.gg;
+                        o[p] = cstep(yv[p], lv1[p], lv2[p], ly1[p], ly2[p], k);
+                    }
+                    fl[(size_t)xx * H] = f4(o[0], o[1], o[2], o[3]);
+                    if (a.edge_all || gx <= a.Ex || gx >= W - 1 - a.Ex) {
+                        const int e = a.edge_all ? gx : (gx <= a.Ex ? gx : gx - (W - 1 - a.Ex) + a.Ex + 1);
+                        ed0[(size_t)e * H + i] = f4(yv[0], yv[1], yv[2], yv[3]);
                     }
                 }
             }
-            float* lc = a.lcarry + ((size_t)(j0 * 16) * a.B + b) * a.ntx * (size_t)H +
-                        (size_t)blockIdx.x * H + i;
+            float4* lc = lc0 + (size_t)i * 4;
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                if (p / 4 < nt) {
-                    lc[(size_t)(p * 4 + 0) * lcq] = lv1[p];
-                    lc[(size_t)(p * 4 + 1) * lcq] = lv2[p];
-                    lc[(size_t)(p * 4 + 2) * lcq] = ly1[p];
-                    lc[(size_t)(p * 4 + 3) * lcq] = ly2[p];
-                }
-            }
+            for (int p = 0; p < 4; ++p) lc[p] = f4(lv1[p], lv2[p], ly1[p], ly2[p]);
         }
         __syncwarp();
     }
 }
 
 // ---------------------------------------------------------------------------
-// Chain: per (row, plane) the x-direction carries and the mirrored x-extension
-// (spatial.py:171 with pad = W-1 truncated to ext_x, _core.pyx:56-96).
+// Chain: per (row, term) the x-direction carries of the 4 planes and the
+// mirrored x-extension (spatial.py:171 with pad = W-1 truncated to ext_x,
+// _core.pyx:56-96).
 // ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void cstep4(const float4& u, float (&v1)[4], float (&v2)[4],
+                                       float (&y1)[4], float (&y2)[4], const Casc& k,
+                                       float (&o)[4]) {
+    o[0] = cstep(u.x, v1[0], v2[0], y1[0], y2[0], k);
+    o[1] = cstep(u.y, v1[1], v2[1], y1[1], y2[1], k);
+    o[2] = cstep(u.z, v1[2], v2[2], y1[2], y2[2], k);
+    o[3] = cstep(u.w, v1[3], v2[3], y1[3], y2[3], k);
+}
 
 __global__ void __launch_bounds__(128) k_chain(const __grid_constant__ ChainArgs a) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.H) return;
-    const int bt = blockIdx.y;  // tp * B + b
+    const int bt = blockIdx.y;  // term * B + b
     const int H = a.H, W = a.W, Ex = a.Ex;
     const Casc k = a.k;
-    const float* ed = a.edge + (size_t)bt * a.ne * H + i;
+    const float4* ed = reinterpret_cast<const float4*>(a.edge) + (size_t)bt * a.ne * H + i;
     auto eidx = [&](int xx) -> int {
         return a.edge_all ? xx : (xx <= Ex ? xx : xx - (W - 1 - Ex) + Ex + 1);
     };
-    float v1, v2, y1, y2;
-    csteady(ed[(size_t)eidx(Ex) * H], v1, v2, y1, y2, k);  // mirror(-Ex)
-    // left extension x = -Ex..-1 reads Y(-x); chunks of 8 loads in flight
+    float v1[4], v2[4], y1[4], y2[4], o[4];
+    {
+        const float4 u = ed[(size_t)eidx(Ex) * H];  // mirror(-Ex)
+        csteady(u.x, v1[0], v2[0], y1[0], y2[0], k);
+        csteady(u.y, v1[1], v2[1], y1[1], y2[1], k);
+        csteady(u.z, v1[2], v2[2], y1[2], y2[2], k);
+        csteady(u.w, v1[3], v2[3], y1[3], y2[3], k);
+    }
+    // left extension x = -Ex..-1 reads Y(-x); 8 loads in flight
     for (int xb = -Ex; xb < 0; xb += 8) {
-        float u[8];
+        float4 u[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int xx = xb + q;
-            u[q] = xx < 0 ? ed[(size_t)eidx(-xx) * H] : 0.f;
-        }
+        for (int q = 0; q < 8; ++q) u[q] = ed[(size_t)eidx(max(1, -(xb + q))) * H];
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-            if (xb + q < 0) cstep(u[q], v1, v2, y1, y2, k);
+            if (xb + q < 0) cstep4(u[q], v1, v2, y1, y2, k, o);
     }
     // chain along x: C_t = state at tile start; s_{t+1} = M s_t + L_t
     float M[16], Ml[16];
@@ -609,168 +655,175 @@ __global__ void __launch_bounds__(128) k_chain(const __grid_constant__ ChainArgs
         M[q] = a.M[q];
         Ml[q] = a.Mlast[q];
     }
-    const int tp = bt / a.B, b = bt % a.B;
-    const size_t q_stride = (size_t)a.B * a.ntx * H;
-    float* lc = a.lcarry + ((size_t)(tp * 4) * a.B + b) * a.ntx * (size_t)H + i;
-    for (int tb = 0; tb < a.ntx; tb += 8) {
-        float L[8][4];
+    float4* lc = reinterpret_cast<float4*>(a.lcarry) + ((size_t)bt * a.ntx * H + i) * 4;
+    const size_t tstride = (size_t)H * 4;  // float4 stride between tiles
+    for (int tb = 0; tb < a.ntx; tb += 4) {
+        float4 L[4][4];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int t = tb + q;
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
-                L[q][r] = t < a.ntx ? lc[(size_t)t * H + r * q_stride] : 0.f;
-        }
+            for (int p = 0; p < 4; ++p)
+                L[q][p] = tb + q < a.ntx ? lc[(size_t)(tb + q) * tstride + p] : f4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 4; ++q) {
             const int t = tb + q;
             if (t < a.ntx) {
-                float* c = lc + (size_t)t * H;
-                c[0] = v1;
-                c[q_stride] = v2;
-                c[2 * q_stride] = y1;
-                c[3 * q_stride] = y2;
                 const bool last = t == a.ntx - 1;
-                float s0 = v1, s1 = v2, s2 = y1, s3 = y2;
-                float m[16];
 #pragma unroll
-                for (int r = 0; r < 16; ++r) m[r] = last ? Ml[r] : M[r];
-                v1 = fmaf(m[0], s0, fmaf(m[4], s1, fmaf(m[8], s2, fmaf(m[12], s3, L[q][0]))));
-                v2 = fmaf(m[1], s0, fmaf(m[5], s1, fmaf(m[9], s2, fmaf(m[13], s3, L[q][1]))));
-                y1 = fmaf(m[2], s0, fmaf(m[6], s1, fmaf(m[10], s2, fmaf(m[14], s3, L[q][2]))));
-                y2 = fmaf(m[3], s0, fmaf(m[7], s1, fmaf(m[11], s2, fmaf(m[15], s3, L[q][3]))));
+                for (int p = 0; p < 4; ++p) {
+                    lc[(size_t)t * tstride + p] = f4(v1[p], v2[p], y1[p], y2[p]);
+                    const float s0 = v1[p], s1 = v2[p], s2 = y1[p], s3 = y2[p];
+                    float m[16];
+#pragma unroll
+                    for (int r = 0; r < 16; ++r) m[r] = last ? Ml[r] : M[r];
+                    v1[p] = fmaf(m[0], s0, fmaf(m[4], s1, fmaf(m[8], s2, fmaf(m[12], s3, L[q][p].x))));
+                    v2[p] = fmaf(m[1], s0, fmaf(m[5], s1, fmaf(m[9], s2, fmaf(m[13], s3, L[q][p].y))));
+                    y1[p] = fmaf(m[2], s0, fmaf(m[6], s1, fmaf(m[10], s2, fmaf(m[14], s3, L[q][p].z))));
+                    y2[p] = fmaf(m[3], s0, fmaf(m[7], s1, fmaf(m[11], s2, fmaf(m[15], s3, L[q][p].w))));
+                }
             }
         }
     }
-    // right extension: forward over x = W .. W-1+Ex (input Y(2(W-1)-x)), kept
-    // in scratch, then backward over it -> backward start state at x = W-1
-    float last = y1;
-    float* ext = a.extbuf + (size_t)bt * Ex * H + i;
+    // right extension: forward over x = W .. W-1+Ex (input Y(2(W-1)-x)) into
+    // scratch, then backward over it -> backward start state at x = W-1
+    float last[4] = {y1[0], y1[1], y1[2], y1[3]};
+    float4* ext = reinterpret_cast<float4*>(a.extbuf) + (size_t)bt * Ex * H + i;
     for (int eb = 0; eb < Ex; eb += 8) {
-        float u[8];
+        float4 u[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) u[q] = ed[(size_t)eidx(max(0, W - 2 - min(eb + q, Ex - 1))) * H];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const int e = eb + q;
-            u[q] = e < Ex ? ed[(size_t)eidx(W - 2 - e) * H] : 0.f;
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int e = eb + q;
-            if (e < Ex) {
-                last = cstep(u[q], v1, v2, y1, y2, k);
-                ext[(size_t)e * H] = last;
+            if (eb + q < Ex) {
+                cstep4(u[q], v1, v2, y1, y2, k, last);
+                ext[(size_t)(eb + q) * H] = f4(last[0], last[1], last[2], last[3]);
             }
         }
     }
-    float p1, p2, q1, q2;
-    csteady(last, p1, p2, q1, q2, k);
-    for (int eb = Ex - 1; eb >= 0; eb -= 8) {
-        float u[8];
+    float p1[4], p2[4], q1[4], q2[4];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int e = eb - q;
-            u[q] = e >= 0 ? ext[(size_t)e * H] : 0.f;
-        }
+    for (int p = 0; p < 4; ++p) csteady(last[p], p1[p], p2[p], q1[p], q2[p], k);
+    for (int eb = Ex - 1; eb >= 0; eb -= 8) {
+        float4 u[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) u[q] = ext[(size_t)max(eb - q, 0) * H];
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-            if (eb - q >= 0) cstep(u[q], p1, p2, q1, q2, k);
+            if (eb - q >= 0) cstep4(u[q], p1, p2, q1, q2, k, o);
     }
-    float* bs = a.bstate + ((size_t)(tp * 4) * a.B + b) * H + i;
-    const size_t bq = (size_t)a.B * H;
-    bs[0] = p1;
-    bs[bq] = p2;
-    bs[2 * bq] = q1;
-    bs[3 * bq] = q2;
+    float4* bs = reinterpret_cast<float4*>(a.bstate) + ((size_t)bt * H + i) * 4;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) bs[p] = f4(p1[p], p2[p], q1[p], q2[p]);
 }
 
 // ---------------------------------------------------------------------------
 // Pass 2 (recursive Gaussian): x-direction backward sweep on the exact forward
-// output, fused with demodulation + accumulation (engines.py:297-298).
+// output (tile-local + H . carry), fused with demodulation + accumulation
+// (engines.py:297-298).  One thread = one row x G terms.
 // ---------------------------------------------------------------------------
 
-// One 32-column tile of pass 2, right to left.  OUT = false for warm-up tiles
-// (backward state only).  Steps are processed in blocks of 4: loads and
-// phasors of the 4 steps first, then the 4 recurrence steps (branch-free for
-// full tiles).
-template <int G, int R, bool OUT>
-__device__ __forceinline__ void pass2_tile(const Pass2Args& a, int t, const float* fl,
-                                           const float* fT, const float* cr, size_t plane,
-                                           size_t cq, int nt, const float (&nu_hi)[G],
-                                           const float (&nu_lo)[G], const float (&wt)[G],
-                                           float (&p1)[4 * G], float (&p2)[4 * G],
-                                           float (&q1)[4 * G], float (&q2)[4 * G], bool& init,
-                                           float* pn, float* pd, bool iv) {
-    constexpr int NP = 4 * G;
-    const int H = a.H, W = a.W;
-    const int x0 = t * TILE;
-    const int len = min(TILE, W - x0);
+template <int G>
+struct P2Ctx {
+    const float4* fl[G];  // this row, x = 0, per term
+    const float* fT;
+    const float4* cr[G];  // chained carries, this row, tile 0, per term
+    size_t H;             // float4 stride between x
+    float nu_hi[G], nu_lo[G], wt[G];
+};
+
+// Loads of one 4-step block (x = x0+m, m = mb, mb-1, .., mb-3; clamped).
+template <int G, bool OUT>
+__device__ __forceinline__ void p2_load4(const P2Ctx<G>& c, int x0, int mb, float4 (&fo)[4][G],
+                                         float (&fv)[4]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const size_t off = (size_t)(x0 + max(mb - q, 0)) * c.H;
+#pragma unroll
+        for (int g = 0; g < G; ++g) fo[q][g] = c.fl[g][off];
+        if (OUT) fv[q] = c.fT[off];
+    }
+}
+
+template <int G, bool OUT>
+__device__ __forceinline__ void p2_step4(const Pass2Args& a, const P2Ctx<G>& c, int x0, int mb,
+                                         bool full, const float4 (&fo)[4][G], const float (&fv)[4],
+                                         const float (&C)[G][4][4], float (&p1)[G][4],
+                                         float (&p2)[G][4], float (&q1)[G][4], float (&q2)[G][4],
+                                         float* pn, float* pd, bool iv) {
     const Casc k = a.k;
-    float C[NP][4];
+    float cs[4][G], sn[4][G];
+    if (OUT) {
 #pragma unroll
-    for (int p = 0; p < NP; ++p)
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int s = 0; s < 4; ++s)
-            C[p][s] = p / 4 < nt ? cr[(size_t)(p * 4 + s) * cq + (size_t)t * H] : 0.f;
-#pragma unroll 1
-    for (int mb = len - 1; mb >= 0; mb -= 4) {
-        float fv[4], fo[4][NP];
+            for (int g = 0; g < G; ++g)
+                sincos_fma(fmaf(c.nu_hi[g], fv[q], c.nu_lo[g] * fv[q]), &sn[q][g], &cs[q][g]);
+    }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int m = max(mb - q, 0);
-            const size_t off = (size_t)(x0 + m) * H;
-            if (OUT) fv[q] = fT[off];
+    for (int q = 0; q < 4; ++q) {
+        const int m = mb - q;
+        if (full || m >= 0) {
+            const float4 h = *reinterpret_cast<const float4*>(&a.Hm[m][0]);
+            float num = 0.f, den = 0.f;
 #pragma unroll
-            for (int p = 0; p < NP; ++p) fo[q][p] = p / 4 < nt ? fl[(size_t)p * plane + off] : 0.f;
-        }
-        float cc[4][G], sn[4][G];
-        if (OUT) {
+            for (int g = 0; g < G; ++g) {
+                const float fin[4] = {fo[q][g].x, fo[q][g].y, fo[q][g].z, fo[q][g].w};
+                float y[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) phasors<G, R>(fv[q], nu_hi, nu_lo, a.t.dnu, cc[q], sn[q]);
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int m = mb - q;
-            if (len == TILE || m >= 0) {  // full tiles: always true (mb = 31, 27, ...)
-                const float h0 = a.Hm[m][0], h1 = a.Hm[m][1], h2 = a.Hm[m][2], h3 = a.Hm[m][3];
-                float yo[NP];
-#pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    float F = fmaf(h0, C[p][0], fo[q][p]);
-                    F = fmaf(h1, C[p][1], F);
-                    F = fmaf(h2, C[p][2], F);
-                    F = fmaf(h3, C[p][3], F);
-                    if (!init) csteady(F, p1[p], p2[p], q1[p], q2[p], k);
-                    yo[p] = cstep(F, p1[p], p2[p], q1[p], q2[p], k);
+                for (int p = 0; p < 4; ++p) {
+                    float F = fmaf(h.x, C[g][p][0], fin[p]);
+                    F = fmaf(h.y, C[g][p][1], F);
+                    F = fmaf(h.z, C[g][p][2], F);
+                    F = fmaf(h.w, C[g][p][3], F);
+                    y[p] = cstep(F, p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
                 }
-                init = true;
                 if (OUT) {
-                    float num = 0.f, den = 0.f;
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        num = fmaf(wt[g], fmaf(cc[q][g], yo[4 * g + 2], sn[q][g] * yo[4 * g + 3]), num);
-                        den = fmaf(wt[g], fmaf(cc[q][g], yo[4 * g + 0], sn[q][g] * yo[4 * g + 1]), den);
-                    }
-                    if (iv) {
-                        const size_t off = (size_t)(x0 + m) * H;
-                        pn[off] = num;
-                        pd[off] = den;
-                    }
+                    num = fmaf(c.wt[g], fmaf(cs[q][g], y[2], sn[q][g] * y[3]), num);
+                    den = fmaf(c.wt[g], fmaf(cs[q][g], y[0], sn[q][g] * y[1]), den);
                 }
+            }
+            if (OUT && iv) {
+                const size_t off = (size_t)(x0 + m) * c.H;
+                pn[off] = num;
+                pd[off] = den;
             }
         }
     }
 }
 
-// Pass 2 (recursive Gaussian): x-direction backward sweep on the exact forward
-// output (tile-local + H . carry), fused with demodulation + accumulation
-// (engines.py:297-298).  Rows may be split into x-chunks for parallelism:
-// a chunk that does not end at the right edge starts its backward sweep
-// warm_tiles tiles further right from a steady-state guess, which decays
-// below eps = 1e-7 within the decay length K <= 32*warm_tiles samples (the
-// same bound as the mirror truncation).
-template <int G, int R>
+template <int G, bool OUT>
+__device__ __forceinline__ void p2_tile(const Pass2Args& a, const P2Ctx<G>& c, int t,
+                                        float (&p1)[G][4], float (&p2)[G][4], float (&q1)[G][4],
+                                        float (&q2)[G][4], float* pn, float* pd, bool iv) {
+    const int x0 = t * TILE;
+    const int len = min(TILE, a.W - x0);
+    float C[G][4][4];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const float4 v = c.cr[g][(size_t)t * c.H * 4 + p];
+            C[g][p][0] = v.x;
+            C[g][p][1] = v.y;
+            C[g][p][2] = v.z;
+            C[g][p][3] = v.w;
+        }
+    const bool full = len == TILE;
+    float4 fa[4][G], fb[4][G];
+    float va[4], vb[4];
+    p2_load4<G, OUT>(c, x0, len - 1, fa, va);
+#pragma unroll 1
+    for (int mb = len - 1; mb >= 0; mb -= 8) {
+        p2_load4<G, OUT>(c, x0, mb - 4, fb, vb);
+        p2_step4<G, OUT>(a, c, x0, mb, full, fa, va, C, p1, p2, q1, q2, pn, pd, iv);
+        if (mb - 4 < 0) break;
+        p2_load4<G, OUT>(c, x0, mb - 8, fa, va);
+        p2_step4<G, OUT>(a, c, x0, mb - 4, full, fb, vb, C, p1, p2, q1, q2, pn, pd, iv);
+    }
+}
+
+template <int G>
 __global__ void __launch_bounds__(P2_THREADS) k_pass2_gauss(const __grid_constant__ Pass2Args a) {
-    constexpr int NP = 4 * G;
     const int nrb = (a.H + P2_THREADS - 1) / P2_THREADS;
     const int chunk = blockIdx.x / nrb;
     const int i_raw = (blockIdx.x % nrb) * P2_THREADS + threadIdx.x;
@@ -781,49 +834,61 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2_gauss(const __grid_constan
     const int b = blockIdx.z;
     const int j0 = grp * G;
     const int nt = min(G, a.t.n - j0);
-    float nu_hi[G], nu_lo[G], wt[G];
+    P2Ctx<G> c;
+    c.H = (size_t)H;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-        nu_hi[g] = a.t.nu_hi[j0 + g];  // table is padded past n
-        nu_lo[g] = a.t.nu_lo[j0 + g];
-        wt[g] = g < nt ? a.t.w[j0 + g] * a.wscale : 0.f;
+        const int j = min(j0 + g, a.t.n - 1);  // padded terms alias the last one (weight 0)
+        c.nu_hi[g] = a.t.nu_hi[j];
+        c.nu_lo[g] = a.t.nu_lo[j];
+        c.wt[g] = g < nt ? a.t.w[j] * a.wscale : 0.f;
+        c.fl[g] = reinterpret_cast<const float4*>(a.floc) + ((size_t)j * a.B + b) * W * (size_t)H + i;
+        c.cr[g] = reinterpret_cast<const float4*>(a.carry) + (((size_t)j * a.B + b) * a.ntx * H + i) * 4;
     }
-    const size_t plane = (size_t)a.B * W * H;
-    const float* fl = a.floc + ((size_t)(j0 * 4) * a.B + b) * W * (size_t)H + i;
-    const float* fT = a.fT + (size_t)b * W * H + i;
-    const size_t cq = (size_t)a.B * a.ntx * H;
-    const float* cr = a.carry + ((size_t)(j0 * 16) * a.B + b) * a.ntx * (size_t)H + i;
+    c.fT = a.fT + (size_t)b * W * H + i;
     float* pn = a.part + ((size_t)(grp * 2 + 0) * a.B + b) * W * (size_t)H + i_raw;
     float* pd = a.part + ((size_t)(grp * 2 + 1) * a.B + b) * W * (size_t)H + i_raw;
 
     const int t_lo = chunk * a.tiles_per_chunk;
     const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
-    float p1[NP], p2[NP], q1[NP], q2[NP];
-    bool init = false;
-    int t_start = t_hi - 1;
+    float p1[G][4], p2[G][4], q1[G][4], q2[G][4];
     if (t_hi == a.ntx) {  // rightmost chunk: exact start state from the chain
-        const size_t bq = (size_t)a.B * H;
-        const float* bs = a.bstate + ((size_t)(j0 * 16) * a.B + b) * H + i;
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            const bool ok = p / 4 < nt;
-            p1[p] = ok ? bs[(size_t)(p * 4 + 0) * bq] : 0.f;
-            p2[p] = ok ? bs[(size_t)(p * 4 + 1) * bq] : 0.f;
-            q1[p] = ok ? bs[(size_t)(p * 4 + 2) * bq] : 0.f;
-            q2[p] = ok ? bs[(size_t)(p * 4 + 3) * bq] : 0.f;
+        for (int g = 0; g < G; ++g) {
+            const int j = min(j0 + g, a.t.n - 1);
+            const float4* bs = reinterpret_cast<const float4*>(a.bstate) + (((size_t)j * a.B + b) * H + i) * 4;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const float4 v = bs[p];
+                p1[g][p] = v.x;
+                p2[g][p] = v.y;
+                q1[g][p] = v.z;
+                q2[g][p] = v.w;
+            }
         }
-        init = true;
     } else {
+        // warm-up: start from the steady state of the exact forward output at
+        // the warm-up start, then run backward (no output) down to t_hi
         const int tw = min(a.ntx - 1, t_hi - 1 + a.warm_tiles);
+        const int xs = min(W - 1, tw * TILE + TILE - 1);
+        const int ms = xs - tw * TILE;
+        const float4 h = *reinterpret_cast<const float4*>(&a.Hm[ms][0]);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const float4 F = c.fl[g][(size_t)xs * c.H];
+            const float fin[4] = {F.x, F.y, F.z, F.w};
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const float4 cv = c.cr[g][(size_t)tw * c.H * 4 + p];
+                const float v = fmaf(h.x, cv.x, fmaf(h.y, cv.y, fmaf(h.z, cv.z, fmaf(h.w, cv.w, fin[p]))));
+                csteady(v, p1[g][p], p2[g][p], q1[g][p], q2[g][p], a.k);
+            }
+        }
 #pragma unroll 1
-        for (int t = tw; t >= t_hi; --t)
-            pass2_tile<G, R, false>(a, t, fl, fT, cr, plane, cq, nt, nu_hi, nu_lo, wt, p1, p2, q1,
-                                    q2, init, pn, pd, iv);
+        for (int t = tw; t >= t_hi; --t) p2_tile<G, false>(a, c, t, p1, p2, q1, q2, pn, pd, iv);
     }
 #pragma unroll 1
-    for (int t = t_start; t >= t_lo; --t)
-        pass2_tile<G, R, true>(a, t, fl, fT, cr, plane, cq, nt, nu_hi, nu_lo, wt, p1, p2, q1, q2,
-                               init, pn, pd, iv);
+    for (int t = t_hi - 1; t >= t_lo; --t) p2_tile<G, true>(a, c, t, p1, p2, q1, q2, pn, pd, iv);
 }
 
 // ---------------------------------------------------------------------------
@@ -1248,8 +1313,7 @@ constexpr int P1_SMEM = P1_WARPS * 4 * G1 * TILE * BUF_LD * 4;
 void set_p1_smem() {
     static bool done = false;
     if (done) return;
-    cudaFuncSetAttribute(k_pass1_gauss<G1, R_ANCHOR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         P1_SMEM);
+    cudaFuncSetAttribute(k_pass1_gauss, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM);
     cudaFuncSetAttribute(k_pass1_box<G1, R_ANCHOR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          P1_SMEM);
     done = true;
@@ -1347,7 +1411,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             if (box)
                 k_pass1_box<G1, R_ANCHOR><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1, sp->radius);
             else
-                k_pass1_gauss<G1, R_ANCHOR><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1);
+                k_pass1_gauss<<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1);
         }
         if ((rc = check_cuda("pass1"))) return rc;
 
@@ -1362,6 +1426,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             ca.ntx = L.ntx;
             ca.k = kc;
             ca.nplanes = n * 4;
+            ca.n = n;
             for (int q = 0; q < 16; ++q) {
                 ca.M[q] = (float)M[q];
                 ca.Mlast[q] = (float)Mlast[q];
@@ -1370,7 +1435,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             ca.lcarry = lc;
             ca.extbuf = ext;
             ca.bstate = bst;
-            dim3 gc((H + 127) / 128, n * 4 * B);
+            dim3 gc((H + 127) / 128, n * B);
             { Prof pr(KK_CHAIN, st); k_chain<<<gc, 128, 0, st>>>(ca); }
             if ((rc = check_cuda("chain"))) return rc;
         }
@@ -1412,7 +1477,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             if (box)
                 k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, st>>>(p2, sp->radius);
             else
-                k_pass2_gauss<G2, R_ANCHOR><<<g2, P2_THREADS, 0, st>>>(p2);
+                k_pass2_gauss<G2><<<g2, P2_THREADS, 0, st>>>(p2);
         }
         if ((rc = check_cuda("pass2"))) return rc;
 
