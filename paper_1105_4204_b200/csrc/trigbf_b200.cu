@@ -444,6 +444,10 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
 #pragma unroll
             for (int q = 0; q < 8; ++q) cur[q] = nx[q];
         }
+        // segments: f of the next segment is loaded one whole segment ahead
+        float seg_f[TILE];
+#pragma unroll
+        for (int q = 0; q < TILE; ++q) seg_f[q] = fload(q);
 #pragma unroll 1
         for (int seg = 0; seg < a.nseg; ++seg) {
             const int i0 = seg * TILE;
@@ -454,15 +458,18 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
                 for (int p = 0; p < 4; ++p) ck[p] = f4(v1[p], v2[p], y1[p], y2[p]);
             }
             if (len == TILE) {
-#pragma unroll 1
+                float nxt[TILE];
+#pragma unroll
+                for (int q = 0; q < TILE; ++q) nxt[q] = fload(i0 + TILE + q);
+#pragma unroll
                 for (int r0 = 0; r0 < TILE; r0 += 8) {
-                    float nx[8];
+                    float fb[8];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) nx[q] = fload(i0 + r0 + 8 + q);
-                    p1_fwd8<false>(cur, nu_hi, nu_lo, k, v1, v2, y1, y2, nullptr);
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) cur[q] = nx[q];
+                    for (int q = 0; q < 8; ++q) fb[q] = seg_f[r0 + q];
+                    p1_fwd8<false>(fb, nu_hi, nu_lo, k, v1, v2, y1, y2, nullptr);
                 }
+#pragma unroll
+                for (int q = 0; q < TILE; ++q) seg_f[q] = nxt[q];
             } else {
                 for (int r = 0; r < len; ++r) step1(i0 + r);
             }
@@ -475,43 +482,46 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
     float4* const ed0 = reinterpret_cast<float4*>(a.edge) + ((size_t)term * a.B + b) * a.ne * (size_t)H;
     float4* const lc0 = reinterpret_cast<float4*>(a.lcarry) +
                         (((size_t)term * a.B + b) * a.ntx + blockIdx.x) * (size_t)H * 4;
-    float fnx[8];  // prefetch of the first block of the next segment (above)
+    // prefetch (one segment ahead): f rows and the forward checkpoint
+    float seg_f[TILE];
+    float4 ckn[4];
     {
         const int i0 = (a.nseg - 1) * TILE;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) fnx[q] = fload(i0 + q);
+        for (int q = 0; q < TILE; ++q) seg_f[q] = fload(i0 + q);
+        const float4* ck = ck0 + (size_t)(a.nseg - 1) * cks;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) ckn[p] = ck[p];
     }
+#pragma unroll 1
     for (int seg = a.nseg - 1; seg >= 0; --seg) {
         const int i0 = seg * TILE;
         const int len = min(TILE, iend - i0);
-        {
-            const float4* ck = ck0 + (size_t)seg * cks;
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                const float4 c = xv ? ck[p] : f4(0.f, 0.f, 0.f, 0.f);
-                v1[p] = c.x;
-                v2[p] = c.y;
-                y1[p] = c.z;
-                y2[p] = c.w;
-            }
+        for (int p = 0; p < 4; ++p) {
+            v1[p] = ckn[p].x;
+            v2[p] = ckn[p].y;
+            y1[p] = ckn[p].z;
+            y2[p] = ckn[p].w;
+        }
+        float nxt[TILE];
+        {
+            const int sn = max(seg - 1, 0);
+#pragma unroll
+            for (int q = 0; q < TILE; ++q) nxt[q] = fload(sn * TILE + q);
+            const float4* ck = ck0 + (size_t)sn * cks;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) ckn[p] = ck[p];
         }
         // forward recompute of the segment into smem (own column)
         if (len == TILE) {
-            float fcur[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) fcur[q] = fnx[q];
-#pragma unroll 1
             for (int r0 = 0; r0 < TILE; r0 += 8) {
-                float fn[8];
-                const int nr = r0 + 8 < TILE ? i0 + r0 + 8 : i0 - TILE;  // next block or next segment
+                float fb[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) fn[q] = fload(nr + q);
-                p1_fwd8<true>(fcur, nu_hi, nu_lo, k, v1, v2, y1, y2, bl + r0 * BUF_LD);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) fcur[q] = fn[q];
+                for (int q = 0; q < 8; ++q) fb[q] = seg_f[r0 + q];
+                p1_fwd8<true>(fb, nu_hi, nu_lo, k, v1, v2, y1, y2, bl + r0 * BUF_LD);
             }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) fnx[q] = fcur[q];
         } else {
             for (int r = 0; r < len; ++r) {
                 const float fs = fload(i0 + r);
@@ -522,9 +532,9 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
                 for (int p = 0; p < 4; ++p)
                     bl[(p * TILE + r) * BUF_LD] = cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
             }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) fnx[q] = fload(i0 - TILE + q);
         }
+#pragma unroll
+        for (int q = 0; q < TILE; ++q) seg_f[q] = nxt[q];
         if (seg == a.nseg - 1) {
             // backward start = steady state of the last forward output (_core.pyx:85-87)
 #pragma unroll
@@ -808,17 +818,25 @@ __device__ __forceinline__ void p2_tile(const Pass2Args& a, const P2Ctx<G>& c, i
             C[g][p][2] = v.z;
             C[g][p][3] = v.w;
         }
-    const bool full = len == TILE;
     float4 fa[4][G], fb[4][G];
     float va[4], vb[4];
-    p2_load4<G, OUT>(c, x0, len - 1, fa, va);
+    if (len == TILE) {
+        // 4 iterations of 8 steps: the recurrence state returns to the same
+        // registers every iteration (no shuffling moves)
+        p2_load4<G, OUT>(c, x0, TILE - 1, fa, va);
 #pragma unroll 1
-    for (int mb = len - 1; mb >= 0; mb -= 8) {
-        p2_load4<G, OUT>(c, x0, mb - 4, fb, vb);
-        p2_step4<G, OUT>(a, c, x0, mb, full, fa, va, C, p1, p2, q1, q2, pn, pd, iv);
-        if (mb - 4 < 0) break;
-        p2_load4<G, OUT>(c, x0, mb - 8, fa, va);
-        p2_step4<G, OUT>(a, c, x0, mb - 4, full, fb, vb, C, p1, p2, q1, q2, pn, pd, iv);
+        for (int mb = TILE - 1; mb >= 7; mb -= 8) {
+            p2_load4<G, OUT>(c, x0, mb - 4, fb, vb);
+            p2_step4<G, OUT>(a, c, x0, mb, true, fa, va, C, p1, p2, q1, q2, pn, pd, iv);
+            p2_load4<G, OUT>(c, x0, mb - 8, fa, va);  // clamped at x0 on the last iteration
+            p2_step4<G, OUT>(a, c, x0, mb - 4, true, fb, vb, C, p1, p2, q1, q2, pn, pd, iv);
+        }
+    } else {
+#pragma unroll 1
+        for (int mb = len - 1; mb >= 0; mb -= 4) {
+            p2_load4<G, OUT>(c, x0, mb, fa, va);
+            p2_step4<G, OUT>(a, c, x0, mb, false, fa, va, C, p1, p2, q1, q2, pn, pd, iv);
+        }
     }
 }
 
@@ -1045,34 +1063,54 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2_box(const __grid_constant_
 // Reduce partial groups, transpose to row-major, optional guarded ratio.
 // ---------------------------------------------------------------------------
 
+// Tile of 32 x-rows by 128 rows (i): partials are read as float4 along i
+// (512 B contiguous per warp and group), summed over groups in fixed order
+// (deterministic), staged in smem, and written transposed (row-major).
+constexpr int RED_I = 128;
+
 __global__ void __launch_bounds__(256) k_reduce(const __grid_constant__ ReduceArgs a) {
-    __shared__ float tn[TILE][TILE + 1];
-    __shared__ float td[TILE][TILE + 1];
+    __shared__ float tn[TILE][RED_I + 4];
+    __shared__ float td[TILE][RED_I + 4];
     const int b = blockIdx.z;
-    const int x0 = blockIdx.x * TILE, i0 = blockIdx.y * TILE;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
+    const int x0 = blockIdx.x * TILE, i0 = blockIdx.y * RED_I;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;  // 8 warps
     const size_t plane = (size_t)a.B * a.W * a.H;
-    // read partials in [x][i] orientation (coalesced over i)
-    for (int r = ty; r < TILE; r += 8) {
-        const int gx = x0 + r, gi = i0 + tx;
-        float n = 0.f, d = 0.f;
+    const bool vec = (a.H & 3) == 0;
+    for (int r = warp; r < TILE; r += 8) {
+        const int gx = x0 + r;
+        const int gi = i0 + 4 * lane;
+        float n[4] = {0.f, 0.f, 0.f, 0.f}, d[4] = {0.f, 0.f, 0.f, 0.f};
         if (gx < a.W && gi < a.H) {
-            const size_t off = ((size_t)b * a.W + gx) * a.H + gi;
-            for (int g = 0; g < a.ngroups; ++g) {
-                n += a.part[(size_t)(2 * g) * plane + off];
-                d += a.part[(size_t)(2 * g + 1) * plane + off];
+            const float* pp = a.part + ((size_t)b * a.W + gx) * a.H + gi;
+            if (vec) {
+                for (int g = 0; g < a.ngroups; ++g) {
+                    const float4 vn = *reinterpret_cast<const float4*>(pp + (size_t)(2 * g) * plane);
+                    const float4 vd = *reinterpret_cast<const float4*>(pp + (size_t)(2 * g + 1) * plane);
+                    n[0] += vn.x; n[1] += vn.y; n[2] += vn.z; n[3] += vn.w;
+                    d[0] += vd.x; d[1] += vd.y; d[2] += vd.z; d[3] += vd.w;
+                }
+            } else {
+                const int cnt = min(4, a.H - gi);
+                for (int g = 0; g < a.ngroups; ++g)
+                    for (int q = 0; q < cnt; ++q) {
+                        n[q] += pp[(size_t)(2 * g) * plane + q];
+                        d[q] += pp[(size_t)(2 * g + 1) * plane + q];
+                    }
             }
         }
-        tn[r][tx] = n;
-        td[r][tx] = d;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            tn[r][4 * lane + q] = n[q];
+            td[r][4 * lane + q] = d[q];
+        }
     }
     __syncthreads();
     unsigned long long guarded = 0;
-    for (int r = ty; r < TILE; r += 8) {
-        const int gi = i0 + r, gx = x0 + tx;
+    for (int rr = warp; rr < RED_I; rr += 8) {
+        const int gi = i0 + rr, gx = x0 + lane;
         if (gi < a.H && gx < a.W) {
             const size_t off = ((size_t)b * a.H + gi) * a.W + gx;
-            float n = tn[tx][r], d = td[tx][r];
+            float n = tn[lane][rr], d = td[lane][rr];
             if (a.in_num) {
                 n += a.in_num[off];
                 d += a.in_den[off];
@@ -1082,7 +1120,7 @@ __global__ void __launch_bounds__(256) k_reduce(const __grid_constant__ ReduceAr
                 a.den[off] = d;
             }
             if (a.out) {
-                bool gd = !(d >= 1e-12f);
+                const bool gd = !(d >= 1e-12f);
                 guarded += gd;
                 a.out[off] = gd ? a.f[off] : n / d;
             }
@@ -1091,7 +1129,7 @@ __global__ void __launch_bounds__(256) k_reduce(const __grid_constant__ ReduceAr
     if (a.out && a.counters) {
         // warp-aggregate then one atomic per warp (integer -> deterministic total)
         for (int o = 16; o > 0; o >>= 1) guarded += __shfl_down_sync(0xffffffffu, guarded, o);
-        if (tx == 0 && guarded) atomicAdd(&a.counters[1], guarded);
+        if (lane == 0 && guarded) atomicAdd(&a.counters[1], guarded);
     }
 }
 
@@ -1502,7 +1540,11 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             ra.den = den;
             ra.out = nullptr;
         }
-        { Prof pr(KK_REDUCE, st); k_reduce<<<tgrid, 256, 0, st>>>(ra); }
+        {
+            dim3 rgrid((W + TILE - 1) / TILE, (H + RED_I - 1) / RED_I, B);
+            Prof pr(KK_REDUCE, st);
+            k_reduce<<<rgrid, 256, 0, st>>>(ra);
+        }
         if ((rc = check_cuda("reduce"))) return rc;
     }
     return TBF_OK;
