@@ -292,7 +292,8 @@ struct TermDev {
 struct Pass1Args {
     const float* f;
     int B, H, W;
-    int Ey, nseg;  // y warm-up, ceil((H+Ey)/32) checkpoint segments
+    int Ey, nseg;  // y mirror extension; checkpoint segments per y-chunk
+    int nyc, ych_rows, ywarm;  // y-chunks of ych_rows output rows; warm-up rows (mult. of 32)
     int Ex, ne, edge_all, ntx;
     Casc k;
     TermDev t;
@@ -388,7 +389,9 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
     if (term >= a.t.n) return;  // whole warp; no block-level barriers below
     const int b = blockIdx.z;
     const int H = a.H, W = a.W;
-    const int x0 = blockIdx.x * TILE;
+    const int tile_x = blockIdx.x % a.ntx;
+    const int chunk = blockIdx.x / a.ntx;
+    const int x0 = tile_x * TILE;
     const int x = x0 + lane;
     const bool xv = x < W;
     const int xc = xv ? x : W - 1;
@@ -405,14 +408,22 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
         i = max(-Ey, min(i, iend - 1));
         return __ldg(fcol + (size_t)mirror1(i, H) * W);
     };
-    // checkpoints: float4 per plane, [seg][term][b][x][4]
-    float4* const ck0 = reinterpret_cast<float4*>(a.ckpt) +
-                        (((size_t)term * a.B + b) * W + xc) * 4;
+    // y-chunk: output rows [R0, R1).  The forward sweep starts at A0 = R0 -
+    // ywarm from a steady-state guess (exact -Ey start for the top chunk); the
+    // backward starts at Bend = R1 + ywarm (exact H+Ey end for the bottom
+    // chunk).  ywarm >= the decay length K, so guesses fade below eps.
+    const int R0 = chunk * a.ych_rows;
+    const int R1 = min(H, R0 + a.ych_rows);
+    const int A0 = R0 - a.ywarm <= 0 ? -Ey : R0 - a.ywarm;
+    const int Bend = R1 + a.ywarm >= iend ? iend : R1 + a.ywarm;
+    // checkpoints: float4 per plane, [chunk*nseg + local seg][term][b][x][4]
     const size_t cks = (size_t)a.t.n * a.B * W * 4;  // float4 stride between segments
+    float4* const ck0 = reinterpret_cast<float4*>(a.ckpt) +
+                        (((size_t)term * a.B + b) * W + xc) * 4 + (size_t)chunk * a.nseg * cks;
 
     float v1[4], v2[4], y1[4], y2[4];
     {
-        const float f0 = fload(-Ey);
+        const float f0 = fload(A0);
         float s0, c0;
         sincos_fma(fmaf(nu_hi, f0, nu_lo * f0), &s0, &c0);
         const float u[4] = {c0, s0, f0 * c0, f0 * s0};
@@ -430,13 +441,13 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
         for (int p = 0; p < 4; ++p) cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
     };
     {
-        int i = -Ey;
-        for (; i < -Ey + (Ey & 7); ++i) step1(i);  // remainder of the left extension
+        int i = A0;
+        for (; i < A0 + ((R0 - A0) & 7); ++i) step1(i);  // remainder of the lead-in rows
         float cur[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) cur[q] = fload(i + q);
 #pragma unroll 1
-        for (; i < 0; i += 8) {  // rest of the left extension, ends at row 0
+        for (; i < R0; i += 8) {  // rest of the lead-in (mirror extension / warm-up), ends at R0
             float nx[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) nx[q] = fload(i + 8 + q);
@@ -444,98 +455,85 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
 #pragma unroll
             for (int q = 0; q < 8; ++q) cur[q] = nx[q];
         }
-        // segments: f of the next segment is loaded one whole segment ahead
-        float seg_f[TILE];
+    }
+
+    // ---- phases A and B as one loop over 2*nseg steps: steps 0..nseg-1 are
+    // the forward sweep top->bottom (checkpoint stores), steps nseg..2nseg-1
+    // revisit the segments bottom->top (restore, forward recompute into the
+    // smem tile, backward, epilogue).  Both phases share one copy of the
+    // forward code (instruction-cache footprint); phase A also writes the
+    // tile, which is harmless.  f and checkpoints are prefetched one step ahead.
+    float p1[4], p2[4], q1[4], q2[4];
+    float4* const fl0 = reinterpret_cast<float4*>(a.floc) + ((size_t)term * a.B + b) * W * (size_t)H;
+    float4* const ed0 = reinterpret_cast<float4*>(a.edge) + ((size_t)term * a.B + b) * a.ne * (size_t)H;
+    float4* const lc0 = reinterpret_cast<float4*>(a.lcarry) +
+                        (((size_t)term * a.B + b) * a.ntx + tile_x) * (size_t)H * 4;
+    const int nseg = (Bend - R0 + TILE - 1) / TILE;  // local segments of this chunk
+    const int nsteps = 2 * nseg;
+    float seg_f[TILE];
+    float4 ckn[4];
 #pragma unroll
-        for (int q = 0; q < TILE; ++q) seg_f[q] = fload(q);
+    for (int q = 0; q < TILE; ++q) seg_f[q] = fload(R0 + q);
 #pragma unroll 1
-        for (int seg = 0; seg < a.nseg; ++seg) {
-            const int i0 = seg * TILE;
-            const int len = min(TILE, iend - i0);
+    for (int step = 0; step < nsteps; ++step) {
+        const bool phaseB = step >= nseg;
+        const int seg = phaseB ? nsteps - 1 - step : step;
+        const int i0 = R0 + seg * TILE;
+        const int len = min(TILE, Bend - i0);
+        if (!phaseB) {
             if (xv) {
                 float4* ck = ck0 + (size_t)seg * cks;
 #pragma unroll
                 for (int p = 0; p < 4; ++p) ck[p] = f4(v1[p], v2[p], y1[p], y2[p]);
             }
-            if (len == TILE) {
-                float nxt[TILE];
+        } else {
 #pragma unroll
-                for (int q = 0; q < TILE; ++q) nxt[q] = fload(i0 + TILE + q);
+            for (int p = 0; p < 4; ++p) {
+                v1[p] = ckn[p].x;
+                v2[p] = ckn[p].y;
+                y1[p] = ckn[p].z;
+                y2[p] = ckn[p].w;
+            }
+        }
+        // prefetch the next step's f rows (and its checkpoint in phase B)
+        float nxt[TILE];
+        {
+            const int ns = step + 1 < nseg ? step + 1 : max(nsteps - 2 - step, 0);
+#pragma unroll
+            for (int q = 0; q < TILE; ++q) nxt[q] = fload(R0 + ns * TILE + q);
+            if (step + 1 >= nseg && step + 1 < nsteps) {
+                const float4* ck = ck0 + (size_t)ns * cks;  // after this step's store (same thread)
+#pragma unroll
+                for (int p = 0; p < 4; ++p) ckn[p] = ck[p];
+            }
+        }
+        // forward over the segment into the smem tile (own column); the first
+        // phase-B step finds the tile already filled by the last phase-A step
+        if (step != nseg) {
+            if (len == TILE) {
 #pragma unroll
                 for (int r0 = 0; r0 < TILE; r0 += 8) {
                     float fb[8];
 #pragma unroll
                     for (int q = 0; q < 8; ++q) fb[q] = seg_f[r0 + q];
-                    p1_fwd8<false>(fb, nu_hi, nu_lo, k, v1, v2, y1, y2, nullptr);
+                    p1_fwd8<true>(fb, nu_hi, nu_lo, k, v1, v2, y1, y2, bl + r0 * BUF_LD);
                 }
-#pragma unroll
-                for (int q = 0; q < TILE; ++q) seg_f[q] = nxt[q];
             } else {
-                for (int r = 0; r < len; ++r) step1(i0 + r);
-            }
-        }
-    }
-
-    // ---- phase B: segments bottom -> top ----
-    float p1[4], p2[4], q1[4], q2[4];
-    float4* const fl0 = reinterpret_cast<float4*>(a.floc) + ((size_t)term * a.B + b) * W * (size_t)H;
-    float4* const ed0 = reinterpret_cast<float4*>(a.edge) + ((size_t)term * a.B + b) * a.ne * (size_t)H;
-    float4* const lc0 = reinterpret_cast<float4*>(a.lcarry) +
-                        (((size_t)term * a.B + b) * a.ntx + blockIdx.x) * (size_t)H * 4;
-    // prefetch (one segment ahead): f rows and the forward checkpoint
-    float seg_f[TILE];
-    float4 ckn[4];
-    {
-        const int i0 = (a.nseg - 1) * TILE;
+                for (int r = 0; r < len; ++r) {
+                    const float fs = fload(i0 + r);
+                    float s0, c0;
+                    sincos_fma(fmaf(nu_hi, fs, nu_lo * fs), &s0, &c0);
+                    const float u[4] = {c0, s0, fs * c0, fs * s0};
 #pragma unroll
-        for (int q = 0; q < TILE; ++q) seg_f[q] = fload(i0 + q);
-        const float4* ck = ck0 + (size_t)(a.nseg - 1) * cks;
-#pragma unroll
-        for (int p = 0; p < 4; ++p) ckn[p] = ck[p];
-    }
-#pragma unroll 1
-    for (int seg = a.nseg - 1; seg >= 0; --seg) {
-        const int i0 = seg * TILE;
-        const int len = min(TILE, iend - i0);
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            v1[p] = ckn[p].x;
-            v2[p] = ckn[p].y;
-            y1[p] = ckn[p].z;
-            y2[p] = ckn[p].w;
-        }
-        float nxt[TILE];
-        {
-            const int sn = max(seg - 1, 0);
-#pragma unroll
-            for (int q = 0; q < TILE; ++q) nxt[q] = fload(sn * TILE + q);
-            const float4* ck = ck0 + (size_t)sn * cks;
-#pragma unroll
-            for (int p = 0; p < 4; ++p) ckn[p] = ck[p];
-        }
-        // forward recompute of the segment into smem (own column)
-        if (len == TILE) {
-#pragma unroll
-            for (int r0 = 0; r0 < TILE; r0 += 8) {
-                float fb[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) fb[q] = seg_f[r0 + q];
-                p1_fwd8<true>(fb, nu_hi, nu_lo, k, v1, v2, y1, y2, bl + r0 * BUF_LD);
-            }
-        } else {
-            for (int r = 0; r < len; ++r) {
-                const float fs = fload(i0 + r);
-                float s0, c0;
-                sincos_fma(fmaf(nu_hi, fs, nu_lo * fs), &s0, &c0);
-                const float u[4] = {c0, s0, fs * c0, fs * s0};
-#pragma unroll
-                for (int p = 0; p < 4; ++p)
-                    bl[(p * TILE + r) * BUF_LD] = cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
+                    for (int p = 0; p < 4; ++p)
+                        bl[(p * TILE + r) * BUF_LD] = cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
+                }
             }
         }
 #pragma unroll
         for (int q = 0; q < TILE; ++q) seg_f[q] = nxt[q];
-        if (seg == a.nseg - 1) {
+        if (!phaseB) continue;
+        if (seg == nseg - 1) {
             // backward start = steady state of the last forward output (_core.pyx:85-87)
 #pragma unroll
             for (int p = 0; p < 4; ++p)
@@ -566,11 +564,11 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
                 }
             }
         }
-        if (i0 >= H) continue;  // extension segment: no output
+        if (i0 >= R1) continue;  // warm-up / extension segment: no output
         __syncwarp();
         // epilogue: lane <-> row i; tile-local zero-state forward along x
         const int i = i0 + lane;
-        if (lane < min(len, H - i0)) {
+        if (lane < min(len, R1 - i0)) {
             float lv1[4] = {0.f, 0.f, 0.f, 0.f}, lv2[4] = {0.f, 0.f, 0.f, 0.f};
             float ly1[4] = {0.f, 0.f, 0.f, 0.f}, ly2[4] = {0.f, 0.f, 0.f, 0.f};
             float4* fl = fl0 + (size_t)x0 * H + i;
@@ -1242,6 +1240,7 @@ __global__ void k_box_pass_f64(const double* a, double* out, int h, int w, int r
 // ---------------------------------------------------------------------------
 
 constexpr int G1 = 1;  // terms per pass-1 warp == phasor anchor block R
+constexpr int P1_BLOCKS_PER_SM = 3;  // smem-limited residency of pass-1 blocks
 constexpr int G2 = 2;  // terms per pass-2 thread (multiple of G1)
 constexpr int R_ANCHOR = G1;
 constexpr int TAB_PAD = 16;  // zero padding past the last term of the table
@@ -1250,6 +1249,7 @@ size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
     int B, H, W, Ey, Ex, nseg, ntx, ne, edge_all;
+    int nyc, ych_rows, ywarm;  // pass-1 y-chunking (nseg = checkpoint segments per chunk)
     int tb;  // terms per batch (multiple of G2)
     int ng2; // pass-2 groups per batch
     size_t off_fT, off_ckpt, off_floc, off_lc, off_edge, off_ext, off_bst, off_part, off_num,
@@ -1266,7 +1266,6 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     const bool box = sp->kind == TBF_SPATIAL_BOX;
     L->Ey = box ? 0 : std::max(0, std::min(sp->ext_y, H - 1));
     L->Ex = box ? 0 : std::max(0, std::min(sp->ext_x, W - 1));
-    L->nseg = (H + L->Ey + TILE - 1) / TILE;
     L->ntx = (W + TILE - 1) / TILE;
     L->edge_all = 2 * (L->Ex + 1) >= W;
     L->ne = L->edge_all ? W : 2 * (L->Ex + 1);
@@ -1275,12 +1274,30 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     tb = (tb + G2 - 1) / G2 * G2;  // whole groups, so anchors stay aligned across batches
     L->tb = tb;
     L->ng2 = tb / G2;
+    // pass-1 y-chunking: split columns into chunks of rows when column tiles x
+    // terms cannot fill ~4 waves of the GPU, keeping the warm-up <= 1/6 of a chunk
+    L->ywarm = (std::max(sp->ext_y, 1) + TILE - 1) / TILE * TILE;
+    L->nyc = 1;
+    L->ych_rows = H;
+    if (!box) {
+        const long long warps = (long long)L->ntx * tb * B;
+        const long long target = 4LL * 148 * 4 * P1_BLOCKS_PER_SM;
+        int nyc = 1;
+        while (warps * nyc * 2 <= target * 2 && warps * nyc < target) {
+            const int rows = ((H + 2 * nyc - 1) / (2 * nyc) + TILE - 1) / TILE * TILE;
+            if (rows < 6 * L->ywarm) break;
+            nyc *= 2;
+        }
+        L->ych_rows = ((H + nyc - 1) / nyc + TILE - 1) / TILE * TILE;
+        L->nyc = (H + L->ych_rows - 1) / L->ych_rows;
+    }
+    L->nseg = (L->ych_rows + std::max(L->ywarm, L->Ey) + TILE - 1) / TILE + 1;
     const size_t px = (size_t)B * H * W;
     size_t o = 0;
     L->off_fT = o;
     o = align_up(o + px * 4);
     L->off_ckpt = o;
-    if (!box) o = align_up(o + (size_t)L->nseg * tb * 16 * B * W * 4);
+    if (!box) o = align_up(o + (size_t)L->nyc * L->nseg * tb * 16 * B * W * 4);
     L->off_floc = o;
     o = align_up(o + (size_t)tb * 4 * px * 4);
     L->off_lc = o;
@@ -1432,6 +1449,9 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p1.W = W;
         p1.Ey = L.Ey;
         p1.nseg = L.nseg;
+        p1.nyc = L.nyc;
+        p1.ych_rows = L.ych_rows;
+        p1.ywarm = L.ywarm;
         p1.Ex = L.Ex;
         p1.ne = L.ne;
         p1.edge_all = L.edge_all;
@@ -1443,7 +1463,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p1.floc = floc;
         p1.lcarry = lc;
         p1.edge = edge;
-        dim3 g1((W + TILE - 1) / TILE, (p1.ngroups + P1_WARPS - 1) / P1_WARPS, B);
+        dim3 g1(L.ntx * (box ? 1 : L.nyc), (p1.ngroups + P1_WARPS - 1) / P1_WARPS, B);
         {
             Prof pr(KK_PASS1, st);
             if (box)
