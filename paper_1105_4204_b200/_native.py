@@ -23,6 +23,9 @@ TBF_ERR_DIM = 3
 TBF_ERR_CUDA = 4
 TBF_ERR_WORKSPACE = 5
 
+TBF_OPT_PIPELINE = 0
+TBF_OPT_BATCHES = 1
+
 TBF_SPATIAL_RECURSIVE = 0
 TBF_SPATIAL_BOX = 1
 
@@ -41,6 +44,7 @@ EXPORTS = (
     "tbf_profile_kinds",
     "tbf_kernel_name",
     "tbf_profile_collect",
+    "tbf_set_option",
 )
 ABI_VERSION = 1
 
@@ -105,6 +109,8 @@ def _declare(lib):
     lib.tbf_recursive_smooth_f64.argtypes = [
         _vp, _vp, _i32, _i32, _f64, _f64, _f64, _f64, _f64, _i32, _vp, _vp,
     ]
+    lib.tbf_set_option.restype = ctypes.c_int
+    lib.tbf_set_option.argtypes = [_i32, _i64]
     lib.tbf_profile_enable.restype = ctypes.c_int
     lib.tbf_profile_enable.argtypes = [_i32]
     lib.tbf_profile_kinds.restype = _i32

@@ -1250,11 +1250,20 @@ size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 struct Layout {
     int B, H, W, Ey, Ex, nseg, ntx, ne, edge_all;
     int nyc, ych_rows, ywarm;  // pass-1 y-chunking (nseg = checkpoint segments per chunk)
-    int tb;  // terms per batch (multiple of G2)
-    int ng2; // pass-2 groups per batch
-    size_t off_fT, off_ckpt, off_floc, off_lc, off_edge, off_ext, off_bst, off_part, off_num,
-        off_den, off_tab, total;
+    int tb;     // terms per batch (multiple of G2)
+    int ng2;    // pass-2 groups per batch
+    int nb;     // batches
+    int nslot;  // batch buffer sets (2 = pass 1 of batch k+1 overlaps the rest of batch k)
+    // shared buffers
+    size_t off_fT, off_num, off_den, off_tab;
+    // per-slot buffers (offsets relative to the slot base)
+    size_t off_slot, slot_bytes;
+    size_t s_ckpt, s_floc, s_lc, s_edge, s_ext, s_bst, s_part;
+    size_t total;
 };
+
+int g_pipeline = 1;     // tbf_set_option(TBF_OPT_PIPELINE)
+int g_auto_batches = 2; // tbf_set_option(TBF_OPT_BATCHES): batches when batch_terms <= 0
 
 int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, int batch_terms,
                 Layout* L) {
@@ -1269,11 +1278,21 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     L->ntx = (W + TILE - 1) / TILE;
     L->edge_all = 2 * (L->Ex + 1) >= W;
     L->ne = L->edge_all ? W : 2 * (L->Ex + 1);
-    int tb = batch_terms > 0 ? std::min(batch_terms, nterms_range) : nterms_range;
+    int tb;
+    if (batch_terms > 0) {
+        tb = std::min(batch_terms, nterms_range);
+    } else {
+        // automatic: a few batches so pass 1 of one batch overlaps the memory-
+        // bound rest of the previous one (when pipelining is on)
+        const int nbat = (g_pipeline && !box) ? std::max(1, g_auto_batches) : 1;
+        tb = (nterms_range + nbat - 1) / nbat;
+    }
     tb = std::max(tb, 1);
     tb = (tb + G2 - 1) / G2 * G2;  // whole groups, so anchors stay aligned across batches
     L->tb = tb;
     L->ng2 = tb / G2;
+    L->nb = (nterms_range + tb - 1) / tb;
+    L->nslot = (g_pipeline && !box && L->nb > 1) ? 2 : 1;
     // pass-1 y-chunking: split columns into chunks of rows when column tiles x
     // terms cannot fill ~4 waves of the GPU, keeping the warm-up <= 1/6 of a chunk
     L->ywarm = (std::max(sp->ext_y, 1) + TILE - 1) / TILE * TILE;
@@ -1283,7 +1302,7 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
         const long long warps = (long long)L->ntx * tb * B;
         const long long target = 4LL * 148 * 4 * P1_BLOCKS_PER_SM;
         int nyc = 1;
-        while (warps * nyc * 2 <= target * 2 && warps * nyc < target) {
+        while (warps * nyc < target) {
             const int rows = ((H + 2 * nyc - 1) / (2 * nyc) + TILE - 1) / TILE * TILE;
             if (rows < 6 * L->ywarm) break;
             nyc *= 2;
@@ -1296,29 +1315,61 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     size_t o = 0;
     L->off_fT = o;
     o = align_up(o + px * 4);
-    L->off_ckpt = o;
-    if (!box) o = align_up(o + (size_t)L->nyc * L->nseg * tb * 16 * B * W * 4);
-    L->off_floc = o;
-    o = align_up(o + (size_t)tb * 4 * px * 4);
-    L->off_lc = o;
-    if (!box) o = align_up(o + (size_t)tb * 16 * B * L->ntx * H * 4);
-    L->off_edge = o;
-    if (!box) o = align_up(o + (size_t)tb * 4 * B * L->ne * H * 4);
-    L->off_ext = o;
-    if (!box) o = align_up(o + (size_t)tb * 4 * B * L->Ex * H * 4);
-    L->off_bst = o;
-    if (!box) o = align_up(o + (size_t)tb * 16 * B * H * 4);
-    L->off_part = o;
-    o = align_up(o + (size_t)L->ng2 * 2 * px * 4);
-    const bool multi = tb < nterms_range;
+    const bool multi = L->nb > 1;
     L->off_num = o;
     if (multi) o = align_up(o + px * 4);
     L->off_den = o;
     if (multi) o = align_up(o + px * 4);
     L->off_tab = o;
     o = align_up(o + (size_t)3 * (nterms_range + TAB_PAD) * 4);
+    // one slot
+    size_t q = 0;
+    L->s_ckpt = q;
+    if (!box) q = align_up(q + (size_t)L->nyc * L->nseg * tb * 16 * B * W * 4);
+    L->s_floc = q;
+    q = align_up(q + (size_t)tb * 4 * px * 4);
+    L->s_lc = q;
+    if (!box) q = align_up(q + (size_t)tb * 16 * B * L->ntx * H * 4);
+    L->s_edge = q;
+    if (!box) q = align_up(q + (size_t)tb * 4 * B * L->ne * H * 4);
+    L->s_ext = q;
+    if (!box) q = align_up(q + (size_t)tb * 4 * B * L->Ex * H * 4);
+    L->s_bst = q;
+    if (!box) q = align_up(q + (size_t)tb * 16 * B * H * 4);
+    L->s_part = q;
+    q = align_up(q + (size_t)L->ng2 * 2 * px * 4);
+    L->slot_bytes = q;
+    L->off_slot = o;
+    o += (size_t)L->nslot * q;
     L->total = o;
     return TBF_OK;
+}
+
+// Internal second stream per device for the pipelined batches.
+cudaStream_t aux_stream() {
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+    return streams[dev];
+}
+
+// Small pool of timing-free events (reused across calls).
+cudaEvent_t event_get() {
+    static std::mutex mu;
+    static std::vector<cudaEvent_t> pool;
+    static size_t next = 0;
+    std::lock_guard<std::mutex> g(mu);
+    if (pool.size() < 256) {
+        cudaEvent_t e;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        pool.push_back(e);
+        return e;
+    }
+    return pool[next++ % pool.size()];
 }
 
 // Zero-input evolution of the pure cascade: state s=(v1,v2,y1,y2) after
@@ -1391,21 +1442,20 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         return fail(TBF_ERR_WORKSPACE, "workspace too small: need %zu have %zu", L.total, ws_bytes);
     char* w8 = (char*)ws;
     float* fT = (float*)(w8 + L.off_fT);
-    float* ckpt = (float*)(w8 + L.off_ckpt);
-    float* floc = (float*)(w8 + L.off_floc);
-    float* lc = (float*)(w8 + L.off_lc);
-    float* edge = (float*)(w8 + L.off_edge);
-    float* ext = (float*)(w8 + L.off_ext);
-    float* bst = (float*)(w8 + L.off_bst);
-    float* part = (float*)(w8 + L.off_part);
     float* tab = (float*)(w8 + L.off_tab);
+    auto slot = [&](int k, size_t off) { return (float*)(w8 + L.off_slot + (size_t)(k % L.nslot) * L.slot_bytes + off); };
     const bool box = sp->kind == TBF_SPATIAL_BOX;
-    const int nb = (nrange + L.tb - 1) / L.tb;
+    const int nb = L.nb;
     if (out && nb > 1) {  // accumulate batches in workspace num/den, ratio at the end
         num = (float*)(w8 + L.off_num);
         den = (float*)(w8 + L.off_den);
         accumulate = 0;
     }
+    // streams: pass 1 on the caller's stream, the rest of each batch on an
+    // internal stream when pipelining (joined back before returning)
+    cudaStream_t s2 = (L.nslot > 1) ? aux_stream() : st;
+    if (!s2) s2 = st;
+    std::vector<cudaEvent_t> ev_done(nb, nullptr);
 
     // term tables: nu split hi/lo, float weights; zero padded past the end
     const int ld = nrange + TAB_PAD;
@@ -1431,9 +1481,23 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         cascade_responses(sp, W - (L.ntx - 1) * TILE, Mlast, nullptr);
     }
 
+    if (s2 != st) {
+        cudaEvent_t e0 = event_get();
+        cudaEventRecord(e0, st);  // f, fT and the term table are ready
+        cudaStreamWaitEvent(s2, e0, 0);
+    }
     for (int bi = 0; bi < nb; ++bi) {
         const int jb = bi * L.tb;
         const int n = std::min(L.tb, nrange - jb);
+        float* ckpt = slot(bi, L.s_ckpt);
+        float* floc = slot(bi, L.s_floc);
+        float* lc = slot(bi, L.s_lc);
+        float* edge = slot(bi, L.s_edge);
+        float* ext = slot(bi, L.s_ext);
+        float* bst = slot(bi, L.s_bst);
+        float* part = slot(bi, L.s_part);
+        // the slot is free once batch bi - nslot has finished on s2
+        if (s2 != st && bi >= L.nslot) cudaStreamWaitEvent(st, ev_done[bi - L.nslot], 0);
         TermDev td;
         td.nu_hi = tab + jb;
         td.nu_lo = tab + ld + jb;
@@ -1472,6 +1536,11 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 k_pass1_gauss<<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1);
         }
         if ((rc = check_cuda("pass1"))) return rc;
+        if (s2 != st) {  // hand the batch to the second stream
+            cudaEvent_t e1 = event_get();
+            cudaEventRecord(e1, st);
+            cudaStreamWaitEvent(s2, e1, 0);
+        }
 
         if (!box) {
             ChainArgs ca;
@@ -1494,7 +1563,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             ca.extbuf = ext;
             ca.bstate = bst;
             dim3 gc((H + 127) / 128, n * B);
-            { Prof pr(KK_CHAIN, st); k_chain<<<gc, 128, 0, st>>>(ca); }
+            { Prof pr(KK_CHAIN, s2); k_chain<<<gc, 128, 0, s2>>>(ca); }
             if ((rc = check_cuda("chain"))) return rc;
         }
 
@@ -1531,11 +1600,11 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         nchunk = (L.ntx + p2.tiles_per_chunk - 1) / p2.tiles_per_chunk;
         dim3 g2(nrb * (box ? 1 : nchunk), p2.ngroups, B);
         {
-            Prof pr(KK_PASS2, st);
+            Prof pr(KK_PASS2, s2);
             if (box)
-                k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, st>>>(p2, sp->radius);
+                k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, s2>>>(p2, sp->radius);
             else
-                k_pass2_gauss<G2><<<g2, P2_THREADS, 0, st>>>(p2);
+                k_pass2_gauss<G2><<<g2, P2_THREADS, 0, s2>>>(p2);
         }
         if ((rc = check_cuda("pass2"))) return rc;
 
@@ -1562,11 +1631,16 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         }
         {
             dim3 rgrid((W + TILE - 1) / TILE, (H + RED_I - 1) / RED_I, B);
-            Prof pr(KK_REDUCE, st);
-            k_reduce<<<rgrid, 256, 0, st>>>(ra);
+            Prof pr(KK_REDUCE, s2);
+            k_reduce<<<rgrid, 256, 0, s2>>>(ra);
         }
         if ((rc = check_cuda("reduce"))) return rc;
+        if (s2 != st) {
+            ev_done[bi] = event_get();
+            cudaEventRecord(ev_done[bi], s2);
+        }
     }
+    if (s2 != st) cudaStreamWaitEvent(st, ev_done[nb - 1], 0);  // join
     return TBF_OK;
 }
 
@@ -1587,6 +1661,20 @@ int tbf_profile_enable(int32_t on) {
 }
 
 int32_t tbf_profile_kinds(void) { return KK_COUNT; }
+
+int tbf_set_option(int32_t option, int64_t value) {
+    switch (option) {
+        case TBF_OPT_PIPELINE:
+            g_pipeline = value != 0;
+            return TBF_OK;
+        case TBF_OPT_BATCHES:
+            if (value < 1) return fail(TBF_ERR_PARAM, "batches must be >= 1");
+            g_auto_batches = (int)value;
+            return TBF_OK;
+        default:
+            return fail(TBF_ERR_PARAM, "unknown option %d", option);
+    }
+}
 
 const char* tbf_kernel_name(int32_t kind) {
     return (kind >= 0 && kind < KK_COUNT) ? kKernelNames[kind] : "";

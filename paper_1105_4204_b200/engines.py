@@ -136,12 +136,12 @@ class TrigFilter:
         t0, t1 = self.term_range
         n = t1 - t0
         if batch_terms is not None:
-            return max(1, min(int(batch_terms), n))
+            return max(0, min(int(batch_terms), n))
         torch = _torch()
         free, _ = torch.cuda.mem_get_info(self.device)
         budget = WORKSPACE_FRACTION * free
-        if self.workspace_bytes(n) <= budget:
-            return n
+        if self.workspace_bytes(0) <= budget:
+            return 0  # library default: a few pipelined batches
         # workspace is affine in the batch size (the library rounds batches to
         # whole pass-2 groups of 4 terms): fit the slope on multiples of 8
         w8, w16 = self.workspace_bytes(8), self.workspace_bytes(16)
