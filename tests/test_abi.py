@@ -48,10 +48,11 @@ def test_workspace_sizing_host_only(lib):
 
     sp = spatial_struct(SpatialSpec.gaussian_recursive(8.0))
     n = term_pairs(make_trig_kernel(20.0)).count
-    full = lib.tbf_workspace_bytes(1, 2048, 2048, ctypes.byref(sp), 0, n, 0)
-    half = lib.tbf_workspace_bytes(1, 2048, 2048, ctypes.byref(sp), 0, n, n // 2)
-    assert full > half > 0
-    # at least the round-trip planes of every term are resident
+    full = lib.tbf_workspace_bytes(1, 2048, 2048, ctypes.byref(sp), 0, n, n)        # one batch
+    quarter = lib.tbf_workspace_bytes(1, 2048, 2048, ctypes.byref(sp), 0, n, n // 4)  # 2 slots
+    auto = lib.tbf_workspace_bytes(1, 2048, 2048, ctypes.byref(sp), 0, n, 0)
+    assert full > quarter > 0 and auto > 0
+    # one batch keeps the round-trip planes of every term resident
     assert full >= n * 16 * 2048 * 2048
     bad = lib.tbf_workspace_bytes(0, 2048, 2048, ctypes.byref(sp), 0, n, 0)
     assert bad == 0
