@@ -63,58 +63,105 @@ def measured_peaks():
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled DURING the timed region: NVML in
+    a background thread every 2 ms (timed regions can be a few ms long), with
+    nvidia-smi -lms 200 as a fallback when NVML is unavailable."""
+
+    REASONS = {  # NVML clocks-event-reason bits
+        0x0000000000000008: "hw_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000004: "sw_power_cap",
+        0x0000000000000080: "hw_power_brake_slowdown",
+    }
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.path = f"/tmp/tbf_clocks_{os.getpid()}.csv"
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = None
+        self._thread = None
+        self.mode = None
 
     def __enter__(self):
+        import threading
+
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._stop = threading.Event()
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for bit, name in self.REASONS.items():
+                            if bits & bit:
+                                self.reasons.add(name)
+                    except Exception:
+                        pass
+                    self._stop.wait(0.002)
+
+            self._thread = threading.Thread(target=run, daemon=True)
+            self._thread.start()
+            self.mode = "nvml-2ms"
+        except Exception:
+            self.mode = "nvidia-smi-200ms"
+            self._smi_start()
+        return self
+
+    def _smi_start(self):
+        self.path = f"/tmp/tbf_clocks_{os.getpid()}.csv"
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}",
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
-        return self
 
     def __exit__(self, *exc):
-        if self.proc is not None:
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join(timeout=2)
+        elif getattr(self, "proc", None) is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
             self.fh.close()
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            try:
+                for line in open(self.path):
+                    r = [v.strip() for v in line.split(",")]
+                    if len(r) >= 9:
+                        if r[1].replace(".", "").isdigit():
+                            self.samples.append(float(r[1]))
+                        if r[2].replace(".", "").isdigit():
+                            self.max_mhz = float(r[2])
+                        for i in range(4):
+                            if r[5 + i].lower() == "active":
+                                self.reasons.add(names[i])
+            except Exception:
+                pass
         return False
 
     def summary(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        rows = []
-        try:
-            with open(self.path) as fh:
-                for line in fh:
-                    parts = [p.strip() for p in line.split(",")]
-                    if len(parts) >= 9:
-                        rows.append(parts)
-        except Exception:
-            pass
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
-        busy = [v for v in sm if smax and v > 0.3 * max(smax)] or sm
-        return {"sm_mhz": statistics.median(busy) if busy else None,
-                "sm_max_mhz": max(smax) if smax else None,
-                "reasons": reasons, "samples": len(rows)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0, "sampler": self.mode}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "sampler": self.mode}
 
 
 # ---------------------------------------------------------------------------
@@ -134,13 +181,10 @@ def _ref_module():
 
 
 def _ref_crop_job(args):
-    cfg_id, side, seed_off, workers = args
+    cfg_id, crop, workers = args
     cfg = workloads.CONFIGS[cfg_id]
     trigbf, kind = _ref_module()
-    f = workloads.frame(cfg, 0)
-    y0 = (seed_off * 97) % max(1, cfg.height - side + 1)
-    x0 = (seed_off * 131) % max(1, cfg.width - side + 1)
-    crop = np.ascontiguousarray(f[y0:y0 + side, x0:x0 + side], dtype=np.float64)
+    crop = np.ascontiguousarray(crop, dtype=np.float64)
     t = time.perf_counter()
     if kind == "reference":
         k = trigbf.make_trig_kernel(cfg.sigma_r, cfg.T)
@@ -152,28 +196,34 @@ def _ref_crop_job(args):
     return crop.size, time.perf_counter() - t
 
 
-def reference_sample(cfg_id: int, budget_s: float, procs: int):
-    """Time the reference on crops of the workload with `procs` processes
-    (workers=1 each) -- about `budget_s` seconds of CPU work.  Returns
+def reference_sample(cfg_id: int, budget_s: float, procs: int, frame=None):
+    """Time the reference on crops of the workload's first frame, one process
+    per core (workers=1 each), about `budget_s` seconds of CPU work.  Returns
     (Mpx/s, description, kind, cores)."""
     from concurrent.futures import ProcessPoolExecutor
 
     cfg = workloads.CONFIGS[cfg_id]
     _, kind = _ref_module()
-    n_terms = term_pairs(make_trig_kernel(cfg.sigma_r, cfg.T)).spatial_passes
-    # calibrate: reference ~ 30 ns per pixel per spatial pass (compiled core)
-    per_px = 30e-9 * n_terms * (1.0 if kind == "reference" else 6.0)
+    passes = term_pairs(make_trig_kernel(cfg.sigma_r, cfg.T)).spatial_passes
+    # calibration: the compiled reference spends ~30 ns per pixel per spatial pass
+    per_px = 30e-9 * passes * (1.0 if kind == "reference" else 6.0)
     side = int(math.sqrt(max(64 * 64, budget_s / per_px)))
     side = max(64, min(side, cfg.height, cfg.width, 2048))
-    jobs = [(cfg_id, side, i, 1) for i in range(procs)]
+    f = workloads.frame(cfg, 0) if frame is None else frame
+    crops = []
+    for i in range(procs):
+        y0 = (i * 97) % max(1, cfg.height - side + 1)
+        x0 = (i * 131) % max(1, cfg.width - side + 1)
+        crops.append((cfg_id, np.array(f[y0:y0 + side, x0:x0 + side]), 1))
     t0 = time.perf_counter()
     with ProcessPoolExecutor(max_workers=procs) as pool:
-        res = list(pool.map(_ref_crop_job, jobs))
+        res = list(pool.map(_ref_crop_job, crops))
     wall = time.perf_counter() - t0
     px = sum(r[0] for r in res)
-    desc = (f"{procs} x {side}x{side} crop(s) of config {cfg_id} (sigma_s={cfg.sigma_s}, "
+    desc = (f"{procs} x {side}x{side} crop(s) of config {cfg_id} frame 0 (sigma_s={cfg.sigma_s}, "
             f"sigma_r={cfg.sigma_r}, N={make_trig_kernel(cfg.sigma_r, cfg.T).N}), one process "
-            f"per core, workers=1 each; per-pixel cost is size-independent (O(1) filter)")
+            f"per core, workers=1 each, wall time incl. pool start; per-pixel cost is "
+            f"size-independent (O(1) filter)")
     return px / wall / 1e6, desc, kind, procs
 
 
@@ -186,8 +236,9 @@ def run_reference_arm(args, rank: int):
     budget = max(2.0, 150.0 / max(1, steps + warmup))
     vals = []
     desc = kind = None
+    frame = workloads.frame(cfg, 0)
     for i in range(warmup + steps):
-        v, desc, kind, used = reference_sample(args.config, budget, cores)
+        v, desc, kind, used = reference_sample(args.config, budget, cores, frame)
         if i >= warmup:
             vals.append(v)
     value = statistics.median(vals)
@@ -398,7 +449,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v, desc, kind, cores = reference_sample(args.config, args.cpu_budget, os.cpu_count() or 1)
+            v, desc, kind, cores = reference_sample(args.config, args.cpu_budget, os.cpu_count() or 1,
+                                                    host[0] if f0 == 0 else None)
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc}
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": repr(e)}

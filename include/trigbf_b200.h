@@ -130,10 +130,10 @@ TBF_API const char* tbf_kernel_name(int32_t kind);
 TBF_API int tbf_profile_collect(double* ms, long long* launches, int32_t n);
 
 /* Process-wide tuning options.
- *   TBF_OPT_PIPELINE (default 1): with several term batches, run pass 1 of
+ *   TBF_OPT_PIPELINE (default 0): with several term batches, run pass 1 of
  *     batch k+1 on the caller's stream while the rest of batch k runs on an
  *     internal stream (double-buffered batch workspace, event dependencies).
- *   TBF_OPT_BATCHES (default 2): number of batches when batch_terms <= 0.
+ *   TBF_OPT_BATCHES (default 2): batches when batch_terms <= 0 and pipelining is on.
  * Options change tbf_workspace_bytes; set them before sizing. */
 #define TBF_OPT_PIPELINE 0
 #define TBF_OPT_BATCHES 1

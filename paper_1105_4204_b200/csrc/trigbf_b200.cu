@@ -176,8 +176,11 @@ __device__ __forceinline__ void csteady(float u, float& v1, float& v2, float& y1
 // the FMAs), then the Cephes minimax polynomials on [-pi/4, pi/4] (about 1 ulp).
 // Arguments here are nu*f <= ~420 rad.
 __device__ __forceinline__ void sincos_fma(float x, float* sp, float* cp) {
-    const float q = rintf(x * 0.636619772367581343f);
-    const int qi = (int)q;
+    // q = nearest integer to x*2/pi via the 1.5*2^23 magic constant (its low
+    // mantissa bits hold q), no F2I / FRND
+    const float t = fmaf(x, 0.636619772367581343f, 12582912.0f);
+    const float q = t - 12582912.0f;
+    const int qi = __float_as_int(t);
     float r = fmaf(q, -1.5703125f, x);
     r = fmaf(q, -4.837512969970703125e-4f, r);
     r = fmaf(q, -7.54978995489188216e-8f, r);
@@ -499,8 +502,15 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
         float nxt[TILE];
         {
             const int ns = step + 1 < nseg ? step + 1 : max(nsteps - 2 - step, 0);
+            const int r0 = R0 + ns * TILE;
+            if (r0 >= 0 && r0 + TILE <= H) {  // interior segment: no mirror / clamp
+                const float* fp = fcol + (size_t)r0 * W;
 #pragma unroll
-            for (int q = 0; q < TILE; ++q) nxt[q] = fload(R0 + ns * TILE + q);
+                for (int q = 0; q < TILE; ++q) nxt[q] = __ldg(fp + (size_t)q * W);
+            } else {
+#pragma unroll
+                for (int q = 0; q < TILE; ++q) nxt[q] = fload(r0 + q);
+            }
             if (step + 1 >= nseg && step + 1 < nsteps) {
                 const float4* ck = ck0 + (size_t)ns * cks;  // after this step's store (same thread)
 #pragma unroll
@@ -511,11 +521,15 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
         // phase-B step finds the tile already filled by the last phase-A step
         if (step != nseg) {
             if (len == TILE) {
-#pragma unroll
+                // rolled 4 x 8 samples (instruction-cache footprint): the 32
+                // prefetched rows shift down by 8 registers per iteration
+#pragma unroll 1
                 for (int r0 = 0; r0 < TILE; r0 += 8) {
                     float fb[8];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) fb[q] = seg_f[r0 + q];
+                    for (int q = 0; q < 8; ++q) fb[q] = seg_f[q];
+#pragma unroll
+                    for (int q = 0; q < TILE - 8; ++q) seg_f[q] = seg_f[q + 8];
                     p1_fwd8<true>(fb, nu_hi, nu_lo, k, v1, v2, y1, y2, bl + r0 * BUF_LD);
                 }
             } else {
@@ -1262,7 +1276,7 @@ struct Layout {
     size_t total;
 };
 
-int g_pipeline = 1;     // tbf_set_option(TBF_OPT_PIPELINE)
+int g_pipeline = 0;     // tbf_set_option(TBF_OPT_PIPELINE) (measured: no gain on B200, SMs time-slice)
 int g_auto_batches = 2; // tbf_set_option(TBF_OPT_BATCHES): batches when batch_terms <= 0
 
 int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, int batch_terms,
