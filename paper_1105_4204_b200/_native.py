@@ -25,6 +25,8 @@ TBF_ERR_WORKSPACE = 5
 
 TBF_OPT_PIPELINE = 0
 TBF_OPT_BATCHES = 1
+TBF_OPT_PASS2_TMA = 2
+TBF_OPT_P2_CHUNKS = 3
 
 TBF_SPATIAL_RECURSIVE = 0
 TBF_SPATIAL_BOX = 1

@@ -369,18 +369,17 @@ __device__ __forceinline__ float4 f4(float a, float b, float c, float d) {
 template <bool STORE>
 __device__ __forceinline__ void p1_fwd8(const float (&fv)[8], float nu_hi, float nu_lo,
                                         const Casc& k, float (&v1)[4], float (&v2)[4],
-                                        float (&y1)[4], float (&y2)[4], float* row) {
+                                        float (&y1)[4], float (&y2)[4], float4* row) {
     float cs[8], sn[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) sincos_fma(fmaf(nu_hi, fv[q], nu_lo * fv[q]), &sn[q], &cs[q]);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const float u[4] = {cs[q], sn[q], fv[q] * cs[q], fv[q] * sn[q]};
+        float o[4];
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            const float o = cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
-            if (STORE) row[(p * TILE + q) * BUF_LD] = o;
-        }
+        for (int p = 0; p < 4; ++p) o[p] = cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
+        if (STORE) row[q * BUF_LD] = make_float4(o[0], o[1], o[2], o[3]);
     }
 }
 
@@ -399,9 +398,12 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
     const bool xv = x < W;
     const int xc = xv ? x : W - 1;
     const int tlen = min(TILE, W - x0);
-    float* const buf = smem + (size_t)warp * 4 * TILE * BUF_LD;
-    float* const bl = buf + lane;           // own column (phases A/B)
-    float* const br = buf + lane * BUF_LD;  // own row (epilogue)
+    // segment tile [row][col] of float4 (the 4 planes of a pixel adjacent),
+    // padded row stride BUF_LD: column access (phases A/B) is contiguous, row
+    // access (epilogue) hits 4 distinct bank groups -> 4 wavefronts, optimal
+    float4* const buf = reinterpret_cast<float4*>(smem) + (size_t)warp * TILE * BUF_LD;
+    float4* const bl = buf + lane;           // own column (phases A/B)
+    float4* const br = buf + lane * BUF_LD;  // own row (epilogue)
     const float nu_hi = a.t.nu_hi[term], nu_lo = a.t.nu_lo[term];
     const Casc k = a.k;
     const int Ey = a.Ey;
@@ -538,9 +540,10 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
                     float s0, c0;
                     sincos_fma(fmaf(nu_hi, fs, nu_lo * fs), &s0, &c0);
                     const float u[4] = {c0, s0, fs * c0, fs * s0};
+                    float o[4];
 #pragma unroll
-                    for (int p = 0; p < 4; ++p)
-                        bl[(p * TILE + r) * BUF_LD] = cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
+                    for (int p = 0; p < 4; ++p) o[p] = cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
+                    bl[r * BUF_LD] = make_float4(o[0], o[1], o[2], o[3]);
                 }
             }
         }
@@ -549,33 +552,36 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
         if (!phaseB) continue;
         if (seg == nseg - 1) {
             // backward start = steady state of the last forward output (_core.pyx:85-87)
+            const float4 lastf = bl[(len - 1) * BUF_LD];
+            const float lf[4] = {lastf.x, lastf.y, lastf.z, lastf.w};
 #pragma unroll
-            for (int p = 0; p < 4; ++p)
-                csteady(bl[(p * TILE + len - 1) * BUF_LD], p1[p], p2[p], q1[p], q2[p], k);
+            for (int p = 0; p < 4; ++p) csteady(lf[p], p1[p], p2[p], q1[p], q2[p], k);
         }
         // backward sweep over the segment, in place
         if (len == TILE) {
 #pragma unroll 1
             for (int r0 = TILE - 1; r0 >= 0; r0 -= 8) {
-                float* row = bl + r0 * BUF_LD;
-                float in[8][4];
+                float4* row = bl + r0 * BUF_LD;
+                float4 in[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
+                for (int q = 0; q < 8; ++q) in[q] = row[-q * BUF_LD];
 #pragma unroll
-                    for (int p = 0; p < 4; ++p) in[q][p] = row[(p * TILE - q) * BUF_LD];
+                for (int q = 0; q < 8; ++q) {
+                    const float iv4[4] = {in[q].x, in[q].y, in[q].z, in[q].w};
+                    float o[4];
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-#pragma unroll
-                    for (int p = 0; p < 4; ++p)
-                        row[(p * TILE - q) * BUF_LD] = cstep(in[q][p], p1[p], p2[p], q1[p], q2[p], k);
+                    for (int p = 0; p < 4; ++p) o[p] = cstep(iv4[p], p1[p], p2[p], q1[p], q2[p], k);
+                    row[-q * BUF_LD] = make_float4(o[0], o[1], o[2], o[3]);
+                }
             }
         } else {
             for (int r = len - 1; r >= 0; --r) {
+                const float4 c4 = bl[r * BUF_LD];
+                const float iv4[4] = {c4.x, c4.y, c4.z, c4.w};
+                float o[4];
 #pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    float* cell = bl + (p * TILE + r) * BUF_LD;
-                    *cell = cstep(*cell, p1[p], p2[p], q1[p], q2[p], k);
-                }
+                for (int p = 0; p < 4; ++p) o[p] = cstep(iv4[p], p1[p], p2[p], q1[p], q2[p], k);
+                bl[r * BUF_LD] = make_float4(o[0], o[1], o[2], o[3]);
             }
         }
         if (i0 >= R1) continue;  // warm-up / extension segment: no output
@@ -592,9 +598,13 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
                 for (int xb = 0; xb < TILE; xb += 8) {
                     float yv[8][4];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-#pragma unroll
-                        for (int p = 0; p < 4; ++p) yv[q][p] = br[p * TILE * BUF_LD + xb + q] * k.gg;
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 t4 = br[xb + q];
+                        yv[q][0] = t4.x * k.gg;
+                        yv[q][1] = t4.y * k.gg;
+                        yv[q][2] = t4.z * k.gg;
+                        yv[q][3] = t4.w * k.gg;
+                    }
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         float o[4];
@@ -606,13 +616,12 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
             } else {
                 for (int xx = 0; xx < tlen; ++xx) {
                     const int gx = x0 + xx;
-                    float yv[4], o[4];
+                    const float4 t4 = br[xx];
+                    // undo the 1/g^2 of the two pure y sweeps
+                    const float yv[4] = {t4.x * k.gg, t4.y * k.gg, t4.z * k.gg, t4.w * k.gg};
+                    float o[4];
 #pragma unroll
-                    for (int p = 0; p < 4; ++p) {
-                        // undo the 1/g^2 of the two pure y sweeps
-                        yv[p] = br[p * TILE * BUF_LD + xx] * k.gg;
-                        o[p] = cstep(yv[p], lv1[p], lv2[p], ly1[p], ly2[p], k);
-                    }
+                    for (int p = 0; p < 4; ++p) o[p] = cstep(yv[p], lv1[p], lv2[p], ly1[p], ly2[p], k);
                     fl[(size_t)xx * H] = f4(o[0], o[1], o[2], o[3]);
                     if (a.edge_all || gx <= a.Ex || gx >= W - 1 - a.Ex) {
                         const int e = a.edge_all ? gx : (gx <= a.Ex ? gx : gx - (W - 1 - a.Ex) + a.Ex + 1);
@@ -852,8 +861,215 @@ __device__ __forceinline__ void p2_tile(const Pass2Args& a, const P2Ctx<G>& c, i
     }
 }
 
+// ---------------------------------------------------------------------------
+// Pass 2, TMA-staged variant (H % 4 == 0): per block 128 rows x G terms x one
+// x-chunk.  For every x-step the block's inputs are contiguous rows in HBM
+// (F_loc[term][b][x][i0..i0+127] float4 and fT[b][x][i0..]), so one thread
+// streams them into a P2T_NST-stage shared-memory ring with
+// cp.async.bulk (TMA bulk copies) completing on mbarriers; the 128 threads
+// consume from shared memory.  Deep prefetch without register cost.
+// ---------------------------------------------------------------------------
+
+constexpr int P2T_STEPS = 4;  // x-steps per stage
+constexpr int P2T_NST = 4;    // stages in the ring
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra LAB_WAIT%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <int G>
-__global__ void __launch_bounds__(P2_THREADS) k_pass2_gauss(const __grid_constant__ Pass2Args a) {
+constexpr int p2t_smem_bytes() {
+    return 128 + P2T_NST * P2T_STEPS * (G * P2_THREADS * 16 + P2_THREADS * 4);
+}
+
+template <int G>
+__global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_tma(const __grid_constant__ Pass2Args a) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+    float4* Fb = reinterpret_cast<float4*>(sm + 128);  // [NST][STEPS][G][128]
+    float* Tb = reinterpret_cast<float*>(Fb + P2T_NST * P2T_STEPS * G * P2_THREADS);  // [NST][STEPS][128]
+    const int tid = threadIdx.x;
+    const int nrb = (a.H + P2_THREADS - 1) / P2_THREADS;
+    const int chunk = blockIdx.x / nrb;
+    const int i0 = (blockIdx.x % nrb) * P2_THREADS;
+    const int H = a.H, W = a.W;
+    const int i_raw = i0 + tid;
+    const bool iv = i_raw < H;
+    const int i = iv ? i_raw : H - 1;
+    const int nrow = min(P2_THREADS, H - i0);
+    const int nrow4 = (nrow + 3) & ~3;
+    const int grp = blockIdx.y;
+    const int b = blockIdx.z;
+    const int j0 = grp * G;
+    const int nt = min(G, a.t.n - j0);
+    const Casc k = a.k;
+
+    float nu_hi[G], nu_lo[G], wt[G];
+    const float4* flrow[G];  // this block's rows, x = 0
+    const float4* crp[G];    // this thread's carries, tile 0
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const int j = min(j0 + g, a.t.n - 1);
+        nu_hi[g] = a.t.nu_hi[j];
+        nu_lo[g] = a.t.nu_lo[j];
+        wt[g] = g < nt ? a.t.w[j] * a.wscale : 0.f;
+        flrow[g] = reinterpret_cast<const float4*>(a.floc) + ((size_t)j * a.B + b) * W * (size_t)H + i0;
+        crp[g] = reinterpret_cast<const float4*>(a.carry) + (((size_t)j * a.B + b) * a.ntx * H + i) * 4;
+    }
+    const float* fTrow = a.fT + (size_t)b * W * H + i0;
+    float* pn = a.part + ((size_t)(grp * 2 + 0) * a.B + b) * W * (size_t)H + i_raw;
+    float* pd = a.part + ((size_t)(grp * 2 + 1) * a.B + b) * W * (size_t)H + i_raw;
+
+    const int t_lo = chunk * a.tiles_per_chunk;
+    const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
+    const bool last_chunk = t_hi == a.ntx;
+    const int x_out_end = min(W, t_hi * TILE);  // outputs for x < x_out_end
+    const int x_hi = last_chunk ? W - 1 : min(W, (t_hi + a.warm_tiles) * TILE) - 1;
+    const int x_lo = t_lo * TILE;
+    const int nx = x_hi - x_lo + 1;
+    const int nblk = (nx + P2T_STEPS - 1) / P2T_STEPS;
+
+    auto issue = [&](int blk) {  // one thread: stage blk % NST <- x-steps of block blk
+        const int s = blk % P2T_NST;
+        const int xs = x_hi - blk * P2T_STEPS;
+        const int n = min(P2T_STEPS, xs - x_lo + 1);
+        mbar_expect_tx(&full[s], (uint32_t)(n * (G * nrow * 16 + nrow4 * 4)));
+        for (int q = 0; q < n; ++q) {
+            const int x = xs - q;
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+                bulk_g2s(Fb + ((s * P2T_STEPS + q) * G + g) * P2_THREADS, flrow[g] + (size_t)x * H,
+                         (uint32_t)nrow * 16, &full[s]);
+            bulk_g2s(Tb + (s * P2T_STEPS + q) * P2_THREADS, fTrow + (size_t)x * H, (uint32_t)nrow4 * 4,
+                     &full[s]);
+        }
+    };
+    if (tid == 0) {
+        for (int s = 0; s < P2T_NST; ++s) mbar_init(&full[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int blk = 0; blk < min(P2T_NST, nblk); ++blk) issue(blk);
+
+    float p1[G][4], p2[G][4], q1[G][4], q2[G][4], C[G][4][4], Cn[G][4][4];
+    auto load_C = [&](int t, float (&dst)[G][4][4]) {
+        t = max(t, 0);
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const float4 v = crp[g][(size_t)t * H * 4 + p];
+                dst[g][p][0] = v.x;
+                dst[g][p][1] = v.y;
+                dst[g][p][2] = v.z;
+                dst[g][p][3] = v.w;
+            }
+    };
+    load_C(x_hi >> 5, C);
+    load_C((x_hi >> 5) - 1, Cn);
+    if (last_chunk) {  // exact start state from the chain
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int j = min(j0 + g, a.t.n - 1);
+            const float4* bs = reinterpret_cast<const float4*>(a.bstate) + (((size_t)j * a.B + b) * H + i) * 4;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const float4 v = bs[p];
+                p1[g][p] = v.x;
+                p2[g][p] = v.y;
+                q1[g][p] = v.z;
+                q2[g][p] = v.w;
+            }
+        }
+    }
+    bool first = !last_chunk;  // warm-up start: steady state of the first exact F
+
+#pragma unroll 1
+    for (int blk = 0; blk < nblk; ++blk) {
+        const int s = blk % P2T_NST;
+        mbar_wait(&full[s], (blk / P2T_NST) & 1);
+        const int xs = x_hi - blk * P2T_STEPS;
+#pragma unroll
+        for (int q = 0; q < P2T_STEPS; ++q) {
+            const int x = xs - q;
+            if (x < x_lo) break;
+            if ((x & 31) == 31 && x != x_hi) {  // entering the next tile (leftwards)
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) C[g][p][r] = Cn[g][p][r];
+                load_C((x >> 5) - 1, Cn);
+            }
+            const float4 h = *reinterpret_cast<const float4*>(&a.Hm[x & 31][0]);
+            const bool out = x < x_out_end;
+            float num = 0.f, den = 0.f;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float4 fo = Fb[((s * P2T_STEPS + q) * G + g) * P2_THREADS + tid];
+                const float fin[4] = {fo.x, fo.y, fo.z, fo.w};
+                float y[4];
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    float F = fmaf(h.x, C[g][p][0], fin[p]);
+                    F = fmaf(h.y, C[g][p][1], F);
+                    F = fmaf(h.z, C[g][p][2], F);
+                    F = fmaf(h.w, C[g][p][3], F);
+                    if (first) csteady(F, p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
+                    y[p] = cstep(F, p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
+                }
+                if (out) {
+                    const float fv = Tb[(s * P2T_STEPS + q) * P2_THREADS + tid];
+                    float sn, cs;
+                    sincos_fma(fmaf(nu_hi[g], fv, nu_lo[g] * fv), &sn, &cs);
+                    num = fmaf(wt[g], fmaf(cs, y[2], sn * y[3]), num);
+                    den = fmaf(wt[g], fmaf(cs, y[0], sn * y[1]), den);
+                }
+            }
+            first = false;
+            if (out && iv) {
+                pn[(size_t)x * H] = num;
+                pd[(size_t)x * H] = den;
+            }
+        }
+        __syncthreads();  // everyone is done with stage s
+        if (tid == 0 && blk + P2T_NST < nblk) issue(blk + P2T_NST);
+    }
+}
+
+template <int G>
+__global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_gauss(const __grid_constant__ Pass2Args a) {
     const int nrb = (a.H + P2_THREADS - 1) / P2_THREADS;
     const int chunk = blockIdx.x / nrb;
     const int i_raw = (blockIdx.x % nrb) * P2_THREADS + threadIdx.x;
@@ -1276,6 +1492,8 @@ struct Layout {
     size_t total;
 };
 
+int g_p2_chunks = 0;    // tbf_set_option(TBF_OPT_P2_CHUNKS): 0 = automatic
+int g_pass2_tma = 0;    // tbf_set_option(TBF_OPT_PASS2_TMA) (measured slower so far: see DESIGN.md)
 int g_pipeline = 0;     // tbf_set_option(TBF_OPT_PIPELINE) (measured: no gain on B200, SMs time-slice)
 int g_auto_batches = 2; // tbf_set_option(TBF_OPT_BATCHES): batches when batch_terms <= 0
 
@@ -1433,6 +1651,8 @@ constexpr int P1_SMEM = P1_WARPS * 4 * G1 * TILE * BUF_LD * 4;
 void set_p1_smem() {
     static bool done = false;
     if (done) return;
+    cudaFuncSetAttribute(k_pass2_tma<G2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         p2t_smem_bytes<G2>());
     cudaFuncSetAttribute(k_pass1_gauss, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM);
     cudaFuncSetAttribute(k_pass1_box<G1, R_ANCHOR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          P1_SMEM);
@@ -1601,12 +1821,14 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         const int nrb = (H + P2_THREADS - 1) / P2_THREADS;
         int nchunk = 1;
         p2.warm_tiles = (std::max(sp->ext_x, 1) + TILE - 1) / TILE;
-        if (!box) {
+        if (!box && g_p2_chunks > 0) {
+            nchunk = std::min(g_p2_chunks, L.ntx);
+        } else if (!box) {
             const long long threads = (long long)nrb * P2_THREADS * p2.ngroups * B;
-            const long long target = 148LL * 24 * 32;  // ~24 resident warps per SM
+            const long long target = 148LL * 12 * 32 * 3 / 2;  // ~1.5 waves of 12 warps/SM
             while (threads * nchunk < target && nchunk < 64) {
                 const int tpc = (L.ntx + 2 * nchunk - 1) / (2 * nchunk);
-                if (tpc < 2 * p2.warm_tiles) break;  // keep warm-up <= 50% of a chunk
+                if (tpc < 4 * p2.warm_tiles) break;  // keep warm-up <= 25% of a chunk
                 nchunk *= 2;
             }
         }
@@ -1617,6 +1839,8 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             Prof pr(KK_PASS2, s2);
             if (box)
                 k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, s2>>>(p2, sp->radius);
+            else if ((H & 3) == 0 && g_pass2_tma)
+                k_pass2_tma<G2><<<g2, P2_THREADS, p2t_smem_bytes<G2>(), s2>>>(p2);
             else
                 k_pass2_gauss<G2><<<g2, P2_THREADS, 0, s2>>>(p2);
         }
@@ -1680,6 +1904,12 @@ int tbf_set_option(int32_t option, int64_t value) {
     switch (option) {
         case TBF_OPT_PIPELINE:
             g_pipeline = value != 0;
+            return TBF_OK;
+        case TBF_OPT_P2_CHUNKS:
+            g_p2_chunks = (int)std::max<int64_t>(0, value);
+            return TBF_OK;
+        case TBF_OPT_PASS2_TMA:
+            g_pass2_tma = value != 0;
             return TBF_OK;
         case TBF_OPT_BATCHES:
             if (value < 1) return fail(TBF_ERR_PARAM, "batches must be >= 1");

@@ -1,0 +1,30 @@
+"""Time one config under several library options (development aid)."""
+import os, sys, json, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_1105_4204_b200 as tb
+from paper_1105_4204_b200 import _native, workloads
+
+cfg = workloads.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
+lib = _native.load()
+f = torch.from_numpy(workloads.make_input(cfg, frames=min(cfg.frames, 8))).cuda()
+k = tb.make_trig_kernel(cfg.sigma_r, cfg.T)
+spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
+flush = torch.empty(128 << 20, device="cuda")
+variants = [("default", {}), ("chunks1", {3: 1}), ("chunks2", {3: 2}), ("chunks4", {3: 4}), ("chunks8", {3: 8}),
+            ("tma", {2: 1}), ("pipeline", {0: 1})]
+for name, opts in variants:
+    for o, v in {0: 0, 2: 0, 3: 0}.items():
+        lib.tbf_set_option(o, v)
+    for o, v in opts.items():
+        lib.tbf_set_option(o, v)
+    plan = tb.TrigFilter(tuple(f.shape), spec, k)
+    out = plan(f); torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(); plan(f, out); b.record(); torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    print(f"{cfg.name} {name:10s} median {np.median(ts):8.3f} ms  min {min(ts):8.3f}", flush=True)
+    del plan; torch.cuda.empty_cache()
