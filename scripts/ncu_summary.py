@@ -46,12 +46,14 @@ def summarise_rep(rep, out_md, traffic_json):
             det[k][r[mi]] = f"{r[vi]} {r[ui]}".strip()
     raw = ncu_csv(rep, "raw")
     rh = raw[0]
+    units = dict(zip(rh, raw[1]))
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     rawd = collections.OrderedDict()
     stalls = collections.OrderedDict()
     for r in raw[2:]:
         d = dict(zip(rh, r))
         k = short(d["Kernel Name"])
-        rawd[k] = {m: d.get(m) for m in RAW if m in d}
+        rawd[k] = {m: f"{d.get(m)} {units.get(m, '')}".strip() for m in RAW if m in d}
         st = {}
         for key, v in d.items():
             if key.startswith("smsp__pcsamp_warps_issue_stalled") and not key.endswith("not_issued"):
@@ -81,8 +83,11 @@ def summarise_rep(rep, out_md, traffic_json):
         traffic = {}
         for k, d in rawd.items():
             try:
-                rd = float(d["dram__bytes_read.sum"].replace(",", ""))
-                wr = float(d["dram__bytes_write.sum"].replace(",", ""))
+                def nbytes(v):
+                    num, unit = v.split(" ", 1)
+                    return float(num.replace(",", "")) * scale.get(unit.strip(), 1.0)
+                rd = nbytes(d["dram__bytes_read.sum"])
+                wr = nbytes(d["dram__bytes_write.sum"])
                 traffic[k.replace("k_", "").replace("_gauss", "")] = rd + wr
             except Exception:
                 pass
