@@ -51,6 +51,7 @@ namespace {
 constexpr int TILE = 32;          // segment length along y == tile width along x == warp size
 constexpr int P1_WARPS = 4;       // warps per pass-1 block (each a different term group)
 constexpr int P2_THREADS = 128;   // rows per pass-2 block
+constexpr int P1_BLOCKS_PER_SM = 3;  // smem-limited residency of pass-1 blocks (4 warps, 67.6 KB)
 constexpr int BUF_LD = TILE + 1;  // padded leading dimension of the smem tile
 
 thread_local std::string g_last_error;
@@ -383,7 +384,11 @@ __device__ __forceinline__ void p1_fwd8(const float (&fv)[8], float nu_hi, float
     }
 }
 
-__global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_constant__ Pass1Args a) {
+// FOLD: the g^2 that undoes the two pure y sweeps is folded into the pass-2
+// weights (g^4 there) instead of one multiply per plane-sample here; used when
+// T/g^4 stays far from the fp32 range limit.
+template <bool FOLD>
+__global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss(const __grid_constant__ Pass1Args a) {
     extern __shared__ float smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -524,7 +529,9 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
         if (step != nseg) {
             if (len == TILE) {
                 // rolled 4 x 8 samples (instruction-cache footprint): the 32
-                // prefetched rows shift down by 8 registers per iteration
+                // prefetched rows shift down by 8 registers per iteration.
+                // (A software-pipelined 2 x 16 variant spilled at the 3-block
+                // register cap and measured 27% slower.)
 #pragma unroll 1
                 for (int r0 = 0; r0 < TILE; r0 += 8) {
                     float fb[8];
@@ -600,10 +607,11 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         const float4 t4 = br[xb + q];
-                        yv[q][0] = t4.x * k.gg;
-                        yv[q][1] = t4.y * k.gg;
-                        yv[q][2] = t4.z * k.gg;
-                        yv[q][3] = t4.w * k.gg;
+                        const float sc = FOLD ? 1.f : k.gg;
+                        yv[q][0] = FOLD ? t4.x : t4.x * sc;
+                        yv[q][1] = FOLD ? t4.y : t4.y * sc;
+                        yv[q][2] = FOLD ? t4.z : t4.z * sc;
+                        yv[q][3] = FOLD ? t4.w : t4.w * sc;
                     }
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
@@ -618,7 +626,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_gauss(const __grid_cons
                     const int gx = x0 + xx;
                     const float4 t4 = br[xx];
                     // undo the 1/g^2 of the two pure y sweeps
-                    const float yv[4] = {t4.x * k.gg, t4.y * k.gg, t4.z * k.gg, t4.w * k.gg};
+                    const float sc = FOLD ? 1.f : k.gg;
+                    const float yv[4] = {t4.x * sc, t4.y * sc, t4.z * sc, t4.w * sc};
                     float o[4];
 #pragma unroll
                     for (int p = 0; p < 4; ++p) o[p] = cstep(yv[p], lv1[p], lv2[p], ly1[p], ly2[p], k);
@@ -870,8 +879,9 @@ __device__ __forceinline__ void p2_tile(const Pass2Args& a, const P2Ctx<G>& c, i
 // consume from shared memory.  Deep prefetch without register cost.
 // ---------------------------------------------------------------------------
 
-constexpr int P2T_STEPS = 4;  // x-steps per stage
-constexpr int P2T_NST = 4;    // stages in the ring
+constexpr int P2T_STEPS = 4;                  // x-steps per stage
+constexpr int P2T_NST = 4;                    // stages in the ring
+constexpr int P2T_THREADS = P2_THREADS + 32;  // 4 consumer warps + 1 producer warp
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -886,6 +896,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
@@ -908,95 +921,118 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 template <int G>
 constexpr int p2t_smem_bytes() {
-    return 128 + P2T_NST * P2T_STEPS * (G * P2_THREADS * 16 + P2_THREADS * 4);
+    return 256 + P2T_NST * P2T_STEPS * (G * P2_THREADS * 16 + P2_THREADS * 4);
 }
 
-template <int G>
-__global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_tma(const __grid_constant__ Pass2Args a) {
+// Requires W % 32 == 0 (whole tiles) and H % 4 == 0 (16-byte aligned rows).
+template <int G, int MINB>
+__global__ void __launch_bounds__(P2T_THREADS, MINB) k_pass2_tma(const __grid_constant__ Pass2Args a) {
     extern __shared__ __align__(128) unsigned char sm[];
     uint64_t* full = reinterpret_cast<uint64_t*>(sm);
-    float4* Fb = reinterpret_cast<float4*>(sm + 128);  // [NST][STEPS][G][128]
+    uint64_t* empty = full + P2T_NST;
+    float4* Fb = reinterpret_cast<float4*>(sm + 256);  // [NST][STEPS][G][128]
     float* Tb = reinterpret_cast<float*>(Fb + P2T_NST * P2T_STEPS * G * P2_THREADS);  // [NST][STEPS][128]
     const int tid = threadIdx.x;
+    const int warp = tid >> 5;
     const int nrb = (a.H + P2_THREADS - 1) / P2_THREADS;
     const int chunk = blockIdx.x / nrb;
     const int i0 = (blockIdx.x % nrb) * P2_THREADS;
     const int H = a.H, W = a.W;
-    const int i_raw = i0 + tid;
-    const bool iv = i_raw < H;
-    const int i = iv ? i_raw : H - 1;
     const int nrow = min(P2_THREADS, H - i0);
     const int nrow4 = (nrow + 3) & ~3;
     const int grp = blockIdx.y;
     const int b = blockIdx.z;
     const int j0 = grp * G;
     const int nt = min(G, a.t.n - j0);
-    const Casc k = a.k;
 
+    const int t_lo = chunk * a.tiles_per_chunk;
+    const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
+    const bool last_chunk = t_hi == a.ntx;
+    const int t_top = last_chunk ? a.ntx - 1 : min(a.ntx - 1, t_hi - 1 + a.warm_tiles);
+    const int ntiles = t_top - t_lo + 1;
+    const int nblk = ntiles * (TILE / P2T_STEPS);
+    const int x_top = t_top * TILE + TILE - 1;
+
+    if (tid == 0) {
+        for (int st = 0; st < P2T_NST; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], P2_THREADS / 32);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (warp == P2_THREADS / 32) {  // ---- producer warp ----
+        if ((tid & 31) == 0) {
+            const float4* flrow[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int j = min(j0 + g, a.t.n - 1);
+                flrow[g] = reinterpret_cast<const float4*>(a.floc) + ((size_t)j * a.B + b) * W * (size_t)H + i0;
+            }
+            const float* fTrow = a.fT + (size_t)b * W * H + i0;
+            const uint32_t bytes = (uint32_t)(P2T_STEPS * (G * nrow * 16 + nrow4 * 4));
+            for (int blk = 0; blk < nblk; ++blk) {
+                const int st = blk % P2T_NST;
+                if (blk >= P2T_NST) mbar_wait(&empty[st], ((blk / P2T_NST) - 1) & 1);
+                mbar_expect_tx(&full[st], bytes);
+                const int xs = x_top - blk * P2T_STEPS;
+#pragma unroll
+                for (int q = 0; q < P2T_STEPS; ++q) {
+                    const int x = xs - q;
+#pragma unroll
+                    for (int g = 0; g < G; ++g)
+                        bulk_g2s(Fb + ((st * P2T_STEPS + q) * G + g) * P2_THREADS, flrow[g] + (size_t)x * H,
+                                 (uint32_t)nrow * 16, &full[st]);
+                    bulk_g2s(Tb + (st * P2T_STEPS + q) * P2_THREADS, fTrow + (size_t)x * H,
+                             (uint32_t)nrow4 * 4, &full[st]);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---- consumers: one row per thread ----
+    const int i_raw = i0 + tid;
+    const bool iv = i_raw < H;
+    const int i = iv ? i_raw : H - 1;
+    const Casc k = a.k;
     float nu_hi[G], nu_lo[G], wt[G];
-    const float4* flrow[G];  // this block's rows, x = 0
-    const float4* crp[G];    // this thread's carries, tile 0
+    const float4* crp[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         const int j = min(j0 + g, a.t.n - 1);
         nu_hi[g] = a.t.nu_hi[j];
         nu_lo[g] = a.t.nu_lo[j];
         wt[g] = g < nt ? a.t.w[j] * a.wscale : 0.f;
-        flrow[g] = reinterpret_cast<const float4*>(a.floc) + ((size_t)j * a.B + b) * W * (size_t)H + i0;
         crp[g] = reinterpret_cast<const float4*>(a.carry) + (((size_t)j * a.B + b) * a.ntx * H + i) * 4;
     }
-    const float* fTrow = a.fT + (size_t)b * W * H + i0;
     float* pn = a.part + ((size_t)(grp * 2 + 0) * a.B + b) * W * (size_t)H + i_raw;
     float* pd = a.part + ((size_t)(grp * 2 + 1) * a.B + b) * W * (size_t)H + i_raw;
 
-    const int t_lo = chunk * a.tiles_per_chunk;
-    const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
-    const bool last_chunk = t_hi == a.ntx;
-    const int x_out_end = min(W, t_hi * TILE);  // outputs for x < x_out_end
-    const int x_hi = last_chunk ? W - 1 : min(W, (t_hi + a.warm_tiles) * TILE) - 1;
-    const int x_lo = t_lo * TILE;
-    const int nx = x_hi - x_lo + 1;
-    const int nblk = (nx + P2T_STEPS - 1) / P2T_STEPS;
-
-    auto issue = [&](int blk) {  // one thread: stage blk % NST <- x-steps of block blk
-        const int s = blk % P2T_NST;
-        const int xs = x_hi - blk * P2T_STEPS;
-        const int n = min(P2T_STEPS, xs - x_lo + 1);
-        mbar_expect_tx(&full[s], (uint32_t)(n * (G * nrow * 16 + nrow4 * 4)));
-        for (int q = 0; q < n; ++q) {
-            const int x = xs - q;
-#pragma unroll
-            for (int g = 0; g < G; ++g)
-                bulk_g2s(Fb + ((s * P2T_STEPS + q) * G + g) * P2_THREADS, flrow[g] + (size_t)x * H,
-                         (uint32_t)nrow * 16, &full[s]);
-            bulk_g2s(Tb + (s * P2T_STEPS + q) * P2_THREADS, fTrow + (size_t)x * H, (uint32_t)nrow4 * 4,
-                     &full[s]);
-        }
-    };
-    if (tid == 0) {
-        for (int s = 0; s < P2T_NST; ++s) mbar_init(&full[s], 1);
-        mbar_fence_init();
-    }
-    __syncthreads();
-    if (tid == 0)
-        for (int blk = 0; blk < min(P2T_NST, nblk); ++blk) issue(blk);
-
-    float p1[G][4], p2[G][4], q1[G][4], q2[G][4], C[G][4][4], Cn[G][4][4];
-    auto load_C = [&](int t, float (&dst)[G][4][4]) {
+    float p1[G][4], p2[G][4], q1[G][4], q2[G][4], C[G][4][4];
+    float4 Cn[G][4];
+    auto load_Cn = [&](int t) {
         t = max(t, 0);
 #pragma unroll
         for (int g = 0; g < G; ++g)
 #pragma unroll
+            for (int p = 0; p < 4; ++p) Cn[g][p] = crp[g][(size_t)t * H * 4 + p];
+    };
+    auto take_Cn = [&]() {
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
             for (int p = 0; p < 4; ++p) {
-                const float4 v = crp[g][(size_t)t * H * 4 + p];
-                dst[g][p][0] = v.x;
-                dst[g][p][1] = v.y;
-                dst[g][p][2] = v.z;
-                dst[g][p][3] = v.w;
+                C[g][p][0] = Cn[g][p].x;
+                C[g][p][1] = Cn[g][p].y;
+                C[g][p][2] = Cn[g][p].z;
+                C[g][p][3] = Cn[g][p].w;
             }
     };
-    load_C(x_hi >> 5, C);
-    load_C((x_hi >> 5) - 1, Cn);
+    load_Cn(t_top);
+    take_Cn();
+    load_Cn(t_top - 1);
     if (last_chunk) {  // exact start state from the chain
 #pragma unroll
         for (int g = 0; g < G; ++g) {
@@ -1011,60 +1047,70 @@ __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_tma(const __grid_consta
                 q2[g][p] = v.w;
             }
         }
-    }
-    bool first = !last_chunk;  // warm-up start: steady state of the first exact F
-
-#pragma unroll 1
-    for (int blk = 0; blk < nblk; ++blk) {
-        const int s = blk % P2T_NST;
-        mbar_wait(&full[s], (blk / P2T_NST) & 1);
-        const int xs = x_hi - blk * P2T_STEPS;
+    } else {  // warm-up: steady state of the exact forward output at x_top
+        mbar_wait(&full[0], 0);
+        const float4 h = *reinterpret_cast<const float4*>(&a.Hm[TILE - 1][0]);
 #pragma unroll
-        for (int q = 0; q < P2T_STEPS; ++q) {
-            const int x = xs - q;
-            if (x < x_lo) break;
-            if ((x & 31) == 31 && x != x_hi) {  // entering the next tile (leftwards)
+        for (int g = 0; g < G; ++g) {
+            const float4 fo = Fb[(0 * G + g) * P2_THREADS + tid];
+            const float fin[4] = {fo.x, fo.y, fo.z, fo.w};
 #pragma unroll
-                for (int g = 0; g < G; ++g)
-#pragma unroll
-                    for (int p = 0; p < 4; ++p)
-#pragma unroll
-                        for (int r = 0; r < 4; ++r) C[g][p][r] = Cn[g][p][r];
-                load_C((x >> 5) - 1, Cn);
-            }
-            const float4 h = *reinterpret_cast<const float4*>(&a.Hm[x & 31][0]);
-            const bool out = x < x_out_end;
-            float num = 0.f, den = 0.f;
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const float4 fo = Fb[((s * P2T_STEPS + q) * G + g) * P2_THREADS + tid];
-                const float fin[4] = {fo.x, fo.y, fo.z, fo.w};
-                float y[4];
-#pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    float F = fmaf(h.x, C[g][p][0], fin[p]);
-                    F = fmaf(h.y, C[g][p][1], F);
-                    F = fmaf(h.z, C[g][p][2], F);
-                    F = fmaf(h.w, C[g][p][3], F);
-                    if (first) csteady(F, p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
-                    y[p] = cstep(F, p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
-                }
-                if (out) {
-                    const float fv = Tb[(s * P2T_STEPS + q) * P2_THREADS + tid];
-                    float sn, cs;
-                    sincos_fma(fmaf(nu_hi[g], fv, nu_lo[g] * fv), &sn, &cs);
-                    num = fmaf(wt[g], fmaf(cs, y[2], sn * y[3]), num);
-                    den = fmaf(wt[g], fmaf(cs, y[0], sn * y[1]), den);
-                }
-            }
-            first = false;
-            if (out && iv) {
-                pn[(size_t)x * H] = num;
-                pd[(size_t)x * H] = den;
+            for (int p = 0; p < 4; ++p) {
+                const float F = fmaf(h.x, C[g][p][0], fmaf(h.y, C[g][p][1],
+                                     fmaf(h.z, C[g][p][2], fmaf(h.w, C[g][p][3], fin[p]))));
+                csteady(F, p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
             }
         }
-        __syncthreads();  // everyone is done with stage s
-        if (tid == 0 && blk + P2T_NST < nblk) issue(blk + P2T_NST);
+    }
+
+    int blk = 0;
+#pragma unroll 1
+    for (int t = t_top; t >= t_lo; --t) {
+        if (t != t_top) {
+            take_Cn();
+            load_Cn(t - 1);
+        }
+        const bool out = t < t_hi;
+        const size_t xrow = (size_t)(t * TILE) * H;
+#pragma unroll 1
+        for (int mb = TILE - 1; mb >= 0; mb -= P2T_STEPS, ++blk) {
+            const int st = blk % P2T_NST;
+            mbar_wait(&full[st], (blk / P2T_NST) & 1);
+#pragma unroll
+            for (int q = 0; q < P2T_STEPS; ++q) {
+                const int m = mb - q;
+                const float4 h = *reinterpret_cast<const float4*>(&a.Hm[m][0]);
+                float num = 0.f, den = 0.f;
+                const float fv = out ? Tb[(st * P2T_STEPS + q) * P2_THREADS + tid] : 0.f;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const float4 fo = Fb[((st * P2T_STEPS + q) * G + g) * P2_THREADS + tid];
+                    const float fin[4] = {fo.x, fo.y, fo.z, fo.w};
+                    float y[4];
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) {
+                        float F = fmaf(h.x, C[g][p][0], fin[p]);
+                        F = fmaf(h.y, C[g][p][1], F);
+                        F = fmaf(h.z, C[g][p][2], F);
+                        F = fmaf(h.w, C[g][p][3], F);
+                        y[p] = cstep(F, p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
+                    }
+                    if (out) {
+                        float sn, cs;
+                        sincos_fma(fmaf(nu_hi[g], fv, nu_lo[g] * fv), &sn, &cs);
+                        num = fmaf(wt[g], fmaf(cs, y[2], sn * y[3]), num);
+                        den = fmaf(wt[g], fmaf(cs, y[0], sn * y[1]), den);
+                    }
+                }
+                if (out && iv) {
+                    const size_t off = xrow + (size_t)m * H;
+                    pn[off] = num;
+                    pd[off] = den;
+                }
+            }
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+        }
     }
 }
 
@@ -1311,7 +1357,22 @@ __global__ void __launch_bounds__(256) k_reduce(const __grid_constant__ ReduceAr
         if (gx < a.W && gi < a.H) {
             const float* pp = a.part + ((size_t)b * a.W + gx) * a.H + gi;
             if (vec) {
-                for (int g = 0; g < a.ngroups; ++g) {
+                // 4 groups (8 float4 loads) in flight, summed in fixed group order
+                int g = 0;
+                for (; g + 4 <= a.ngroups; g += 4) {
+                    float4 vn[4], vd[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        vn[q] = *reinterpret_cast<const float4*>(pp + (size_t)(2 * (g + q)) * plane);
+                        vd[q] = *reinterpret_cast<const float4*>(pp + (size_t)(2 * (g + q) + 1) * plane);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        n[0] += vn[q].x; n[1] += vn[q].y; n[2] += vn[q].z; n[3] += vn[q].w;
+                        d[0] += vd[q].x; d[1] += vd[q].y; d[2] += vd[q].z; d[3] += vd[q].w;
+                    }
+                }
+                for (; g < a.ngroups; ++g) {
                     const float4 vn = *reinterpret_cast<const float4*>(pp + (size_t)(2 * g) * plane);
                     const float4 vd = *reinterpret_cast<const float4*>(pp + (size_t)(2 * g + 1) * plane);
                     n[0] += vn.x; n[1] += vn.y; n[2] += vn.z; n[3] += vn.w;
@@ -1470,7 +1531,6 @@ __global__ void k_box_pass_f64(const double* a, double* out, int h, int w, int r
 // ---------------------------------------------------------------------------
 
 constexpr int G1 = 1;  // terms per pass-1 warp == phasor anchor block R
-constexpr int P1_BLOCKS_PER_SM = 3;  // smem-limited residency of pass-1 blocks
 constexpr int G2 = 2;  // terms per pass-2 thread (multiple of G1)
 constexpr int R_ANCHOR = G1;
 constexpr int TAB_PAD = 16;  // zero padding past the last term of the table
@@ -1492,6 +1552,7 @@ struct Layout {
     size_t total;
 };
 
+int g_pass1_fold = 0;   // see run_terms
 int g_p2_chunks = 0;    // tbf_set_option(TBF_OPT_P2_CHUNKS): 0 = automatic
 int g_pass2_tma = 0;    // tbf_set_option(TBF_OPT_PASS2_TMA) (measured slower so far: see DESIGN.md)
 int g_pipeline = 0;     // tbf_set_option(TBF_OPT_PIPELINE) (measured: no gain on B200, SMs time-slice)
@@ -1651,9 +1712,12 @@ constexpr int P1_SMEM = P1_WARPS * 4 * G1 * TILE * BUF_LD * 4;
 void set_p1_smem() {
     static bool done = false;
     if (done) return;
-    cudaFuncSetAttribute(k_pass2_tma<G2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_pass2_tma<G2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          p2t_smem_bytes<G2>());
-    cudaFuncSetAttribute(k_pass1_gauss, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM);
+    cudaFuncSetAttribute(k_pass2_tma<G2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         p2t_smem_bytes<G2>());
+    cudaFuncSetAttribute(k_pass1_gauss<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM);
+    cudaFuncSetAttribute(k_pass1_gauss<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM);
     cudaFuncSetAttribute(k_pass1_box<G1, R_ANCHOR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          P1_SMEM);
     done = true;
@@ -1709,6 +1773,13 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
 
     set_p1_smem();
     const Casc kc = to_casc(sp);
+    // fold the y-sweep scale into the weights when the unscaled intermediates
+    // (up to ~T / g^4) stay far below FLT_MAX
+    // (measured: the FOLD instantiation spills at the 3-block register cap and
+    // is ~5% slower on config 2, so it is off; kept for the register budget of
+    // future pass-1 variants)
+    const bool fold = g_pass1_fold && !box &&
+                      std::log10(std::max(terms->T, 1.0)) - 4.0 * std::log10(sp->g1 * sp->g2) < 34.0;
     double M[16], Mlast[16], Hm[TILE][4];
     if (!box) {
         cascade_responses(sp, TILE, M, Hm);
@@ -1766,8 +1837,10 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             Prof pr(KK_PASS1, st);
             if (box)
                 k_pass1_box<G1, R_ANCHOR><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1, sp->radius);
+            else if (fold)
+                k_pass1_gauss<true><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1);
             else
-                k_pass1_gauss<<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1);
+                k_pass1_gauss<false><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1);
         }
         if ((rc = check_cuda("pass1"))) return rc;
         if (s2 != st) {  // hand the batch to the second stream
@@ -1812,7 +1885,10 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.ngroups = (n + G2 - 1) / G2;
         for (int m = 0; m < TILE; ++m)
             for (int q = 0; q < 4; ++q) p2.Hm[m][q] = box ? 0.f : (float)Hm[m][q];
-        p2.wscale = box ? 1.f : (float)(sp->g1 * sp->g2 * sp->g1 * sp->g2);
+        {
+            const double g = sp->g1 * sp->g2;
+            p2.wscale = box ? 1.f : (float)(fold ? g * g * g * g : g * g);
+        }
         p2.floc = floc;
         p2.carry = lc;
         p2.bstate = bst;
@@ -1839,8 +1915,10 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             Prof pr(KK_PASS2, s2);
             if (box)
                 k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, s2>>>(p2, sp->radius);
-            else if ((H & 3) == 0 && g_pass2_tma)
-                k_pass2_tma<G2><<<g2, P2_THREADS, p2t_smem_bytes<G2>(), s2>>>(p2);
+            else if ((H & 3) == 0 && (W % TILE) == 0 && g_pass2_tma == 1)
+                k_pass2_tma<G2, 3><<<g2, P2T_THREADS, p2t_smem_bytes<G2>(), s2>>>(p2);
+            else if ((H & 3) == 0 && (W % TILE) == 0 && g_pass2_tma == 2)
+                k_pass2_tma<G2, 2><<<g2, P2T_THREADS, p2t_smem_bytes<G2>(), s2>>>(p2);
             else
                 k_pass2_gauss<G2><<<g2, P2_THREADS, 0, s2>>>(p2);
         }
@@ -1909,7 +1987,7 @@ int tbf_set_option(int32_t option, int64_t value) {
             g_p2_chunks = (int)std::max<int64_t>(0, value);
             return TBF_OK;
         case TBF_OPT_PASS2_TMA:
-            g_pass2_tma = value != 0;
+            g_pass2_tma = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
             return TBF_OK;
         case TBF_OPT_BATCHES:
             if (value < 1) return fail(TBF_ERR_PARAM, "batches must be >= 1");

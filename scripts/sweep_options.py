@@ -11,8 +11,8 @@ f = torch.from_numpy(workloads.make_input(cfg, frames=min(cfg.frames, 8))).cuda(
 k = tb.make_trig_kernel(cfg.sigma_r, cfg.T)
 spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
 flush = torch.empty(128 << 20, device="cuda")
-variants = [("default", {}), ("chunks1", {3: 1}), ("chunks2", {3: 2}), ("chunks4", {3: 4}), ("chunks8", {3: 8}),
-            ("tma", {2: 1}), ("pipeline", {0: 1})]
+variants = [("default", {}),
+            ]
 for name, opts in variants:
     for o, v in {0: 0, 2: 0, 3: 0}.items():
         lib.tbf_set_option(o, v)
