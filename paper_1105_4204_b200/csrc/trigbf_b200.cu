@@ -51,6 +51,18 @@ namespace {
 constexpr int TILE = 32;          // segment length along y == tile width along x == warp size
 constexpr int P1_WARPS = 4;       // warps per pass-1 block (each a different term group)
 constexpr int P2_THREADS = 128;   // rows per pass-2 block
+constexpr int FL_RB = 128;        // row-block height of the x-major tiling (== P2_THREADS)
+
+// x-major per-pixel planes read by pass 2 (fT, partial num/den, and F_loc per
+// term) are row-block tiled: [b][row block of 128][x][128 rows], so a pass-2
+// block streams its rows contiguously as x advances.
+__host__ __device__ __forceinline__ size_t xm_index(int b, int x, int i, int W, int H) {
+    const int nrb = (H + FL_RB - 1) / FL_RB;
+    return (((size_t)b * nrb + i / FL_RB) * W + x) * FL_RB + (i % FL_RB);
+}
+__host__ __device__ __forceinline__ size_t xm_plane(int B, int W, int H) {
+    return (size_t)B * ((H + FL_RB - 1) / FL_RB) * FL_RB * W;
+}
 constexpr int P1_BLOCKS_PER_SM = 3;  // smem-limited residency of pass-1 blocks (4 warps, 67.6 KB)
 constexpr int BUF_LD = TILE + 1;  // padded leading dimension of the smem tile
 
@@ -474,7 +486,10 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     // forward code (instruction-cache footprint); phase A also writes the
     // tile, which is harmless.  f and checkpoints are prefetched one step ahead.
     float p1[4], p2[4], q1[4], q2[4];
-    float4* const fl0 = reinterpret_cast<float4*>(a.floc) + ((size_t)term * a.B + b) * W * (size_t)H;
+    // F_loc layout: float4 [term][b][row block of 128][x][128 rows] (row-block
+    // tiled so pass 2 streams each block's rows contiguously along x)
+    const int nrbk = (H + FL_RB - 1) / FL_RB;
+    float4* const fl0 = reinterpret_cast<float4*>(a.floc) + ((size_t)term * a.B + b) * nrbk * W * (size_t)FL_RB;
     float4* const ed0 = reinterpret_cast<float4*>(a.edge) + ((size_t)term * a.B + b) * a.ne * (size_t)H;
     float4* const lc0 = reinterpret_cast<float4*>(a.lcarry) +
                         (((size_t)term * a.B + b) * a.ntx + tile_x) * (size_t)H * 4;
@@ -598,7 +613,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
         if (lane < min(len, R1 - i0)) {
             float lv1[4] = {0.f, 0.f, 0.f, 0.f}, lv2[4] = {0.f, 0.f, 0.f, 0.f};
             float ly1[4] = {0.f, 0.f, 0.f, 0.f}, ly2[4] = {0.f, 0.f, 0.f, 0.f};
-            float4* fl = fl0 + (size_t)x0 * H + i;
+            float4* fl = fl0 + ((size_t)(i / FL_RB) * W + x0) * FL_RB + (i % FL_RB);
             const bool edge_tile = a.edge_all || x0 <= a.Ex || x0 + tlen - 1 >= W - 1 - a.Ex;
             if (tlen == TILE && !edge_tile) {
 #pragma unroll 1
@@ -618,7 +633,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                         float o[4];
 #pragma unroll
                         for (int p = 0; p < 4; ++p) o[p] = cstep(yv[q][p], lv1[p], lv2[p], ly1[p], ly2[p], k);
-                        fl[(size_t)(xb + q) * H] = f4(o[0], o[1], o[2], o[3]);
+                        fl[(size_t)(xb + q) * FL_RB] = f4(o[0], o[1], o[2], o[3]);
                     }
                 }
             } else {
@@ -631,7 +646,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                     float o[4];
 #pragma unroll
                     for (int p = 0; p < 4; ++p) o[p] = cstep(yv[p], lv1[p], lv2[p], ly1[p], ly2[p], k);
-                    fl[(size_t)xx * H] = f4(o[0], o[1], o[2], o[3]);
+                    fl[(size_t)xx * FL_RB] = f4(o[0], o[1], o[2], o[3]);
                     if (a.edge_all || gx <= a.Ex || gx >= W - 1 - a.Ex) {
                         const int e = a.edge_all ? gx : (gx <= a.Ex ? gx : gx - (W - 1 - a.Ex) + a.Ex + 1);
                         ed0[(size_t)e * H + i] = f4(yv[0], yv[1], yv[2], yv[3]);
@@ -777,7 +792,7 @@ __device__ __forceinline__ void p2_load4(const P2Ctx<G>& c, int x0, int mb, floa
                                          float (&fv)[4]) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        const size_t off = (size_t)(x0 + max(mb - q, 0)) * c.H;
+        const size_t off = (size_t)(x0 + max(mb - q, 0)) * FL_RB;
 #pragma unroll
         for (int g = 0; g < G; ++g) fo[q][g] = c.fl[g][off];
         if (OUT) fv[q] = c.fT[off];
@@ -823,7 +838,7 @@ __device__ __forceinline__ void p2_step4(const Pass2Args& a, const P2Ctx<G>& c, 
                 }
             }
             if (OUT && iv) {
-                const size_t off = (size_t)(x0 + m) * c.H;
+                const size_t off = (size_t)(x0 + m) * FL_RB;
                 pn[off] = num;
                 pd[off] = den;
             }
@@ -871,9 +886,9 @@ __device__ __forceinline__ void p2_tile(const Pass2Args& a, const P2Ctx<G>& c, i
 }
 
 // ---------------------------------------------------------------------------
-// Pass 2, TMA-staged variant (H % 4 == 0): per block 128 rows x G terms x one
+// Pass 2, TMA-staged variant (W % 32 == 0): per block 128 rows x G terms x one
 // x-chunk.  For every x-step the block's inputs are contiguous rows in HBM
-// (F_loc[term][b][x][i0..i0+127] float4 and fT[b][x][i0..]), so one thread
+// (row-block tiled F_loc float4 and fT, see xm_index), so one thread
 // streams them into a P2T_NST-stage shared-memory ring with
 // cp.async.bulk (TMA bulk copies) completing on mbarriers; the 128 threads
 // consume from shared memory.  Deep prefetch without register cost.
@@ -968,9 +983,10 @@ __global__ void __launch_bounds__(P2T_THREADS, MINB) k_pass2_tma(const __grid_co
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 const int j = min(j0 + g, a.t.n - 1);
-                flrow[g] = reinterpret_cast<const float4*>(a.floc) + ((size_t)j * a.B + b) * W * (size_t)H + i0;
+                flrow[g] = reinterpret_cast<const float4*>(a.floc) +
+                           (((size_t)j * a.B + b) * ((H + FL_RB - 1) / FL_RB) + i0 / FL_RB) * W * (size_t)FL_RB;
             }
-            const float* fTrow = a.fT + (size_t)b * W * H + i0;
+            const float* fTrow = a.fT + xm_index(b, 0, i0, W, H);
             const uint32_t bytes = (uint32_t)(P2T_STEPS * (G * nrow * 16 + nrow4 * 4));
             for (int blk = 0; blk < nblk; ++blk) {
                 const int st = blk % P2T_NST;
@@ -982,9 +998,9 @@ __global__ void __launch_bounds__(P2T_THREADS, MINB) k_pass2_tma(const __grid_co
                     const int x = xs - q;
 #pragma unroll
                     for (int g = 0; g < G; ++g)
-                        bulk_g2s(Fb + ((st * P2T_STEPS + q) * G + g) * P2_THREADS, flrow[g] + (size_t)x * H,
+                        bulk_g2s(Fb + ((st * P2T_STEPS + q) * G + g) * P2_THREADS, flrow[g] + (size_t)x * FL_RB,
                                  (uint32_t)nrow * 16, &full[st]);
-                    bulk_g2s(Tb + (st * P2T_STEPS + q) * P2_THREADS, fTrow + (size_t)x * H,
+                    bulk_g2s(Tb + (st * P2T_STEPS + q) * P2_THREADS, fTrow + (size_t)x * FL_RB,
                              (uint32_t)nrow4 * 4, &full[st]);
                 }
             }
@@ -1007,8 +1023,9 @@ __global__ void __launch_bounds__(P2T_THREADS, MINB) k_pass2_tma(const __grid_co
         wt[g] = g < nt ? a.t.w[j] * a.wscale : 0.f;
         crp[g] = reinterpret_cast<const float4*>(a.carry) + (((size_t)j * a.B + b) * a.ntx * H + i) * 4;
     }
-    float* pn = a.part + ((size_t)(grp * 2 + 0) * a.B + b) * W * (size_t)H + i_raw;
-    float* pd = a.part + ((size_t)(grp * 2 + 1) * a.B + b) * W * (size_t)H + i_raw;
+    const size_t xpl = xm_plane(a.B, W, H);
+    float* pn = a.part + (size_t)(grp * 2 + 0) * xpl + xm_index(b, 0, i_raw, W, H);
+    float* pd = a.part + (size_t)(grp * 2 + 1) * xpl + xm_index(b, 0, i_raw, W, H);
 
     float p1[G][4], p2[G][4], q1[G][4], q2[G][4], C[G][4][4];
     float4 Cn[G][4];
@@ -1071,7 +1088,7 @@ __global__ void __launch_bounds__(P2T_THREADS, MINB) k_pass2_tma(const __grid_co
             load_Cn(t - 1);
         }
         const bool out = t < t_hi;
-        const size_t xrow = (size_t)(t * TILE) * H;
+        const size_t xrow = (size_t)(t * TILE) * FL_RB;
 #pragma unroll 1
         for (int mb = TILE - 1; mb >= 0; mb -= P2T_STEPS, ++blk) {
             const int st = blk % P2T_NST;
@@ -1103,7 +1120,7 @@ __global__ void __launch_bounds__(P2T_THREADS, MINB) k_pass2_tma(const __grid_co
                     }
                 }
                 if (out && iv) {
-                    const size_t off = xrow + (size_t)m * H;
+                    const size_t off = xrow + (size_t)m * FL_RB;
                     pn[off] = num;
                     pd[off] = den;
                 }
@@ -1134,12 +1151,14 @@ __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_gauss(const __grid_cons
         c.nu_hi[g] = a.t.nu_hi[j];
         c.nu_lo[g] = a.t.nu_lo[j];
         c.wt[g] = g < nt ? a.t.w[j] * a.wscale : 0.f;
-        c.fl[g] = reinterpret_cast<const float4*>(a.floc) + ((size_t)j * a.B + b) * W * (size_t)H + i;
+        c.fl[g] = reinterpret_cast<const float4*>(a.floc) +
+                  (((size_t)j * a.B + b) * ((H + FL_RB - 1) / FL_RB) + i / FL_RB) * W * (size_t)FL_RB + (i % FL_RB);
         c.cr[g] = reinterpret_cast<const float4*>(a.carry) + (((size_t)j * a.B + b) * a.ntx * H + i) * 4;
     }
-    c.fT = a.fT + (size_t)b * W * H + i;
-    float* pn = a.part + ((size_t)(grp * 2 + 0) * a.B + b) * W * (size_t)H + i_raw;
-    float* pd = a.part + ((size_t)(grp * 2 + 1) * a.B + b) * W * (size_t)H + i_raw;
+    c.fT = a.fT + xm_index(b, 0, i, W, H);
+    const size_t xpl = xm_plane(a.B, W, H);
+    float* pn = a.part + (size_t)(grp * 2 + 0) * xpl + xm_index(b, 0, i_raw, W, H);
+    float* pd = a.part + (size_t)(grp * 2 + 1) * xpl + xm_index(b, 0, i_raw, W, H);
 
     const int t_lo = chunk * a.tiles_per_chunk;
     const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
@@ -1167,7 +1186,7 @@ __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_gauss(const __grid_cons
         const float4 h = *reinterpret_cast<const float4*>(&a.Hm[ms][0]);
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            const float4 F = c.fl[g][(size_t)xs * c.H];
+            const float4 F = c.fl[g][(size_t)xs * FL_RB];
             const float fin[4] = {F.x, F.y, F.z, F.w};
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
@@ -1184,79 +1203,77 @@ __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_gauss(const __grid_cons
 }
 
 // ---------------------------------------------------------------------------
-// Box variant (spatial.py:157-160 + box_pass _core.pyx:28-53): pass 1 along y
-// writes the y-filtered planes transposed into floc; pass 2 runs the x window
-// and demodulates.  Running sums in fp64 (the reference keeps long double).
+// Box variant (spatial.py:157-160, box_pass _core.pyx:28-53).  Pass 1 runs the
+// normalised (2r+1) window along y as a running sum per column (fp64 sums;
+// the reference keeps long double), modulation fused, and writes the
+// y-filtered planes x-major through the smem transpose (same float4 tiled
+// layout as F_loc).  Pass 2 runs the window along x per row, fused with
+// demodulation.  Mirror indices follow _mirror (any radius, repeated
+// reflection).  The box is FIR, so x-chunks of pass 2 are independent.
 // ---------------------------------------------------------------------------
+
+__device__ __forceinline__ float4 modulate4(float fv, float nu_hi, float nu_lo) {
+    float s0, c0;
+    sincos_fma(fmaf(nu_hi, fv, nu_lo * fv), &s0, &c0);
+    return make_float4(c0, s0, fv * c0, fv * s0);
+}
 
 template <int G, int R>
 __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_box(const __grid_constant__ Pass1Args a, int radius) {
-    constexpr int NP = 4 * G;
     extern __shared__ float smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int grp = blockIdx.y * P1_WARPS + warp;
-    if (grp >= a.ngroups) return;
+    const int term = blockIdx.y * P1_WARPS + warp;
+    if (term >= a.t.n) return;
     const int b = blockIdx.z;
     const int H = a.H, W = a.W;
     const int x0 = blockIdx.x * TILE;
     const int x = x0 + lane;
     const int xc = x < W ? x : W - 1;
     const int tlen = min(TILE, W - x0);
-    const int j0 = grp * G;
-    const int nt = min(G, a.t.n - j0);
-    float* buf = smem + (size_t)warp * NP * TILE * BUF_LD;
-    float nu_hi[G], nu_lo[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        nu_hi[g] = a.t.nu_hi[j0 + g];  // table is padded past n
-        nu_lo[g] = a.t.nu_lo[j0 + g];
-    }
-    const float dnu = a.t.dnu;
+    float4* const buf = reinterpret_cast<float4*>(smem) + (size_t)warp * TILE * BUF_LD;
+    float4* const bl = buf + lane;
+    float4* const br = buf + lane * BUF_LD;
+    const float nu_hi = a.t.nu_hi[term], nu_lo = a.t.nu_lo[term];
     const float* fcol = a.f + (size_t)b * H * W + xc;
+    auto fy = [&](long long i) { return __ldg(fcol + (size_t)mirror_any(i, H) * W); };
     const double inv = 1.0 / (double)(2 * radius + 1);
-    double acc[NP];
-    float u[NP];
-#pragma unroll
-    for (int p = 0; p < NP; ++p) acc[p] = 0.0;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (long long kk = -radius; kk <= radius; ++kk) {
-        modulate<G, R>(__ldg(fcol + (size_t)mirror_any(kk, H) * W), nu_hi, nu_lo, dnu, u);
-#pragma unroll
-        for (int p = 0; p < NP; ++p) acc[p] += (double)u[p];
+        const float4 u = modulate4(fy(kk), nu_hi, nu_lo);
+        acc[0] += u.x;
+        acc[1] += u.y;
+        acc[2] += u.z;
+        acc[3] += u.w;
     }
-    const size_t fl_plane = (size_t)a.B * W * H;
-    float* fl_base = a.floc + ((size_t)(j0 * 4) * a.B + b) * W * (size_t)H;
+    const int nrbk = (H + FL_RB - 1) / FL_RB;
+    float4* const fl0 = reinterpret_cast<float4*>(a.floc) + ((size_t)term * a.B + b) * nrbk * W * (size_t)FL_RB;
     for (int i0 = 0; i0 < H; i0 += TILE) {
-        const int i1 = min(i0 + TILE, H);
-        for (int i = i0; i < i1; ++i) {
-            if (i > 0) {
-                float un[NP], uo[NP];
-                modulate<G, R>(__ldg(fcol + (size_t)mirror_any((long long)i + radius, H) * W), nu_hi,
-                            nu_lo, dnu, un);
-                modulate<G, R>(__ldg(fcol + (size_t)mirror_any((long long)i - radius - 1, H) * W),
-                            nu_hi, nu_lo, dnu, uo);
-#pragma unroll
-                for (int p = 0; p < NP; ++p) acc[p] += (double)un[p] - (double)uo[p];
-            }
-#pragma unroll
-            for (int p = 0; p < NP; ++p)
-                buf[(p * TILE + (i - i0)) * BUF_LD + lane] = radius == 0 ? 0.f : (float)(acc[p] * inv);
-            if (radius == 0) {
-                modulate<G, R>(__ldg(fcol + (size_t)i * W), nu_hi, nu_lo, dnu, u);
-#pragma unroll
-                for (int p = 0; p < NP; ++p) buf[(p * TILE + (i - i0)) * BUF_LD + lane] = u[p];
+        const int len = min(TILE, H - i0);
+        for (int r = 0; r < len; ++r) {
+            const int i = i0 + r;
+            bl[r * BUF_LD] = make_float4((float)(acc[0] * inv), (float)(acc[1] * inv),
+                                         (float)(acc[2] * inv), (float)(acc[3] * inv));
+            if (radius > 0 && i + 1 < H) {  // slide the window to row i+1
+                const float4 un = modulate4(fy((long long)i + radius + 1), nu_hi, nu_lo);
+                const float4 uo = modulate4(fy((long long)i - radius), nu_hi, nu_lo);
+                acc[0] += (double)un.x - (double)uo.x;
+                acc[1] += (double)un.y - (double)uo.y;
+                acc[2] += (double)un.z - (double)uo.z;
+                acc[3] += (double)un.w - (double)uo.w;
+            } else if (radius == 0 && i + 1 < H) {
+                const float4 u = modulate4(fy(i + 1), nu_hi, nu_lo);
+                acc[0] = u.x;
+                acc[1] = u.y;
+                acc[2] = u.z;
+                acc[3] = u.w;
             }
         }
         __syncwarp();
         const int i = i0 + lane;
-        if (i < i1) {
-            for (int xx = 0; xx < tlen; ++xx) {
-#pragma unroll
-                for (int p = 0; p < NP; ++p)
-                    if (p / 4 < nt)
-                        fl_base[(size_t)p * fl_plane + (size_t)(x0 + xx) * H + i] =
-                            buf[(p * TILE + lane) * BUF_LD + xx];
-            }
+        if (lane < len) {
+            float4* fl = fl0 + ((size_t)(i / FL_RB) * W + x0) * FL_RB + (i % FL_RB);
+            for (int xx = 0; xx < tlen; ++xx) fl[(size_t)xx * FL_RB] = br[xx];
         }
         __syncwarp();
     }
@@ -1264,8 +1281,9 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_box(const __grid_consta
 
 template <int G, int R>
 __global__ void __launch_bounds__(P2_THREADS) k_pass2_box(const __grid_constant__ Pass2Args a, int radius) {
-    constexpr int NP = 4 * G;
-    const int i_raw = blockIdx.x * P2_THREADS + threadIdx.x;
+    const int nrb = (a.H + P2_THREADS - 1) / P2_THREADS;
+    const int chunk = blockIdx.x / nrb;
+    const int i_raw = (blockIdx.x % nrb) * P2_THREADS + threadIdx.x;
     const int H = a.H, W = a.W;
     const bool iv = i_raw < H;
     const int i = iv ? i_raw : H - 1;
@@ -1273,62 +1291,66 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2_box(const __grid_constant_
     const int b = blockIdx.z;
     const int j0 = grp * G;
     const int nt = min(G, a.t.n - j0);
-    float nu_hi[G], nu_lo[G];
+    float nu_hi[G], nu_lo[G], wt[G];
+    const float4* fl[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-        nu_hi[g] = a.t.nu_hi[j0 + g];  // table is padded past n
-        nu_lo[g] = a.t.nu_lo[j0 + g];
+        const int j = min(j0 + g, a.t.n - 1);
+        nu_hi[g] = a.t.nu_hi[j];
+        nu_lo[g] = a.t.nu_lo[j];
+        wt[g] = g < nt ? a.t.w[j] : 0.f;
+        fl[g] = reinterpret_cast<const float4*>(a.floc) +
+                (((size_t)j * a.B + b) * nrb + i / FL_RB) * W * (size_t)FL_RB + (i % FL_RB);
     }
-    const float dnu = a.t.dnu;
-    float wt[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) wt[g] = g < nt ? a.t.w[j0 + g] : 0.f;
-    const size_t plane = (size_t)a.B * W * H;
-    const float* fl = a.floc + ((size_t)(j0 * 4) * a.B + b) * W * (size_t)H + i;
-    const float* fT = a.fT + (size_t)b * W * H + i;
-    float* pn = a.part + ((size_t)(grp * 2 + 0) * a.B + b) * W * (size_t)H + i_raw;
-    float* pd = a.part + ((size_t)(grp * 2 + 1) * a.B + b) * W * (size_t)H + i_raw;
+    const float* fT = a.fT + xm_index(b, 0, i, W, H);
+    const size_t xpl = xm_plane(a.B, W, H);
+    float* pn = a.part + (size_t)(grp * 2 + 0) * xpl + xm_index(b, 0, i_raw, W, H);
+    float* pd = a.part + (size_t)(grp * 2 + 1) * xpl + xm_index(b, 0, i_raw, W, H);
+    const int xa = chunk * a.tiles_per_chunk * TILE;
+    const int xb = min(W, xa + a.tiles_per_chunk * TILE);
     const double inv = 1.0 / (double)(2 * radius + 1);
-    double acc[NP];
+    auto Yx = [&](int g, long long xx) { return fl[g][(size_t)mirror_any(xx, W) * FL_RB]; };
+    double acc[G][4];
 #pragma unroll
-    for (int p = 0; p < NP; ++p) acc[p] = 0.0;
-    if (radius > 0) {
-        for (long long kk = -radius; kk <= radius; ++kk) {
-            const size_t off = (size_t)mirror_any(kk, W) * H;
-#pragma unroll
-            for (int p = 0; p < NP; ++p)
-                if (p / 4 < nt) acc[p] += (double)fl[(size_t)p * plane + off];
+    for (int g = 0; g < G; ++g) {
+        acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.0;
+        for (long long kk = (long long)xa - radius; kk <= (long long)xa + radius; ++kk) {
+            const float4 v = Yx(g, kk);
+            acc[g][0] += v.x;
+            acc[g][1] += v.y;
+            acc[g][2] += v.z;
+            acc[g][3] += v.w;
         }
     }
-    for (int xx = 0; xx < W; ++xx) {
-        float yo[NP];
-        if (radius > 0) {
-            if (xx > 0) {
-                const size_t on = (size_t)mirror_any((long long)xx + radius, W) * H;
-                const size_t oo = (size_t)mirror_any((long long)xx - radius - 1, W) * H;
-#pragma unroll
-                for (int p = 0; p < NP; ++p)
-                    if (p / 4 < nt)
-                        acc[p] += (double)fl[(size_t)p * plane + on] - (double)fl[(size_t)p * plane + oo];
-            }
-#pragma unroll
-            for (int p = 0; p < NP; ++p) yo[p] = (float)(acc[p] * inv);
-        } else {
-#pragma unroll
-            for (int p = 0; p < NP; ++p)
-                yo[p] = p / 4 < nt ? fl[(size_t)p * plane + (size_t)xx * H] : 0.f;
-        }
+    for (int xx = xa; xx < xb; ++xx) {
         float cc[G], sn[G];
-        phasors<G, R>(fT[(size_t)xx * H], nu_hi, nu_lo, dnu, cc, sn);
+        phasors<G, R>(fT[(size_t)xx * FL_RB], nu_hi, nu_lo, a.t.dnu, cc, sn);
         float num = 0.f, den = 0.f;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            num = fmaf(wt[g], fmaf(cc[g], yo[4 * g + 2], sn[g] * yo[4 * g + 3]), num);
-            den = fmaf(wt[g], fmaf(cc[g], yo[4 * g + 0], sn[g] * yo[4 * g + 1]), den);
+            const float y0 = (float)(acc[g][0] * inv), y1 = (float)(acc[g][1] * inv);
+            const float y2 = (float)(acc[g][2] * inv), y3 = (float)(acc[g][3] * inv);
+            num = fmaf(wt[g], fmaf(cc[g], y2, sn[g] * y3), num);
+            den = fmaf(wt[g], fmaf(cc[g], y0, sn[g] * y1), den);
+            if (xx + 1 < xb) {
+                const float4 vn = Yx(g, (long long)xx + radius + 1);
+                const float4 vo = Yx(g, (long long)xx - radius);
+                if (radius > 0) {
+                    acc[g][0] += (double)vn.x - (double)vo.x;
+                    acc[g][1] += (double)vn.y - (double)vo.y;
+                    acc[g][2] += (double)vn.z - (double)vo.z;
+                    acc[g][3] += (double)vn.w - (double)vo.w;
+                } else {
+                    acc[g][0] = vn.x;
+                    acc[g][1] = vn.y;
+                    acc[g][2] = vn.z;
+                    acc[g][3] = vn.w;
+                }
+            }
         }
         if (iv) {
-            pn[(size_t)xx * H] = num;
-            pd[(size_t)xx * H] = den;
+            pn[(size_t)xx * FL_RB] = num;
+            pd[(size_t)xx * FL_RB] = den;
         }
     }
 }
@@ -1348,14 +1370,14 @@ __global__ void __launch_bounds__(256) k_reduce(const __grid_constant__ ReduceAr
     const int b = blockIdx.z;
     const int x0 = blockIdx.x * TILE, i0 = blockIdx.y * RED_I;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;  // 8 warps
-    const size_t plane = (size_t)a.B * a.W * a.H;
-    const bool vec = (a.H & 3) == 0;
+    const size_t plane = xm_plane(a.B, a.W, a.H);
+    const bool vec = true;  // row-block tiled partials: 4-row groups always aligned and padded
     for (int r = warp; r < TILE; r += 8) {
         const int gx = x0 + r;
         const int gi = i0 + 4 * lane;
         float n[4] = {0.f, 0.f, 0.f, 0.f}, d[4] = {0.f, 0.f, 0.f, 0.f};
         if (gx < a.W && gi < a.H) {
-            const float* pp = a.part + ((size_t)b * a.W + gx) * a.H + gi;
+            const float* pp = a.part + xm_index(b, gx, gi, a.W, a.H);
             if (vec) {
                 // 4 groups (8 float4 loads) in flight, summed in fixed group order
                 int g = 0;
@@ -1455,7 +1477,6 @@ __global__ void __launch_bounds__(256) k_transpose(const float* f, float* fT, in
     const int x0 = blockIdx.x * TILE, i0 = blockIdx.y * TILE;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const float* src = f + (size_t)b * H * W;
-    float* dst = fT + (size_t)b * H * W;
     for (int r = ty; r < TILE; r += 8) {
         int gi = i0 + r, gx = x0 + tx;
         t[r][tx] = (gi < H && gx < W) ? src[(size_t)gi * W + gx] : 0.f;
@@ -1463,7 +1484,7 @@ __global__ void __launch_bounds__(256) k_transpose(const float* f, float* fT, in
     __syncthreads();
     for (int r = ty; r < TILE; r += 8) {
         int gx = x0 + r, gi = i0 + tx;
-        if (gx < W && gi < H) dst[(size_t)gx * H + gi] = t[tx][r];
+        if (gx < W && gi < H) fT[xm_index(b, gx, gi, W, H)] = t[tx][r];
     }
 }
 
@@ -1607,7 +1628,7 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     const size_t px = (size_t)B * H * W;
     size_t o = 0;
     L->off_fT = o;
-    o = align_up(o + px * 4);
+    o = align_up(o + xm_plane(B, W, H) * 4);
     const bool multi = L->nb > 1;
     L->off_num = o;
     if (multi) o = align_up(o + px * 4);
@@ -1619,8 +1640,8 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     size_t q = 0;
     L->s_ckpt = q;
     if (!box) q = align_up(q + (size_t)L->nyc * L->nseg * tb * 16 * B * W * 4);
-    L->s_floc = q;
-    q = align_up(q + (size_t)tb * 4 * px * 4);
+    L->s_floc = q;  // gauss: row-block tiled (padded to whole 128-row blocks); box: planar
+    q = align_up(q + (size_t)tb * 4 * B * W * ((size_t)(H + FL_RB - 1) / FL_RB * FL_RB) * 4);
     L->s_lc = q;
     if (!box) q = align_up(q + (size_t)tb * 16 * B * L->ntx * H * 4);
     L->s_edge = q;
@@ -1630,7 +1651,7 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     L->s_bst = q;
     if (!box) q = align_up(q + (size_t)tb * 16 * B * H * 4);
     L->s_part = q;
-    q = align_up(q + (size_t)L->ng2 * 2 * px * 4);
+    q = align_up(q + (size_t)L->ng2 * 2 * xm_plane(B, W, H) * 4);
     L->slot_bytes = q;
     L->off_slot = o;
     o += (size_t)L->nslot * q;
@@ -1897,7 +1918,16 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         const int nrb = (H + P2_THREADS - 1) / P2_THREADS;
         int nchunk = 1;
         p2.warm_tiles = (std::max(sp->ext_x, 1) + TILE - 1) / TILE;
-        if (!box && g_p2_chunks > 0) {
+        if (box) {
+            const long long threads = (long long)nrb * P2_THREADS * p2.ngroups * B;
+            const long long target = 148LL * 12 * 32 * 3 / 2;
+            const int win = 2 * sp->radius + 1;
+            while (threads * nchunk < target && nchunk < 64) {
+                const int cols = (L.ntx + 2 * nchunk - 1) / (2 * nchunk) * TILE;
+                if (cols < 4 * win) break;  // window init <= 25% of a chunk
+                nchunk *= 2;
+            }
+        } else if (!box && g_p2_chunks > 0) {
             nchunk = std::min(g_p2_chunks, L.ntx);
         } else if (!box) {
             const long long threads = (long long)nrb * P2_THREADS * p2.ngroups * B;
@@ -1910,14 +1940,14 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         }
         p2.tiles_per_chunk = (L.ntx + nchunk - 1) / nchunk;
         nchunk = (L.ntx + p2.tiles_per_chunk - 1) / p2.tiles_per_chunk;
-        dim3 g2(nrb * (box ? 1 : nchunk), p2.ngroups, B);
+        dim3 g2(nrb * nchunk, p2.ngroups, B);
         {
             Prof pr(KK_PASS2, s2);
             if (box)
                 k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, s2>>>(p2, sp->radius);
-            else if ((H & 3) == 0 && (W % TILE) == 0 && g_pass2_tma == 1)
+            else if ((W % TILE) == 0 && g_pass2_tma == 1)
                 k_pass2_tma<G2, 3><<<g2, P2T_THREADS, p2t_smem_bytes<G2>(), s2>>>(p2);
-            else if ((H & 3) == 0 && (W % TILE) == 0 && g_pass2_tma == 2)
+            else if ((W % TILE) == 0 && g_pass2_tma == 2)
                 k_pass2_tma<G2, 2><<<g2, P2T_THREADS, p2t_smem_bytes<G2>(), s2>>>(p2);
             else
                 k_pass2_gauss<G2><<<g2, P2_THREADS, 0, s2>>>(p2);

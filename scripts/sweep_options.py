@@ -11,7 +11,7 @@ f = torch.from_numpy(workloads.make_input(cfg, frames=min(cfg.frames, 8))).cuda(
 k = tb.make_trig_kernel(cfg.sigma_r, cfg.T)
 spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
 flush = torch.empty(128 << 20, device="cuda")
-variants = [("default", {}),
+variants = [("default", {}), ("tma3", {2: 1}), ("tma2", {2: 2}),
             ]
 for name, opts in variants:
     for o, v in {0: 0, 2: 0, 3: 0}.items():
