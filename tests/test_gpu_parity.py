@@ -282,3 +282,66 @@ def test_brute_force_error_reported(tb, orc):
     e = np.abs(got - brute)
     print(f"vs brute-force Gaussian BF (128^2 crop of cfg1): max {e.max():.3g} mean {e.mean():.3g}")
     assert e.max() < 10.0
+
+
+# ---------------------------------------------------------------------------
+# coverage of less-travelled device paths
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("h,w,r", [(37, 5, 7), (9, 130, 40), (70, 45, 3), (64, 64, 0)])
+def test_box_large_radius_and_odd_shapes(tb, orc, h, w, r):
+    """Box radius beyond the image (repeated reflection, _mirror) and widths
+    that are not multiples of the 32-column tile."""
+    f = np.random.default_rng(h * 1000 + w).uniform(0, 255, (h, w)).astype(np.float32)
+    got = _run(tb, f, "box", r, 40.0)
+    ref, _ = orc.bilateral_trig(f.astype(np.float64), "box", r, orc.make_trig_kernel(40.0, 255.0))
+    assert np.max(np.abs(got - ref)) <= TOL
+
+
+@pytest.mark.parametrize("h,w,s,sr", [(1000, 33, 5.0, 25.0), (33, 1000, 5.0, 25.0), (700, 70, 8.0, 20.0)])
+def test_gauss_odd_shapes_with_chunking(tb, orc, h, w, s, sr):
+    """Tall/thin and wide/short images: y-chunking (pass 1) and x-chunking
+    (pass 2) boundaries, partial last tiles and row blocks."""
+    f = np.random.default_rng(h + w).uniform(0, 255, (h, w)).astype(np.float32)
+    got = _run(tb, f, "gauss-recursive", s, sr)
+    ref, _ = orc.bilateral_trig(f.astype(np.float64), "gauss-recursive", s, orc.make_trig_kernel(sr, 255.0))
+    assert np.max(np.abs(got - ref)) <= TOL
+
+
+def test_options_match_default(tb):
+    """The optional pass-2 TMA variants and the two-stream pipeline compute the
+    same filter (up to fp32 reassociation)."""
+    from paper_1105_4204_b200 import _native, workloads
+
+    lib = _native.load()
+    cfg = workloads.CONFIGS[2]
+    f = torch.from_numpy(workloads.frame(cfg, 0)[:512, :768].copy()).cuda()
+    k = tb.make_trig_kernel(cfg.sigma_r)
+    spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
+    base = tb.TrigFilter(tuple(f.shape), spec, k)(f)
+    try:
+        for opts in ({_native.TBF_OPT_PASS2_TMA: 1}, {_native.TBF_OPT_PASS2_TMA: 2},
+                     {_native.TBF_OPT_PIPELINE: 1}, {_native.TBF_OPT_P2_CHUNKS: 1}):
+            for o, v in opts.items():
+                lib.tbf_set_option(o, v)
+            out = tb.TrigFilter(tuple(f.shape), spec, k)(f)
+            torch.cuda.synchronize()
+            assert float((out - base).abs().max()) < 1e-3, opts
+            for o in opts:
+                lib.tbf_set_option(o, 0)
+    finally:
+        for o in (_native.TBF_OPT_PASS2_TMA, _native.TBF_OPT_PIPELINE, _native.TBF_OPT_P2_CHUNKS):
+            lib.tbf_set_option(o, 0)
+
+
+def test_batch_with_y_chunks_matches_single(tb):
+    """Frames of a batch through the y-chunked pass 1 equal single-frame calls."""
+    from paper_1105_4204_b200.workloads import smooth_image
+
+    fs = np.stack([smooth_image(1536, 256, 6, seed=s) for s in (1, 2)])
+    k = tb.make_trig_kernel(20.0)
+    spec = tb.SpatialSpec.gaussian_recursive(8.0)
+    batch = tb.bilateral_trig(torch.from_numpy(fs).cuda(), spec, k).cpu().numpy()
+    for i in range(2):
+        one = tb.bilateral_trig(torch.from_numpy(fs[i]).cuda(), spec, k).cpu().numpy()
+        assert np.max(np.abs(batch[i] - one)) < 1e-4
