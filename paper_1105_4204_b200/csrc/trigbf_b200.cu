@@ -1574,6 +1574,7 @@ struct Layout {
 };
 
 int g_pass1_fold = 0;   // see run_terms
+int g_p1_occ = 3;       // tbf_set_option(TBF_OPT_P1_OCC): pass-1 blocks per SM (2 leaves room for a pass-2 block)
 int g_p2_chunks = 0;    // tbf_set_option(TBF_OPT_P2_CHUNKS): 0 = automatic
 int g_pass2_tma = 0;    // tbf_set_option(TBF_OPT_PASS2_TMA) (measured slower so far: see DESIGN.md)
 int g_pipeline = 0;     // tbf_set_option(TBF_OPT_PIPELINE) (measured: no gain on B200, SMs time-slice)
@@ -1729,6 +1730,7 @@ int validate(const tbf_spatial* sp, const tbf_terms* terms, int tbeg, int tend) 
 }
 
 constexpr int P1_SMEM = P1_WARPS * 4 * G1 * TILE * BUF_LD * 4;
+constexpr int P1_SMEM_OCC2 = 80 * 1024;  // padded request: at most 2 pass-1 blocks per SM
 
 void set_p1_smem() {
     static bool done = false;
@@ -1737,8 +1739,8 @@ void set_p1_smem() {
                          p2t_smem_bytes<G2>());
     cudaFuncSetAttribute(k_pass2_tma<G2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          p2t_smem_bytes<G2>());
-    cudaFuncSetAttribute(k_pass1_gauss<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM);
-    cudaFuncSetAttribute(k_pass1_gauss<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM);
+    cudaFuncSetAttribute(k_pass1_gauss<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
+    cudaFuncSetAttribute(k_pass1_gauss<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
     cudaFuncSetAttribute(k_pass1_box<G1, R_ANCHOR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          P1_SMEM);
     done = true;
@@ -1859,9 +1861,9 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             if (box)
                 k_pass1_box<G1, R_ANCHOR><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1, sp->radius);
             else if (fold)
-                k_pass1_gauss<true><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1);
+                k_pass1_gauss<true><<<g1, P1_WARPS * 32, g_p1_occ == 2 ? P1_SMEM_OCC2 : P1_SMEM, st>>>(p1);
             else
-                k_pass1_gauss<false><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1);
+                k_pass1_gauss<false><<<g1, P1_WARPS * 32, g_p1_occ == 2 ? P1_SMEM_OCC2 : P1_SMEM, st>>>(p1);
         }
         if ((rc = check_cuda("pass1"))) return rc;
         if (s2 != st) {  // hand the batch to the second stream
@@ -2012,6 +2014,10 @@ int tbf_set_option(int32_t option, int64_t value) {
     switch (option) {
         case TBF_OPT_PIPELINE:
             g_pipeline = value != 0;
+            return TBF_OK;
+        case TBF_OPT_P1_OCC:
+            if (value < 2 || value > 3) return fail(TBF_ERR_PARAM, "pass-1 occupancy must be 2 or 3");
+            g_p1_occ = (int)value;
             return TBF_OK;
         case TBF_OPT_P2_CHUNKS:
             g_p2_chunks = (int)std::max<int64_t>(0, value);
