@@ -1131,6 +1131,172 @@ __global__ void __launch_bounds__(P2T_THREADS, MINB) k_pass2_tma(const __grid_co
     }
 }
 
+// ---------------------------------------------------------------------------
+// Pass 2, cp.async-staged variant with G terms per thread (G = 4 halves the
+// partial num/den and fT traffic of G = 2).  Each thread streams its own
+// 16-byte F_loc slices (and its fT sample) P2A_DEPTH steps ahead into private
+// shared-memory slots with cp.async; no producer warp, no block barriers, no
+// register prefetch buffers (so G = 4 fits the 3-blocks/SM register budget).
+// ---------------------------------------------------------------------------
+
+constexpr int P2A_DEPTH = 8;
+
+template <int G>
+constexpr int p2a_smem_bytes() {
+    return P2A_DEPTH * P2_THREADS * (G * 16 + 4);
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int G>
+__global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_async(const __grid_constant__ Pass2Args a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    float4* Fs = reinterpret_cast<float4*>(sm);                                  // [DEPTH][G][128]
+    float* Ts = reinterpret_cast<float*>(Fs + P2A_DEPTH * G * P2_THREADS);       // [DEPTH][128]
+    const int tid = threadIdx.x;
+    const int nrb = (a.H + P2_THREADS - 1) / P2_THREADS;
+    const int chunk = blockIdx.x / nrb;
+    const int i_raw = (blockIdx.x % nrb) * P2_THREADS + tid;
+    const int H = a.H, W = a.W;
+    const bool iv = i_raw < H;
+    const int i = iv ? i_raw : H - 1;
+    const int grp = blockIdx.y;
+    const int b = blockIdx.z;
+    const int j0 = grp * G;
+    const int nt = min(G, a.t.n - j0);
+    const Casc k = a.k;
+    float nu_hi[G], nu_lo[G], wt[G];
+    const float4* fl[G];
+    const float4* crp[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const int j = min(j0 + g, a.t.n - 1);
+        nu_hi[g] = a.t.nu_hi[j];
+        nu_lo[g] = a.t.nu_lo[j];
+        wt[g] = g < nt ? a.t.w[j] * a.wscale : 0.f;
+        fl[g] = reinterpret_cast<const float4*>(a.floc) +
+                (((size_t)j * a.B + b) * nrb + i / FL_RB) * W * (size_t)FL_RB + (i % FL_RB);
+        crp[g] = reinterpret_cast<const float4*>(a.carry) + (((size_t)j * a.B + b) * a.ntx * H + i) * 4;
+    }
+    const float* fT = a.fT + xm_index(b, 0, i, W, H);
+    const size_t xpl = xm_plane(a.B, W, H);
+    float* pn = a.part + (size_t)(grp * 2 + 0) * xpl + xm_index(b, 0, i_raw, W, H);
+    float* pd = a.part + (size_t)(grp * 2 + 1) * xpl + xm_index(b, 0, i_raw, W, H);
+
+    const int t_lo = chunk * a.tiles_per_chunk;
+    const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
+    const bool last_chunk = t_hi == a.ntx;
+    const int x_hi = last_chunk ? W - 1 : min(W, (t_hi + a.warm_tiles) * TILE) - 1;
+    const int x_lo = t_lo * TILE;
+    const int x_out = min(W, t_hi * TILE);  // outputs for x < x_out
+    const int nx = x_hi - x_lo + 1;
+
+    auto issue = [&](int s) {  // stage slot s % DEPTH <- step s (x = x_hi - s), clamped
+        const int x = max(x_hi - s, x_lo);
+        const int slot = s % P2A_DEPTH;
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+            cp_async16(&Fs[(slot * G + g) * P2_THREADS + tid], fl[g] + (size_t)x * FL_RB);
+        cp_async4(&Ts[slot * P2_THREADS + tid], fT + (size_t)x * FL_RB);
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < P2A_DEPTH - 1; ++s) issue(s);
+
+    float C[G][4][4];
+    auto load_C = [&](int t) {
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const float4 v = crp[g][(size_t)t * H * 4 + p];
+                C[g][p][0] = v.x;
+                C[g][p][1] = v.y;
+                C[g][p][2] = v.z;
+                C[g][p][3] = v.w;
+            }
+    };
+    float p1[G][4], p2[G][4], q1[G][4], q2[G][4];
+    load_C(x_hi >> 5);
+    if (last_chunk) {  // exact start state from the chain
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int j = min(j0 + g, a.t.n - 1);
+            const float4* bs = reinterpret_cast<const float4*>(a.bstate) + (((size_t)j * a.B + b) * H + i) * 4;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const float4 v = bs[p];
+                p1[g][p] = v.x;
+                p2[g][p] = v.y;
+                q1[g][p] = v.z;
+                q2[g][p] = v.w;
+            }
+        }
+    } else {  // warm-up: steady state of the exact forward output at x_hi
+        const float4 h = *reinterpret_cast<const float4*>(&a.Hm[x_hi & 31][0]);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const float4 fo = fl[g][(size_t)x_hi * FL_RB];
+            const float fin[4] = {fo.x, fo.y, fo.z, fo.w};
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const float F = fmaf(h.x, C[g][p][0], fmaf(h.y, C[g][p][1],
+                                     fmaf(h.z, C[g][p][2], fmaf(h.w, C[g][p][3], fin[p]))));
+                csteady(F, p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
+            }
+        }
+    }
+
+#pragma unroll 1
+    for (int s = 0; s < nx; ++s) {
+        issue(s + P2A_DEPTH - 1);
+        cp_async_wait<P2A_DEPTH - 1>();  // step s has landed (own slots only)
+        const int x = x_hi - s;
+        const int m = x & 31;
+        if (m == 31 && s > 0) load_C(x >> 5);
+        const int slot = s % P2A_DEPTH;
+        const float4 h = *reinterpret_cast<const float4*>(&a.Hm[m][0]);
+        const bool out = x < x_out;
+        const float fv = Ts[slot * P2_THREADS + tid];
+        float num = 0.f, den = 0.f;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const float4 fo = Fs[(slot * G + g) * P2_THREADS + tid];
+            const float fin[4] = {fo.x, fo.y, fo.z, fo.w};
+            float y[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                float F = fmaf(h.x, C[g][p][0], fin[p]);
+                F = fmaf(h.y, C[g][p][1], F);
+                F = fmaf(h.z, C[g][p][2], F);
+                F = fmaf(h.w, C[g][p][3], F);
+                y[p] = cstep(F, p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
+            }
+            if (out) {
+                float sn, cs;
+                sincos_fma(fmaf(nu_hi[g], fv, nu_lo[g] * fv), &sn, &cs);
+                num = fmaf(wt[g], fmaf(cs, y[2], sn * y[3]), num);
+                den = fmaf(wt[g], fmaf(cs, y[0], sn * y[1]), den);
+            }
+        }
+        if (out && iv) {
+            pn[(size_t)x * FL_RB] = num;
+            pd[(size_t)x * FL_RB] = den;
+        }
+    }
+    cp_async_wait<0>();
+}
+
 template <int G>
 __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_gauss(const __grid_constant__ Pass2Args a) {
     const int nrb = (a.H + P2_THREADS - 1) / P2_THREADS;
@@ -1576,7 +1742,7 @@ struct Layout {
 int g_pass1_fold = 0;   // see run_terms
 int g_p1_occ = 3;       // tbf_set_option(TBF_OPT_P1_OCC): pass-1 blocks per SM (2 leaves room for a pass-2 block)
 int g_p2_chunks = 0;    // tbf_set_option(TBF_OPT_P2_CHUNKS): 0 = automatic
-int g_pass2_tma = 0;    // tbf_set_option(TBF_OPT_PASS2_TMA) (measured slower so far: see DESIGN.md)
+int g_pass2_tma = 3;    // tbf_set_option(TBF_OPT_PASS2_TMA): 0 register prefetch (G=2), 1/2 TMA producer warp, 3 cp.async G=4 (default)
 int g_pipeline = 0;     // tbf_set_option(TBF_OPT_PIPELINE) (measured: no gain on B200, SMs time-slice)
 int g_auto_batches = 2; // tbf_set_option(TBF_OPT_BATCHES): batches when batch_terms <= 0
 
@@ -1735,6 +1901,8 @@ constexpr int P1_SMEM_OCC2 = 80 * 1024;  // padded request: at most 2 pass-1 blo
 void set_p1_smem() {
     static bool done = false;
     if (done) return;
+    cudaFuncSetAttribute(k_pass2_async<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         p2a_smem_bytes<4>());
     cudaFuncSetAttribute(k_pass2_tma<G2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          p2t_smem_bytes<G2>());
     cudaFuncSetAttribute(k_pass2_tma<G2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1905,7 +2073,8 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.ntx = L.ntx;
         p2.k = kc;
         p2.t = td;
-        p2.ngroups = (n + G2 - 1) / G2;
+        const int g2run = (!box && g_pass2_tma == 3) ? 4 : G2;  // terms per pass-2 thread this launch
+        p2.ngroups = (n + g2run - 1) / g2run;
         for (int m = 0; m < TILE; ++m)
             for (int q = 0; q < 4; ++q) p2.Hm[m][q] = box ? 0.f : (float)Hm[m][q];
         {
@@ -1934,7 +2103,8 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         } else if (!box) {
             const long long threads = (long long)nrb * P2_THREADS * p2.ngroups * B;
             const long long target = 148LL * 12 * 32 * 3 / 2;  // ~1.5 waves of 12 warps/SM
-            while (threads * nchunk < target && nchunk < 64) {
+            const int max_chunks = g2run == 4 ? 2 : 64;  // measured: G=4 prefers fewer, longer rows
+            while (threads * nchunk < target && nchunk < max_chunks) {
                 const int tpc = (L.ntx + 2 * nchunk - 1) / (2 * nchunk);
                 if (tpc < 4 * p2.warm_tiles) break;  // keep warm-up <= 25% of a chunk
                 nchunk *= 2;
@@ -1947,6 +2117,8 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             Prof pr(KK_PASS2, s2);
             if (box)
                 k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, s2>>>(p2, sp->radius);
+            else if (g_pass2_tma == 3)
+                k_pass2_async<4><<<g2, P2_THREADS, p2a_smem_bytes<4>(), s2>>>(p2);
             else if ((W % TILE) == 0 && g_pass2_tma == 1)
                 k_pass2_tma<G2, 3><<<g2, P2T_THREADS, p2t_smem_bytes<G2>(), s2>>>(p2);
             else if ((W % TILE) == 0 && g_pass2_tma == 2)
@@ -2023,7 +2195,7 @@ int tbf_set_option(int32_t option, int64_t value) {
             g_p2_chunks = (int)std::max<int64_t>(0, value);
             return TBF_OK;
         case TBF_OPT_PASS2_TMA:
-            g_pass2_tma = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
+            g_pass2_tma = (int)std::max<int64_t>(0, std::min<int64_t>(3, value));
             return TBF_OK;
         case TBF_OPT_BATCHES:
             if (value < 1) return fail(TBF_ERR_PARAM, "batches must be >= 1");

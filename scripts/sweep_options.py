@@ -11,11 +11,10 @@ f = torch.from_numpy(workloads.make_input(cfg, frames=min(cfg.frames, 8))).cuda(
 k = tb.make_trig_kernel(cfg.sigma_r, cfg.T)
 spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
 flush = torch.empty(128 << 20, device="cuda")
-variants = [("default", {}), ("occ2", {4: 2}), ("pipe", {0: 1}), ("pipe_occ2", {0: 1, 4: 2}),
-            ("pipe_occ2_b3", {0: 1, 4: 2, 1: 3}), ("pipe_occ2_b4", {0: 1, 4: 2, 1: 4}), ("pipe_occ2_tma2", {0: 1, 4: 2, 2: 2}),
+variants = [("default", {}), ("reg2", {2: 0}), ("async4_c1", {3: 1}), ("async4_c2", {3: 2}),
             ]
 for name, opts in variants:
-    for o, v in {0: 0, 2: 0, 3: 0, 4: 3, 1: 2}.items():
+    for o, v in {0: 0, 2: 3, 3: 0, 4: 3, 1: 2}.items():
         lib.tbf_set_option(o, v)
     for o, v in opts.items():
         lib.tbf_set_option(o, v)

@@ -314,13 +314,14 @@ def test_options_match_default(tb):
     from paper_1105_4204_b200 import _native, workloads
 
     lib = _native.load()
+    DEFAULTS = {_native.TBF_OPT_PASS2_TMA: 3, _native.TBF_OPT_PIPELINE: 0, _native.TBF_OPT_P2_CHUNKS: 0}
     cfg = workloads.CONFIGS[2]
     f = torch.from_numpy(workloads.frame(cfg, 0)[:512, :768].copy()).cuda()
     k = tb.make_trig_kernel(cfg.sigma_r)
     spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
     base = tb.TrigFilter(tuple(f.shape), spec, k)(f)
     try:
-        for opts in ({_native.TBF_OPT_PASS2_TMA: 1}, {_native.TBF_OPT_PASS2_TMA: 2},
+        for opts in ({_native.TBF_OPT_PASS2_TMA: 1}, {_native.TBF_OPT_PASS2_TMA: 2}, {_native.TBF_OPT_PASS2_TMA: 0},
                      {_native.TBF_OPT_PIPELINE: 1}, {_native.TBF_OPT_P2_CHUNKS: 1}):
             for o, v in opts.items():
                 lib.tbf_set_option(o, v)
@@ -328,10 +329,10 @@ def test_options_match_default(tb):
             torch.cuda.synchronize()
             assert float((out - base).abs().max()) < 1e-3, opts
             for o in opts:
-                lib.tbf_set_option(o, 0)
+                lib.tbf_set_option(o, DEFAULTS[o])
     finally:
-        for o in (_native.TBF_OPT_PASS2_TMA, _native.TBF_OPT_PIPELINE, _native.TBF_OPT_P2_CHUNKS):
-            lib.tbf_set_option(o, 0)
+        for o, v in DEFAULTS.items():
+            lib.tbf_set_option(o, v)
 
 
 def test_batch_with_y_chunks_matches_single(tb):
