@@ -28,6 +28,7 @@ TBF_OPT_BATCHES = 1
 TBF_OPT_PASS2_TMA = 2
 TBF_OPT_P2_CHUNKS = 3
 TBF_OPT_P1_OCC = 4
+TBF_OPT_P1_YCHUNKS = 5
 
 TBF_SPATIAL_RECURSIVE = 0
 TBF_SPATIAL_BOX = 1

@@ -962,8 +962,10 @@ __global__ void __launch_bounds__(P2T_THREADS, MINB) k_pass2_tma(const __grid_co
 
     const int t_lo = chunk * a.tiles_per_chunk;
     const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
-    const bool last_chunk = t_hi == a.ntx;
-    const int t_top = last_chunk ? a.ntx - 1 : min(a.ntx - 1, t_hi - 1 + a.warm_tiles);
+    // a chunk whose warm-up would reach the right edge starts there from the
+    // exact chained backward state instead (a clamped warm-up would be < K)
+    const bool last_chunk = t_hi + a.warm_tiles >= a.ntx;
+    const int t_top = last_chunk ? a.ntx - 1 : t_hi - 1 + a.warm_tiles;
     const int ntiles = t_top - t_lo + 1;
     const int nblk = ntiles * (TILE / P2T_STEPS);
     const int x_top = t_top * TILE + TILE - 1;
@@ -1195,8 +1197,10 @@ __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_async(const __grid_cons
 
     const int t_lo = chunk * a.tiles_per_chunk;
     const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
-    const bool last_chunk = t_hi == a.ntx;
-    const int x_hi = last_chunk ? W - 1 : min(W, (t_hi + a.warm_tiles) * TILE) - 1;
+    // a chunk whose warm-up would reach the right edge starts there from the
+    // exact chained backward state instead (a clamped warm-up would be < K)
+    const bool last_chunk = t_hi + a.warm_tiles >= a.ntx;
+    const int x_hi = last_chunk ? W - 1 : (t_hi + a.warm_tiles) * TILE - 1;
     const int x_lo = t_lo * TILE;
     const int x_out = min(W, t_hi * TILE);  // outputs for x < x_out
     const int nx = x_hi - x_lo + 1;
@@ -1329,7 +1333,8 @@ __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_gauss(const __grid_cons
     const int t_lo = chunk * a.tiles_per_chunk;
     const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
     float p1[G][4], p2[G][4], q1[G][4], q2[G][4];
-    if (t_hi == a.ntx) {  // rightmost chunk: exact start state from the chain
+    const bool exact_start = t_hi + a.warm_tiles >= a.ntx;  // warm-up would reach the edge
+    if (exact_start) {  // start at the right edge from the exact chained state
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             const int j = min(j0 + g, a.t.n - 1);
@@ -1343,6 +1348,8 @@ __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_gauss(const __grid_cons
                 q2[g][p] = v.w;
             }
         }
+#pragma unroll 1
+        for (int t = a.ntx - 1; t >= t_hi; --t) p2_tile<G, false>(a, c, t, p1, p2, q1, q2, pn, pd, iv);
     } else {
         // warm-up: start from the steady state of the exact forward output at
         // the warm-up start, then run backward (no output) down to t_hi
@@ -1740,9 +1747,10 @@ struct Layout {
 };
 
 int g_pass1_fold = 0;   // see run_terms
+int g_p1_ychunks = 0;   // tbf_set_option(TBF_OPT_P1_YCHUNKS): 0 = automatic
 int g_p1_occ = 3;       // tbf_set_option(TBF_OPT_P1_OCC): pass-1 blocks per SM (2 leaves room for a pass-2 block)
 int g_p2_chunks = 0;    // tbf_set_option(TBF_OPT_P2_CHUNKS): 0 = automatic
-int g_pass2_tma = 3;    // tbf_set_option(TBF_OPT_PASS2_TMA): 0 register prefetch (G=2), 1/2 TMA producer warp, 3 cp.async G=4 (default)
+int g_pass2_tma = 3;    // tbf_set_option(TBF_OPT_PASS2_TMA): 0 register prefetch (G=2), 1/2 TMA producer warp, 3 auto (default), 4 cp.async G=4
 int g_pipeline = 0;     // tbf_set_option(TBF_OPT_PIPELINE) (measured: no gain on B200, SMs time-slice)
 int g_auto_batches = 2; // tbf_set_option(TBF_OPT_BATCHES): batches when batch_terms <= 0
 
@@ -1785,9 +1793,14 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
         int nyc = 1;
         while (warps * nyc < target) {
             const int rows = ((H + 2 * nyc - 1) / (2 * nyc) + TILE - 1) / TILE * TILE;
-            if (rows < 6 * L->ywarm) break;
+            // long chunks: warm-up <= 1/6; below one wave of warps (latency-
+            // bound small images) accept warm-up up to the chunk length
+            const bool ok = rows >= 6 * L->ywarm ||
+                            (warps * nyc < 148LL * 4 * P1_BLOCKS_PER_SM && rows >= L->ywarm);
+            if (!ok) break;
             nyc *= 2;
         }
+        if (g_p1_ychunks > 0) nyc = std::min(g_p1_ychunks, (H + TILE - 1) / TILE);
         L->ych_rows = ((H + nyc - 1) / nyc + TILE - 1) / TILE * TILE;
         L->nyc = (H + L->ych_rows - 1) / L->ych_rows;
     }
@@ -2073,7 +2086,15 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.ntx = L.ntx;
         p2.k = kc;
         p2.t = td;
-        const int g2run = (!box && g_pass2_tma == 3) ? 4 : G2;  // terms per pass-2 thread this launch
+        // pass-2 variant: cp.async with 4 terms/thread when rows x term groups
+        // fill >= 2 waves (configs 3-5), else register prefetch with 2 (1-2)
+        int p2var = g_pass2_tma;
+        if (!box && p2var == 3) {
+            const long long thr4 = (long long)((H + P2_THREADS - 1) / P2_THREADS) * P2_THREADS *
+                                   ((n + 3) / 4) * B;
+            p2var = thr4 >= 2LL * 148 * 12 * 32 ? 4 : 0;
+        }
+        const int g2run = (!box && p2var == 4) ? 4 : G2;  // terms per pass-2 thread this launch
         p2.ngroups = (n + g2run - 1) / g2run;
         for (int m = 0; m < TILE; ++m)
             for (int q = 0; q < 4; ++q) p2.Hm[m][q] = box ? 0.f : (float)Hm[m][q];
@@ -2103,10 +2124,16 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         } else if (!box) {
             const long long threads = (long long)nrb * P2_THREADS * p2.ngroups * B;
             const long long target = 148LL * 12 * 32 * 3 / 2;  // ~1.5 waves of 12 warps/SM
-            const int max_chunks = g2run == 4 ? 2 : 64;  // measured: G=4 prefers fewer, longer rows
+            const long long wave = 148LL * 12 * 32;
+            // measured: G=4 prefers fewer, longer rows unless the GPU is far from full
+            const int max_chunks = (g2run == 4 && threads * 2 >= wave) ? 2 : 64;
             while (threads * nchunk < target && nchunk < max_chunks) {
                 const int tpc = (L.ntx + 2 * nchunk - 1) / (2 * nchunk);
-                if (tpc < 4 * p2.warm_tiles) break;  // keep warm-up <= 25% of a chunk
+                // warm-up <= 25% of a chunk; below one wave (latency-bound small
+                // images) accept warm-up up to the chunk length
+                const bool ok = tpc >= 4 * p2.warm_tiles ||
+                                (threads * nchunk < wave && tpc >= p2.warm_tiles);
+                if (!ok) break;
                 nchunk *= 2;
             }
         }
@@ -2117,11 +2144,11 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             Prof pr(KK_PASS2, s2);
             if (box)
                 k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, s2>>>(p2, sp->radius);
-            else if (g_pass2_tma == 3)
+            else if (p2var == 4)
                 k_pass2_async<4><<<g2, P2_THREADS, p2a_smem_bytes<4>(), s2>>>(p2);
-            else if ((W % TILE) == 0 && g_pass2_tma == 1)
+            else if ((W % TILE) == 0 && p2var == 1)
                 k_pass2_tma<G2, 3><<<g2, P2T_THREADS, p2t_smem_bytes<G2>(), s2>>>(p2);
-            else if ((W % TILE) == 0 && g_pass2_tma == 2)
+            else if ((W % TILE) == 0 && p2var == 2)
                 k_pass2_tma<G2, 2><<<g2, P2T_THREADS, p2t_smem_bytes<G2>(), s2>>>(p2);
             else
                 k_pass2_gauss<G2><<<g2, P2_THREADS, 0, s2>>>(p2);
@@ -2187,6 +2214,9 @@ int tbf_set_option(int32_t option, int64_t value) {
         case TBF_OPT_PIPELINE:
             g_pipeline = value != 0;
             return TBF_OK;
+        case TBF_OPT_P1_YCHUNKS:
+            g_p1_ychunks = (int)std::max<int64_t>(0, value);
+            return TBF_OK;
         case TBF_OPT_P1_OCC:
             if (value < 2 || value > 3) return fail(TBF_ERR_PARAM, "pass-1 occupancy must be 2 or 3");
             g_p1_occ = (int)value;
@@ -2195,7 +2225,7 @@ int tbf_set_option(int32_t option, int64_t value) {
             g_p2_chunks = (int)std::max<int64_t>(0, value);
             return TBF_OK;
         case TBF_OPT_PASS2_TMA:
-            g_pass2_tma = (int)std::max<int64_t>(0, std::min<int64_t>(3, value));
+            g_pass2_tma = (int)std::max<int64_t>(0, std::min<int64_t>(4, value));
             return TBF_OK;
         case TBF_OPT_BATCHES:
             if (value < 1) return fail(TBF_ERR_PARAM, "batches must be >= 1");
