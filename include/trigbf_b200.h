@@ -142,7 +142,7 @@ TBF_API int tbf_profile_collect(double* ms, long long* launches, int32_t n);
 #define TBF_OPT_P1_YCHUNKS 5 /* default 0 = automatic row chunks per pass-1 column */
 #define TBF_OPT_PASS2_TMA 2 /* pass-2 variant: 0 register prefetch (2 terms/thread), 1|2 TMA bulk
                                copies + mbarriers with a producer warp (3|2 blocks/SM, W % 32 == 0),
-                               3 (default) automatic: 4 when rows x term groups fill 2 waves, else 0,
+                               3 (default) automatic: 4 when rows x term groups fill a wave, else 0,
                                4 per-thread cp.async staging, 4 terms/thread */
 TBF_API int tbf_set_option(int32_t option, int64_t value);
 

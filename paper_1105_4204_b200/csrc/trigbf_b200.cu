@@ -2087,12 +2087,12 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.k = kc;
         p2.t = td;
         // pass-2 variant: cp.async with 4 terms/thread when rows x term groups
-        // fill >= 2 waves (configs 3-5), else register prefetch with 2 (1-2)
+        // fill >= 1 wave (configs 3-5), else register prefetch with 2 (1-2)
         int p2var = g_pass2_tma;
         if (!box && p2var == 3) {
             const long long thr4 = (long long)((H + P2_THREADS - 1) / P2_THREADS) * P2_THREADS *
                                    ((n + 3) / 4) * B;
-            p2var = thr4 >= 2LL * 148 * 12 * 32 ? 4 : 0;
+            p2var = thr4 >= 148LL * 12 * 32 ? 4 : 0;
         }
         const int g2run = (!box && p2var == 4) ? 4 : G2;  // terms per pass-2 thread this launch
         p2.ngroups = (n + g2run - 1) / g2run;

@@ -11,7 +11,7 @@ f = torch.from_numpy(workloads.make_input(cfg, frames=min(cfg.frames, 8))).cuda(
 k = tb.make_trig_kernel(cfg.sigma_r, cfg.T)
 spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
 flush = torch.empty(128 << 20, device="cuda")
-variants = [("default", {}), ("reg2", {2: 0}), ("y1", {5: 1}), ("y2", {5: 2}), ("y4", {5: 4}), ("y8", {5: 8}), ("y4c4", {5: 4, 3: 4}), ("y8c8", {5: 8, 3: 8}),
+variants = [("default", {}), ("reg2", {2: 0}), ("async4", {2: 4}), 
             ]
 for name, opts in variants:
     for o, v in {0: 0, 2: 3, 3: 0, 4: 3, 1: 2, 5: 0}.items():
