@@ -13,6 +13,7 @@ from .engines import (
     bilateral_color,
     bilateral_trig,
     bilateral_trig_color,
+    clear_plans,
     get_plan,
 )
 from .errors import DimensionError, NativeUnavailableError, ParameterError, TrigbfError
@@ -43,7 +44,7 @@ __all__ = [
     "Boundary", "DEGREE_TABLE_8BIT", "DimensionError", "ETA_GUARD", "EngineDiagnostics",
     "ErrorStats", "Image", "NativeUnavailableError", "ParameterError", "SpatialKind",
     "SpatialSpec", "TermPairs", "TrigFilter", "TrigKernel", "TrigbfError", "bilateral_color",
-    "bilateral_trig", "bilateral_trig_color", "decay_length", "degree_estimate", "error_stats",
+    "bilateral_trig", "bilateral_trig_color", "clear_plans", "decay_length", "degree_estimate", "error_stats",
     "gaussian_eval", "get_plan", "image_from_planes", "make_trig_kernel", "recursive_biquads",
     "recursive_coeffs", "select_degree", "term_pairs", "trig_eval",
 ]

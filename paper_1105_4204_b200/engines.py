@@ -242,9 +242,22 @@ def get_plan(shape, spatial: SpatialSpec, kernel: TrigKernel, device=None) -> Tr
     if plan is None:
         while len(_PLANS) >= _MAX_PLANS:
             _PLANS.pop(next(iter(_PLANS)))
-        plan = TrigFilter(shape, spatial, kernel, device=dev)
+        try:
+            plan = TrigFilter(shape, spatial, kernel, device=dev)
+        except torch.cuda.OutOfMemoryError:
+            # cached plans hold large workspaces (up to ~80% of free memory for
+            # a 16k^2 image): drop them and size the new plan from scratch
+            _PLANS.clear()
+            torch.cuda.empty_cache()
+            plan = TrigFilter(shape, spatial, kernel, device=dev)
         _PLANS[key] = plan
     return plan
+
+
+def clear_plans() -> None:
+    """Release the cached plans and their device workspaces."""
+    _PLANS.clear()
+    _torch().cuda.empty_cache()
 
 
 def _check_kernel(kernel):
@@ -302,9 +315,15 @@ def bilateral_trig(img, spatial, kernel, *, workers: int = 1,
             raise DimensionError(f"unsupported input type {type(img).__name__}")
         if t.dim() not in (2, 3):
             raise DimensionError(f"expected [H, W] or [B, H, W], got shape {tuple(t.shape)}")
+        shape = (1, *t.shape) if t.dim() == 2 else tuple(t.shape)
+        if kind == "cpu" and shape[0] >= 4 and t.is_pinned() and t.dtype == torch.float32:
+            _require_cuda()
+            if diagnostics is not None:
+                diagnostics.degree = kernel.N
+                diagnostics.workers = workers
+            return _bilateral_trig_streamed(t, spatial, kernel, diagnostics)
         f = t.to(device="cuda" if not t.is_cuda else t.device, dtype=torch.float32,
                  non_blocking=bool(not t.is_cuda and t.is_pinned())).contiguous()
-        shape = (1, *f.shape) if f.dim() == 2 else tuple(f.shape)
     if diagnostics is not None:
         diagnostics.degree = kernel.N
         diagnostics.workers = workers
@@ -331,6 +350,64 @@ def bilateral_trig(img, spatial, kernel, *, workers: int = 1,
                       pin_memory=(kind == "cpu" and t.is_pinned()))
     res.copy_(out.reshape(t.shape))
     return res.numpy() if kind == "numpy" else res
+
+
+def _bilateral_trig_streamed(t, spatial, kernel, diagnostics, sub: int | None = None):
+    """Pinned host batch [B, H, W]: frames flow through the device in
+    sub-batches so host->device copies, filtering and device->host copies of
+    different sub-batches overlap (copy engines run beside the SMs).  Same
+    result as one call: frames are independent."""
+    torch = _torch()
+    B, H, W = t.shape
+    if sub is None:
+        sub = max(1, min(B, (B + 7) // 8))  # ~8 sub-batches
+    nsub = (B + sub - 1) // sub
+    dev = torch.device("cuda", torch.cuda.current_device())
+    comp = torch.cuda.current_stream(dev)
+    h2d = torch.cuda.Stream(dev)
+    d2h = torch.cuda.Stream(dev)
+    out_host = torch.empty((B, H, W), dtype=torch.float32, pin_memory=True)
+    d_in = [torch.empty((sub, H, W), dtype=torch.float32, device=dev) for _ in range(2)]
+    d_out = [torch.empty((sub, H, W), dtype=torch.float32, device=dev) for _ in range(2)]
+    plans = {}
+    ev_in = [torch.cuda.Event() for _ in range(nsub)]
+    ev_comp = [torch.cuda.Event() for _ in range(nsub)]
+    ev_out = [torch.cuda.Event() for _ in range(nsub)]
+    for kk in range(nsub):
+        b0, b1 = kk * sub, min(B, (kk + 1) * sub)
+        nb = b1 - b0
+        slot = kk % 2
+        with torch.cuda.stream(h2d):
+            if kk >= 2:  # the slot's previous compute has consumed it
+                h2d.wait_event(ev_comp[kk - 2])
+            d_in[slot][:nb].copy_(t[b0:b1], non_blocking=True)
+            ev_in[kk].record(h2d)
+        comp.wait_event(ev_in[kk])
+        if kk >= 2:  # the slot's previous result has been copied out
+            comp.wait_event(ev_out[kk - 2])
+        plan = plans.get(nb)
+        if plan is None:
+            plan = plans[nb] = get_plan((nb, H, W), spatial, kernel, device=dev)
+        plan(d_in[slot][:nb], d_out[slot][:nb])
+        ev_comp[kk].record(comp)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(ev_comp[kk])
+            out_host[b0:b1].copy_(d_out[slot][:nb], non_blocking=True)
+            ev_out[kk].record(d2h)
+    comp.wait_event(ev_out[nsub - 1])
+    bad = guarded = 0
+    for plan in plans.values():
+        b_, g_ = plan.read_counters()  # synchronizes
+        bad += b_
+        guarded += g_
+    torch.cuda.current_stream(dev).synchronize()
+    if bad:
+        raise ParameterError(
+            f"samples exceed the declared range [0, {kernel.T:g}]; rescale the input or raise T")
+    if diagnostics is not None:
+        diagnostics.spatial_passes += plans[next(iter(plans))].spatial_passes * B
+        diagnostics.guarded_pixels += guarded
+    return out_host
 
 
 def bilateral_color(img: Image, engine, workers: int = 1) -> Image:

@@ -346,3 +346,20 @@ def test_batch_with_y_chunks_matches_single(tb):
     for i in range(2):
         one = tb.bilateral_trig(torch.from_numpy(fs[i]).cuda(), spec, k).cpu().numpy()
         assert np.max(np.abs(batch[i] - one)) < 1e-3  # chunk counts differ with B (eps-level warm-ups)
+
+
+def test_pinned_host_batch_streamed_matches_device(tb):
+    """A pinned host batch goes through the copy/compute-overlapped sub-batch
+    path; frames are independent, so it equals the device-resident call."""
+    from paper_1105_4204_b200.workloads import rects_image
+
+    fs = np.stack([rects_image(96, 160, 6, seed=s) for s in range(9)])
+    k = tb.make_trig_kernel(25.0)
+    spec = tb.SpatialSpec.gaussian_recursive(5.0)
+    dev = tb.bilateral_trig(torch.from_numpy(fs).cuda(), spec, k).cpu().numpy()
+    pinned = torch.from_numpy(fs).pin_memory()
+    diag = tb.EngineDiagnostics()
+    host = tb.bilateral_trig(pinned, spec, k, diagnostics=diag)
+    assert not host.is_cuda and host.shape == pinned.shape
+    assert np.max(np.abs(host.numpy() - dev)) < 1e-3
+    assert diag.spatial_passes == 9 * (2 * (k.N + 1) - (1 if k.N % 2 == 0 else 0))
