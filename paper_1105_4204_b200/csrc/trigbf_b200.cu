@@ -525,6 +525,11 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
         {
             const int ns = step + 1 < nseg ? step + 1 : max(nsteps - 2 - step, 0);
             const int r0 = R0 + ns * TILE;
+            if (step + 1 >= nseg && step + 1 < nsteps) {  // checkpoint first (before the f burst)
+                const float4* ck = ck0 + (size_t)ns * cks;  // after this step's store (same thread)
+#pragma unroll
+                for (int p = 0; p < 4; ++p) ckn[p] = ck[p];
+            }
             if (r0 >= 0 && r0 + TILE <= H) {  // interior segment: no mirror / clamp
                 const float* fp = fcol + (size_t)r0 * W;
 #pragma unroll
@@ -532,11 +537,6 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
             } else {
 #pragma unroll
                 for (int q = 0; q < TILE; ++q) nxt[q] = fload(r0 + q);
-            }
-            if (step + 1 >= nseg && step + 1 < nsteps) {
-                const float4* ck = ck0 + (size_t)ns * cks;  // after this step's store (same thread)
-#pragma unroll
-                for (int p = 0; p < 4; ++p) ckn[p] = ck[p];
             }
         }
         // forward over the segment into the smem tile (own column); the first
@@ -1916,6 +1916,8 @@ void set_p1_smem() {
     if (done) return;
     cudaFuncSetAttribute(k_pass2_async<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          p2a_smem_bytes<4>());
+    cudaFuncSetAttribute(k_pass2_async<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         p2a_smem_bytes<2>());
     cudaFuncSetAttribute(k_pass2_tma<G2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          p2t_smem_bytes<G2>());
     cudaFuncSetAttribute(k_pass2_tma<G2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2095,6 +2097,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             p2var = thr4 >= 148LL * 12 * 32 ? 4 : 0;
         }
         const int g2run = (!box && p2var == 4) ? 4 : G2;  // terms per pass-2 thread this launch
+        // (p2var 5: cp.async staging with 2 terms/thread)
         p2.ngroups = (n + g2run - 1) / g2run;
         for (int m = 0; m < TILE; ++m)
             for (int q = 0; q < 4; ++q) p2.Hm[m][q] = box ? 0.f : (float)Hm[m][q];
@@ -2146,6 +2149,8 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, s2>>>(p2, sp->radius);
             else if (p2var == 4)
                 k_pass2_async<4><<<g2, P2_THREADS, p2a_smem_bytes<4>(), s2>>>(p2);
+            else if (p2var == 5)
+                k_pass2_async<2><<<g2, P2_THREADS, p2a_smem_bytes<2>(), s2>>>(p2);
             else if ((W % TILE) == 0 && p2var == 1)
                 k_pass2_tma<G2, 3><<<g2, P2T_THREADS, p2t_smem_bytes<G2>(), s2>>>(p2);
             else if ((W % TILE) == 0 && p2var == 2)
@@ -2225,7 +2230,7 @@ int tbf_set_option(int32_t option, int64_t value) {
             g_p2_chunks = (int)std::max<int64_t>(0, value);
             return TBF_OK;
         case TBF_OPT_PASS2_TMA:
-            g_pass2_tma = (int)std::max<int64_t>(0, std::min<int64_t>(4, value));
+            g_pass2_tma = (int)std::max<int64_t>(0, std::min<int64_t>(5, value));
             return TBF_OK;
         case TBF_OPT_BATCHES:
             if (value < 1) return fail(TBF_ERR_PARAM, "batches must be >= 1");
