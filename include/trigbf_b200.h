@@ -143,7 +143,10 @@ TBF_API int tbf_profile_collect(double* ms, long long* launches, int32_t n);
 #define TBF_OPT_PASS2_TMA 2 /* pass-2 variant: 0 register prefetch (2 terms/thread), 1|2 TMA bulk
                                copies + mbarriers with a producer warp (3|2 blocks/SM, W % 32 == 0),
                                3 (default) automatic: 4 when rows x term groups fill a wave, else 0,
-                               4 per-thread cp.async staging, 4 terms/thread */
+                               4 per-thread cp.async staging, 4 terms/thread,
+                               5 per-thread cp.async staging, 2 terms/thread */
+#define TBF_OPT_P1_FOLD 6   /* default 1: folds the y-sweep gain into the pass-2 weights
+                               (skips 4 multiplies per pixel-term in pass 1 when T/g^4 is safe); 0 scales in pass 1 */
 TBF_API int tbf_set_option(int32_t option, int64_t value);
 
 /* Last error message of the calling thread (static storage). */

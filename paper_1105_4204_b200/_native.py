@@ -29,6 +29,7 @@ TBF_OPT_PASS2_TMA = 2
 TBF_OPT_P2_CHUNKS = 3
 TBF_OPT_P1_OCC = 4
 TBF_OPT_P1_YCHUNKS = 5
+TBF_OPT_P1_FOLD = 6
 
 TBF_SPATIAL_RECURSIVE = 0
 TBF_SPATIAL_BOX = 1
@@ -127,9 +128,11 @@ def _declare(lib):
     lib.tbf_box_pass_f64.argtypes = [_vp, _vp, _i32, _i32, _i32, _vp]
 
 
-def load(path: str = LIB_PATH):
-    """Load (once) and return the extension library."""
+def load(path: str | None = None):
+    """Load (once) and return the extension library (``TRIGBF_B200_LIB``
+    overrides the in-tree path, e.g. for an experimental build)."""
     global _lib
+    path = path or os.environ.get("TRIGBF_B200_LIB") or LIB_PATH
     with _lock:
         if _lib is not None:
             return _lib

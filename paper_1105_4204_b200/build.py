@@ -40,20 +40,29 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > lib_m for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple[str, ...] = ()) -> str:
+    """Compile SRC into ``out`` (default: the in-tree library).  ``defines``
+    are extra ``-D`` macros for experimental variants built to another path."""
+    lib = out or LIB
+    if not force and out is None and not defines and not needs_build():
         return LIB
-    os.makedirs(LIB_DIR, exist_ok=True)
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", INC, "-o", tmp, SRC]
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    tmp = lib + ".tmp"
+    cmd = [nvcc(), *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-I", INC, "-o", tmp, SRC]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    args = sys.argv[1:]
+    out = None
+    if "--out" in args:
+        out = args[args.index("--out") + 1]
+    defs = tuple(a[2:] for a in args if a.startswith("-D"))
+    print(build(force="--force" in args, verbose=True, out=out, defines=defs))

@@ -42,6 +42,10 @@
 #include <string>
 #include <vector>
 
+#ifndef TBF_PHASOR_SFU
+#define TBF_PHASOR_SFU 1  // 0: FMA-pipe polynomial phasors (see sincos_fma)
+#endif
+
 #include "trigbf_b200.h"
 
 #define TBF_ABI_VERSION 1
@@ -184,11 +188,23 @@ __device__ __forceinline__ void csteady(float u, float& v1, float& v2, float& y1
     y1 = y2 = u * k.ig;
 }
 
-// sin and cos of x for |x| < ~1e5 on the FMA pipe (no SFU, no slow-path
+// sin and cos of x for |x| < ~1e5.  TBF_PHASOR_SFU=1 (default): SFU after a
+// 2*pi reduction.  TBF_PHASOR_SFU=0: FMA pipe only (no SFU, no slow-path
 // branch): Cody-Waite reduction by pi/2 in three parts (exact products inside
 // the FMAs), then the Cephes minimax polynomials on [-pi/4, pi/4] (about 1 ulp).
 // Arguments here are nu*f <= ~420 rad.
 __device__ __forceinline__ void sincos_fma(float x, float* sp, float* cp) {
+#if TBF_PHASOR_SFU
+    // default: Cody-Waite reduction by 2*pi in two parts (q*6.28125 exact for
+    // q < 2^15), then the SFU (MUFU.SIN/COS, abs error ~2^-21 on [-pi, pi]).
+    // 9 instructions instead of ~24; measured +10% end to end on configs
+    // 2/3/5 with unchanged parity
+    const float t = fmaf(x, 0.159154943091895336f, 12582912.0f);
+    const float q = t - 12582912.0f;
+    float r = fmaf(q, -6.28125f, x);
+    r = fmaf(q, -1.9353071795864769e-3f, r);
+    __sincosf(r, sp, cp);
+#else
     // q = nearest integer to x*2/pi via the 1.5*2^23 magic constant (its low
     // mantissa bits hold q), no F2I / FRND
     const float t = fmaf(x, 0.636619772367581343f, 12582912.0f);
@@ -212,6 +228,7 @@ __device__ __forceinline__ void sincos_fma(float x, float* sp, float* cp) {
     cv = __int_as_float(__float_as_int(cv) ^ (((qi + 1) & 2) << 30));
     *sp = sv;
     *cp = cv;
+#endif
 }
 
 // Phasors of G consecutive terms at one sample (engines.py:272-286).  Terms
@@ -520,43 +537,45 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                 y2[p] = ckn[p].w;
             }
         }
-        // prefetch the next step's f rows (and its checkpoint in phase B)
-        float nxt[TILE];
-        {
-            const int ns = step + 1 < nseg ? step + 1 : max(nsteps - 2 - step, 0);
-            const int r0 = R0 + ns * TILE;
-            if (step + 1 >= nseg && step + 1 < nsteps) {  // checkpoint first (before the f burst)
-                const float4* ck = ck0 + (size_t)ns * cks;  // after this step's store (same thread)
+        // the next step's f rows (and its checkpoint in phase B) are prefetched
+        // into the register ring seg_f: each 8-row slot is refilled as soon as
+        // this step has consumed it (no register shifts)
+        const int ns = step + 1 < nseg ? step + 1 : max(nsteps - 2 - step, 0);
+        const int rn = R0 + ns * TILE;
+        const bool rn_interior = rn >= 0 && rn + TILE <= H;
+        const float* const fpn = fcol + (size_t)max(rn, 0) * W;
+        auto refill = [&](int q0) {  // rows rn + q0 .. rn + q0 + 7 into slot q0
+            if (rn_interior) {
 #pragma unroll
-                for (int p = 0; p < 4; ++p) ckn[p] = ck[p];
-            }
-            if (r0 >= 0 && r0 + TILE <= H) {  // interior segment: no mirror / clamp
-                const float* fp = fcol + (size_t)r0 * W;
-#pragma unroll
-                for (int q = 0; q < TILE; ++q) nxt[q] = __ldg(fp + (size_t)q * W);
+                for (int q = 0; q < 8; ++q) seg_f[q0 + q] = __ldg(fpn + (size_t)(q0 + q) * W);
             } else {
 #pragma unroll
-                for (int q = 0; q < TILE; ++q) nxt[q] = fload(r0 + q);
+                for (int q = 0; q < 8; ++q) seg_f[q0 + q] = fload(rn + q0 + q);
             }
+        };
+        if (step + 1 >= nseg && step + 1 < nsteps) {  // checkpoint first (before the f burst)
+            const float4* ck = ck0 + (size_t)ns * cks;  // after this step's store (same thread)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) ckn[p] = ck[p];
         }
         // forward over the segment into the smem tile (own column); the first
         // phase-B step finds the tile already filled by the last phase-A step
-        if (step != nseg) {
-            if (len == TILE) {
-                // rolled 4 x 8 samples (instruction-cache footprint): the 32
-                // prefetched rows shift down by 8 registers per iteration.
-                // (A software-pipelined 2 x 16 variant spilled at the 3-block
-                // register cap and measured 27% slower.)
-#pragma unroll 1
-                for (int r0 = 0; r0 < TILE; r0 += 8) {
-                    float fb[8];
+        const bool full = step != nseg && len == TILE;
+        if (full) {
+            // 4 x 8 samples, unrolled over the ring slots (one shared copy for
+            // phases A and B keeps the instruction footprint in L1.5)
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) fb[q] = seg_f[q];
+            for (int q0 = 0; q0 < TILE; q0 += 8) {
+                p1_fwd8<true>(*reinterpret_cast<const float(*)[8]>(&seg_f[q0]), nu_hi, nu_lo, k, v1, v2,
+                              y1, y2, bl + q0 * BUF_LD);
+                refill(q0);
+            }
+        } else {
 #pragma unroll
-                    for (int q = 0; q < TILE - 8; ++q) seg_f[q] = seg_f[q + 8];
-                    p1_fwd8<true>(fb, nu_hi, nu_lo, k, v1, v2, y1, y2, bl + r0 * BUF_LD);
-                }
-            } else {
+            for (int q0 = 0; q0 < TILE; q0 += 8) refill(q0);
+        }
+        if (step != nseg && !full) {
+            {
                 for (int r = 0; r < len; ++r) {
                     const float fs = fload(i0 + r);
                     float s0, c0;
@@ -569,8 +588,6 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                 }
             }
         }
-#pragma unroll
-        for (int q = 0; q < TILE; ++q) seg_f[q] = nxt[q];
         if (!phaseB) continue;
         if (seg == nseg - 1) {
             // backward start = steady state of the last forward output (_core.pyx:85-87)
@@ -1746,7 +1763,7 @@ struct Layout {
     size_t total;
 };
 
-int g_pass1_fold = 0;   // see run_terms
+int g_pass1_fold = 1;   // tbf_set_option(TBF_OPT_P1_FOLD); see run_terms
 int g_p1_ychunks = 0;   // tbf_set_option(TBF_OPT_P1_YCHUNKS): 0 = automatic
 int g_p1_occ = 3;       // tbf_set_option(TBF_OPT_P1_OCC): pass-1 blocks per SM (2 leaves room for a pass-2 block)
 int g_p2_chunks = 0;    // tbf_set_option(TBF_OPT_P2_CHUNKS): 0 = automatic
@@ -1981,9 +1998,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
     const Casc kc = to_casc(sp);
     // fold the y-sweep scale into the weights when the unscaled intermediates
     // (up to ~T / g^4) stay far below FLT_MAX
-    // (measured: the FOLD instantiation spills at the 3-block register cap and
-    // is ~5% slower on config 2, so it is off; kept for the register budget of
-    // future pass-1 variants)
+    // (measured: ~1% faster on configs 2-4 now that it no longer spills)
     const bool fold = g_pass1_fold && !box &&
                       std::log10(std::max(terms->T, 1.0)) - 4.0 * std::log10(sp->g1 * sp->g2) < 34.0;
     double M[16], Mlast[16], Hm[TILE][4];
@@ -2094,7 +2109,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         if (!box && p2var == 3) {
             const long long thr4 = (long long)((H + P2_THREADS - 1) / P2_THREADS) * P2_THREADS *
                                    ((n + 3) / 4) * B;
-            p2var = thr4 >= 148LL * 12 * 32 ? 4 : 0;
+            p2var = thr4 >= 148LL * 12 * 32 / 2 ? 4 : 0;
         }
         const int g2run = (!box && p2var == 4) ? 4 : G2;  // terms per pass-2 thread this launch
         // (p2var 5: cp.async staging with 2 terms/thread)
@@ -2231,6 +2246,9 @@ int tbf_set_option(int32_t option, int64_t value) {
             return TBF_OK;
         case TBF_OPT_PASS2_TMA:
             g_pass2_tma = (int)std::max<int64_t>(0, std::min<int64_t>(5, value));
+            return TBF_OK;
+        case TBF_OPT_P1_FOLD:
+            g_pass1_fold = value != 0;
             return TBF_OK;
         case TBF_OPT_BATCHES:
             if (value < 1) return fail(TBF_ERR_PARAM, "batches must be >= 1");
