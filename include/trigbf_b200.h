@@ -95,6 +95,22 @@ TBF_API int tbf_bilateral_trig(const float* f, float* out, int32_t B, int32_t H,
                        void* workspace, size_t workspace_bytes,
                        unsigned long long* d_counters, void* stream);
 
+/* Host-buffer form of tbf_bilateral_trig: what a reference-side FFI binds
+ * with NumPy arrays (replaces engines.py:228-306 end to end, host in, host
+ * out).  h_f / h_out are host [B][H][W] fp32 arrays (pinned memory lets the
+ * copies overlap the filter; pageable memory works).  d_io is a device
+ * buffer of 2*B*H*W floats (input copy, then output); the workspace is sized
+ * by tbf_workspace_bytes as for tbf_bilateral_trig.  Column strips of h_f
+ * are copied on an internal stream and pass 1 starts on each strip as it
+ * lands; the output returns in row bands while later bands filter.  The
+ * range check runs on the device copy (d_counters[0], as tbf_range_check).
+ * Stream-ordered: h_out is complete and d_counters valid once `stream`
+ * reaches this point; h_f and h_out must stay valid until then. */
+TBF_API int tbf_bilateral_trig_host(const float* h_f, float* h_out, int32_t B, int32_t H, int32_t W,
+                            const tbf_spatial* sp, const tbf_terms* terms, int32_t batch_terms,
+                            float* d_io, void* workspace, size_t workspace_bytes,
+                            unsigned long long* d_counters, void* stream);
+
 /* Term-sharded piece: num/den[b][y][x] (+)= the contribution of pairs
  * [term_begin, term_end).  accumulate=0 overwrites num/den. */
 TBF_API int tbf_trig_partial(const float* f, float* num, float* den, int32_t B, int32_t H, int32_t W,
@@ -145,6 +161,8 @@ TBF_API int tbf_profile_collect(double* ms, long long* launches, int32_t n);
                                3 (default) automatic: 4 when rows x term groups fill a wave, else 0,
                                4 per-thread cp.async staging, 4 terms/thread,
                                5 per-thread cp.async staging, 2 terms/thread */
+#define TBF_OPT_HOST_STRIPS 7 /* default 4: column strips of tbf_bilateral_trig_host's input copy */
+#define TBF_OPT_HOST_BANDS 8  /* default 4: row bands of tbf_bilateral_trig_host's output copy */
 #define TBF_OPT_P1_FOLD 6   /* default 1: folds the y-sweep gain into the pass-2 weights
                                (skips 4 multiplies per pixel-term in pass 1 when T/g^4 is safe); 0 scales in pass 1 */
 TBF_API int tbf_set_option(int32_t option, int64_t value);

@@ -30,6 +30,8 @@ TBF_OPT_P2_CHUNKS = 3
 TBF_OPT_P1_OCC = 4
 TBF_OPT_P1_YCHUNKS = 5
 TBF_OPT_P1_FOLD = 6
+TBF_OPT_HOST_STRIPS = 7
+TBF_OPT_HOST_BANDS = 8
 
 TBF_SPATIAL_RECURSIVE = 0
 TBF_SPATIAL_BOX = 1
@@ -38,6 +40,7 @@ TBF_SPATIAL_BOX = 1
 EXPORTS = (
     "tbf_workspace_bytes",
     "tbf_bilateral_trig",
+    "tbf_bilateral_trig_host",
     "tbf_trig_partial",
     "tbf_finalize",
     "tbf_range_check",
@@ -100,6 +103,11 @@ def _declare(lib):
     lib.tbf_bilateral_trig.argtypes = [
         _vp, _vp, _i32, _i32, _i32, ctypes.POINTER(TbfSpatial), ctypes.POINTER(TbfTerms), _i32,
         _vp, _sz, _vp, _vp,
+    ]
+    lib.tbf_bilateral_trig_host.restype = ctypes.c_int
+    lib.tbf_bilateral_trig_host.argtypes = [
+        _vp, _vp, _i32, _i32, _i32, ctypes.POINTER(TbfSpatial), ctypes.POINTER(TbfTerms), _i32,
+        _vp, _vp, _sz, _vp, _vp,
     ]
     lib.tbf_trig_partial.restype = ctypes.c_int
     lib.tbf_trig_partial.argtypes = [

@@ -328,6 +328,7 @@ struct Pass1Args {
     int Ey, nseg;  // y mirror extension; checkpoint segments per y-chunk
     int nyc, ych_rows, ywarm;  // y-chunks of ych_rows output rows; warm-up rows (mult. of 32)
     int Ex, ne, edge_all, ntx;
+    int tile0, ntx_run;  // column tiles [tile0, tile0 + ntx_run) in this launch
     Casc k;
     TermDev t;
     int ngroups;    // ceil(t.n / G1)
@@ -362,6 +363,7 @@ struct Pass2Args {
     int ngroups;       // ceil(t.n / G2)
     float Hm[TILE][4]; // homogeneous response of the cascade to a unit state
     float wscale;      // g^2: undoes the two pure x sweeps (1 for box)
+    int rb0, nrb_run;     // 128-row blocks [rb0, rb0 + nrb_run) in this launch
     int tiles_per_chunk;  // x-chunking of rows (gauss); == ntx for one chunk
     int warm_tiles;       // warm-up tiles of a chunk's backward sweep
     const float* floc;
@@ -381,6 +383,7 @@ struct ReduceArgs {
     const float* f;       // guard fallback (when out != null)
     float* out;           // [B][H][W] guarded ratio when non-null
     unsigned long long* counters;
+    int i_base;           // first row of this launch (multiple of RED_I)
 };
 
 // ---------------------------------------------------------------------------
@@ -425,8 +428,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     if (term >= a.t.n) return;  // whole warp; no block-level barriers below
     const int b = blockIdx.z;
     const int H = a.H, W = a.W;
-    const int tile_x = blockIdx.x % a.ntx;
-    const int chunk = blockIdx.x / a.ntx;
+    const int tile_x = a.tile0 + blockIdx.x % a.ntx_run;
+    const int chunk = blockIdx.x / a.ntx_run;
     const int x0 = tile_x * TILE;
     const int x = x0 + lane;
     const bool xv = x < W;
@@ -966,9 +969,8 @@ __global__ void __launch_bounds__(P2T_THREADS, MINB) k_pass2_tma(const __grid_co
     float* Tb = reinterpret_cast<float*>(Fb + P2T_NST * P2T_STEPS * G * P2_THREADS);  // [NST][STEPS][128]
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
-    const int nrb = (a.H + P2_THREADS - 1) / P2_THREADS;
-    const int chunk = blockIdx.x / nrb;
-    const int i0 = (blockIdx.x % nrb) * P2_THREADS;
+    const int chunk = blockIdx.x / a.nrb_run;
+    const int i0 = (a.rb0 + blockIdx.x % a.nrb_run) * P2_THREADS;
     const int H = a.H, W = a.W;
     const int nrow = min(P2_THREADS, H - i0);
     const int nrow4 = (nrow + 3) & ~3;
@@ -1183,9 +1185,8 @@ __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_async(const __grid_cons
     float4* Fs = reinterpret_cast<float4*>(sm);                                  // [DEPTH][G][128]
     float* Ts = reinterpret_cast<float*>(Fs + P2A_DEPTH * G * P2_THREADS);       // [DEPTH][128]
     const int tid = threadIdx.x;
-    const int nrb = (a.H + P2_THREADS - 1) / P2_THREADS;
-    const int chunk = blockIdx.x / nrb;
-    const int i_raw = (blockIdx.x % nrb) * P2_THREADS + tid;
+    const int chunk = blockIdx.x / a.nrb_run;
+    const int i_raw = (a.rb0 + blockIdx.x % a.nrb_run) * P2_THREADS + tid;
     const int H = a.H, W = a.W;
     const bool iv = i_raw < H;
     const int i = iv ? i_raw : H - 1;
@@ -1204,7 +1205,7 @@ __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_async(const __grid_cons
         nu_lo[g] = a.t.nu_lo[j];
         wt[g] = g < nt ? a.t.w[j] * a.wscale : 0.f;
         fl[g] = reinterpret_cast<const float4*>(a.floc) +
-                (((size_t)j * a.B + b) * nrb + i / FL_RB) * W * (size_t)FL_RB + (i % FL_RB);
+                (((size_t)j * a.B + b) * ((H + FL_RB - 1) / FL_RB) + i / FL_RB) * W * (size_t)FL_RB + (i % FL_RB);
         crp[g] = reinterpret_cast<const float4*>(a.carry) + (((size_t)j * a.B + b) * a.ntx * H + i) * 4;
     }
     const float* fT = a.fT + xm_index(b, 0, i, W, H);
@@ -1320,9 +1321,8 @@ __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_async(const __grid_cons
 
 template <int G>
 __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_gauss(const __grid_constant__ Pass2Args a) {
-    const int nrb = (a.H + P2_THREADS - 1) / P2_THREADS;
-    const int chunk = blockIdx.x / nrb;
-    const int i_raw = (blockIdx.x % nrb) * P2_THREADS + threadIdx.x;
+    const int chunk = blockIdx.x / a.nrb_run;
+    const int i_raw = (a.rb0 + blockIdx.x % a.nrb_run) * P2_THREADS + threadIdx.x;
     const int H = a.H, W = a.W;
     const bool iv = i_raw < H;
     const int i = iv ? i_raw : H - 1;
@@ -1471,9 +1471,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32) k_pass1_box(const __grid_consta
 
 template <int G, int R>
 __global__ void __launch_bounds__(P2_THREADS) k_pass2_box(const __grid_constant__ Pass2Args a, int radius) {
-    const int nrb = (a.H + P2_THREADS - 1) / P2_THREADS;
-    const int chunk = blockIdx.x / nrb;
-    const int i_raw = (blockIdx.x % nrb) * P2_THREADS + threadIdx.x;
+    const int chunk = blockIdx.x / a.nrb_run;
+    const int i_raw = (a.rb0 + blockIdx.x % a.nrb_run) * P2_THREADS + threadIdx.x;
     const int H = a.H, W = a.W;
     const bool iv = i_raw < H;
     const int i = iv ? i_raw : H - 1;
@@ -1490,7 +1489,7 @@ __global__ void __launch_bounds__(P2_THREADS) k_pass2_box(const __grid_constant_
         nu_lo[g] = a.t.nu_lo[j];
         wt[g] = g < nt ? a.t.w[j] : 0.f;
         fl[g] = reinterpret_cast<const float4*>(a.floc) +
-                (((size_t)j * a.B + b) * nrb + i / FL_RB) * W * (size_t)FL_RB + (i % FL_RB);
+                (((size_t)j * a.B + b) * ((H + FL_RB - 1) / FL_RB) + i / FL_RB) * W * (size_t)FL_RB + (i % FL_RB);
     }
     const float* fT = a.fT + xm_index(b, 0, i, W, H);
     const size_t xpl = xm_plane(a.B, W, H);
@@ -1558,7 +1557,7 @@ __global__ void __launch_bounds__(256) k_reduce(const __grid_constant__ ReduceAr
     __shared__ float tn[TILE][RED_I + 4];
     __shared__ float td[TILE][RED_I + 4];
     const int b = blockIdx.z;
-    const int x0 = blockIdx.x * TILE, i0 = blockIdx.y * RED_I;
+    const int x0 = blockIdx.x * TILE, i0 = a.i_base + blockIdx.y * RED_I;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;  // 8 warps
     const size_t plane = xm_plane(a.B, a.W, a.H);
     const bool vec = true;  // row-block tiled partials: 4-row groups always aligned and padded
@@ -1770,6 +1769,8 @@ int g_p2_chunks = 0;    // tbf_set_option(TBF_OPT_P2_CHUNKS): 0 = automatic
 int g_pass2_tma = 3;    // tbf_set_option(TBF_OPT_PASS2_TMA): 0 register prefetch (G=2), 1/2 TMA producer warp, 3 auto (default), 4 cp.async G=4
 int g_pipeline = 0;     // tbf_set_option(TBF_OPT_PIPELINE) (measured: no gain on B200, SMs time-slice)
 int g_auto_batches = 2; // tbf_set_option(TBF_OPT_BATCHES): batches when batch_terms <= 0
+int g_host_strips = 4;  // tbf_set_option(TBF_OPT_HOST_STRIPS): column strips of the host input
+int g_host_bands = 4;   // tbf_set_option(TBF_OPT_HOST_BANDS): row bands of the host output
 
 int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, int batch_terms,
                 Layout* L) {
@@ -1856,16 +1857,19 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     return TBF_OK;
 }
 
-// Internal second stream per device for the pipelined batches.
-cudaStream_t aux_stream() {
+// Internal streams per device: 0 = pipelined batches, 1 = host->device
+// copies, 2/3 = pass-1 strips and pass-2 bands of the host pipeline, 4 =
+// device->host copies.
+constexpr int N_AUX = 5;
+cudaStream_t aux_stream(int idx = 0) {
     static std::mutex mu;
-    static cudaStream_t streams[64] = {};
+    static cudaStream_t streams[64][N_AUX] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> g(mu);
-    if (dev < 0 || dev >= 64) return nullptr;
-    if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
-    return streams[dev];
+    if (dev < 0 || dev >= 64 || idx < 0 || idx >= N_AUX) return nullptr;
+    if (!streams[dev][idx]) cudaStreamCreateWithFlags(&streams[dev][idx], cudaStreamNonBlocking);
+    return streams[dev][idx];
 }
 
 // Small pool of timing-free events (reused across calls).
@@ -1949,10 +1953,19 @@ void set_p1_smem() {
 // Core driver: pairs [tbeg, tend) in batches of L.tb terms.  Either
 // accumulates into caller num/den (row-major), or (out != null) writes the
 // guarded ratio.
+// Host-buffer I/O of tbf_bilateral_trig_host: f and out are device buffers,
+// h_f / h_out the caller's host arrays.
+struct HostIO {
+    const float* h_f;
+    float* h_out;
+    int strips;  // column strips: H2D of strip s+1 overlaps pass 1 of strip s
+    int bands;   // row bands: D2H of band b overlaps pass 2 of band b+1
+};
+
 int run_terms(const float* f, float* num, float* den, float* out, int B, int H, int W,
               const tbf_spatial* sp, const tbf_terms* terms, int tbeg, int tend, int batch_terms,
               int accumulate, void* ws, size_t ws_bytes, unsigned long long* counters,
-              cudaStream_t st) {
+              cudaStream_t st, const HostIO* hio = nullptr) {
     int rc = validate(sp, terms, tbeg, tend);
     if (rc) return rc;
     const int nrange = tend - tbeg;
@@ -1989,6 +2002,42 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         h_tab[2 * ld + j] = (float)terms->weight[tbeg + j];
     }
     cudaMemcpyAsync(tab, h_tab.data(), h_tab.size() * 4, cudaMemcpyHostToDevice, st);
+
+    // host input: column strips copied on an internal stream; pass 1 of the
+    // first batch runs strip by strip as they land (columns are independent
+    // in pass 1), the range check and transpose once the whole input is in
+    const bool hpipe = hio && !box && L.nslot == 1 && out;
+    std::vector<cudaEvent_t> ev_strip;
+    int tps = L.ntx;  // column tiles per strip
+    cudaEvent_t e_ready = nullptr;
+    if (hio) {
+        cudaStream_t sh = aux_stream(1);
+        if (!sh) return fail(TBF_ERR_CUDA, "no copy stream");
+        e_ready = event_get();
+        cudaEventRecord(e_ready, st);  // term table queued, earlier users of f done
+        cudaStreamWaitEvent(sh, e_ready, 0);
+        if (hpipe) {
+            const int ns = std::max(1, std::min(hio->strips, L.ntx));
+            tps = (L.ntx + ns - 1) / ns;
+        }
+        float* df = const_cast<float*>(f);
+        for (int t0 = 0; t0 < L.ntx; t0 += tps) {
+            const int x0 = t0 * TILE;
+            const int cols = std::min(W, (t0 + tps) * TILE) - x0;
+            cudaMemcpy2DAsync(df + x0, (size_t)W * 4, hio->h_f + x0, (size_t)W * 4, (size_t)cols * 4,
+                              (size_t)B * H, cudaMemcpyHostToDevice, sh);
+            ev_strip.push_back(event_get());
+            cudaEventRecord(ev_strip.back(), sh);
+        }
+        cudaStreamWaitEvent(st, ev_strip.back(), 0);
+        if ((rc = check_cuda("host to device"))) return rc;
+        if (counters) {
+            const long long count = (long long)B * H * W;
+            const long long blocks = std::min<long long>((count + 255) / 256, 148LL * 8);
+            Prof pr(KK_RANGE, st);
+            k_range_check<<<(unsigned)blocks, 256, 0, st>>>(f, count, -1e-9, terms->T + 1e-9, counters);
+        }
+    }
 
     dim3 tgrid((W + TILE - 1) / TILE, (H + TILE - 1) / TILE, B);
     { Prof pr(KK_TRANSPOSE, st); k_transpose<<<tgrid, 256, 0, st>>>(f, fT, H, W); }
@@ -2046,6 +2095,8 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p1.ne = L.ne;
         p1.edge_all = L.edge_all;
         p1.ntx = L.ntx;
+        p1.tile0 = 0;
+        p1.ntx_run = L.ntx;
         p1.k = kc;
         p1.t = td;
         p1.ngroups = (n + G1 - 1) / G1;
@@ -2054,14 +2105,37 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p1.lcarry = lc;
         p1.edge = edge;
         dim3 g1(L.ntx * (box ? 1 : L.nyc), (p1.ngroups + P1_WARPS - 1) / P1_WARPS, B);
-        {
+        const int p1smem = g_p1_occ == 2 ? P1_SMEM_OCC2 : P1_SMEM;
+        if (hpipe && bi == 0 && ev_strip.size() > 1) {
+            // strip s on alternating streams, after its copy; joined before the chain
+            for (size_t s = 0; s < ev_strip.size(); ++s) {
+                cudaStream_t ps = aux_stream(2 + (int)(s & 1));
+                cudaStreamWaitEvent(ps, e_ready, 0);
+                cudaStreamWaitEvent(ps, ev_strip[s], 0);
+                p1.tile0 = (int)s * tps;
+                p1.ntx_run = std::min(tps, L.ntx - p1.tile0);
+                dim3 gs(p1.ntx_run * L.nyc, g1.y, B);
+                {
+                    Prof pr(KK_PASS1, ps);
+                    if (fold)
+                        k_pass1_gauss<true><<<gs, P1_WARPS * 32, p1smem, ps>>>(p1);
+                    else
+                        k_pass1_gauss<false><<<gs, P1_WARPS * 32, p1smem, ps>>>(p1);
+                }
+                cudaEvent_t e = event_get();
+                cudaEventRecord(e, ps);
+                cudaStreamWaitEvent(st, e, 0);
+            }
+            p1.tile0 = 0;
+            p1.ntx_run = L.ntx;
+        } else {
             Prof pr(KK_PASS1, st);
             if (box)
                 k_pass1_box<G1, R_ANCHOR><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1, sp->radius);
             else if (fold)
-                k_pass1_gauss<true><<<g1, P1_WARPS * 32, g_p1_occ == 2 ? P1_SMEM_OCC2 : P1_SMEM, st>>>(p1);
+                k_pass1_gauss<true><<<g1, P1_WARPS * 32, p1smem, st>>>(p1);
             else
-                k_pass1_gauss<false><<<g1, P1_WARPS * 32, g_p1_occ == 2 ? P1_SMEM_OCC2 : P1_SMEM, st>>>(p1);
+                k_pass1_gauss<false><<<g1, P1_WARPS * 32, p1smem, st>>>(p1);
         }
         if ((rc = check_cuda("pass1"))) return rc;
         if (s2 != st) {  // hand the batch to the second stream
@@ -2157,24 +2231,6 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         }
         p2.tiles_per_chunk = (L.ntx + nchunk - 1) / nchunk;
         nchunk = (L.ntx + p2.tiles_per_chunk - 1) / p2.tiles_per_chunk;
-        dim3 g2(nrb * nchunk, p2.ngroups, B);
-        {
-            Prof pr(KK_PASS2, s2);
-            if (box)
-                k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, s2>>>(p2, sp->radius);
-            else if (p2var == 4)
-                k_pass2_async<4><<<g2, P2_THREADS, p2a_smem_bytes<4>(), s2>>>(p2);
-            else if (p2var == 5)
-                k_pass2_async<2><<<g2, P2_THREADS, p2a_smem_bytes<2>(), s2>>>(p2);
-            else if ((W % TILE) == 0 && p2var == 1)
-                k_pass2_tma<G2, 3><<<g2, P2T_THREADS, p2t_smem_bytes<G2>(), s2>>>(p2);
-            else if ((W % TILE) == 0 && p2var == 2)
-                k_pass2_tma<G2, 2><<<g2, P2T_THREADS, p2t_smem_bytes<G2>(), s2>>>(p2);
-            else
-                k_pass2_gauss<G2><<<g2, P2_THREADS, 0, s2>>>(p2);
-        }
-        if ((rc = check_cuda("pass2"))) return rc;
-
         ReduceArgs ra;
         ra.part = part;
         ra.ngroups = p2.ngroups;
@@ -2183,6 +2239,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         ra.W = W;
         ra.f = f;
         ra.counters = counters;
+        ra.i_base = 0;
         const bool add = bi > 0 || (accumulate && !out);
         ra.in_num = add ? num : nullptr;
         ra.in_den = add ? den : nullptr;
@@ -2196,18 +2253,75 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             ra.den = den;
             ra.out = nullptr;
         }
-        {
-            dim3 rgrid((W + TILE - 1) / TILE, (H + RED_I - 1) / RED_I, B);
-            Prof pr(KK_REDUCE, s2);
-            k_reduce<<<rgrid, 256, 0, s2>>>(ra);
+        // pass 2 + reduce over 128-row blocks [rb0, rb0 + nrb_run) on stream q
+        auto pass2_reduce = [&](int rb0, int nrun, cudaStream_t q) -> int {
+            p2.rb0 = rb0;
+            p2.nrb_run = nrun;
+            dim3 g2(nrun * nchunk, p2.ngroups, B);
+            {
+                Prof pr(KK_PASS2, q);
+                if (box)
+                    k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, q>>>(p2, sp->radius);
+                else if (p2var == 4)
+                    k_pass2_async<4><<<g2, P2_THREADS, p2a_smem_bytes<4>(), q>>>(p2);
+                else if (p2var == 5)
+                    k_pass2_async<2><<<g2, P2_THREADS, p2a_smem_bytes<2>(), q>>>(p2);
+                else if ((W % TILE) == 0 && p2var == 1)
+                    k_pass2_tma<G2, 3><<<g2, P2T_THREADS, p2t_smem_bytes<G2>(), q>>>(p2);
+                else if ((W % TILE) == 0 && p2var == 2)
+                    k_pass2_tma<G2, 2><<<g2, P2T_THREADS, p2t_smem_bytes<G2>(), q>>>(p2);
+                else
+                    k_pass2_gauss<G2><<<g2, P2_THREADS, 0, q>>>(p2);
+            }
+            int e;
+            if ((e = check_cuda("pass2"))) return e;
+            ra.i_base = rb0 * P2_THREADS;  // RED_I == P2_THREADS
+            {
+                const int rows = std::min(H - ra.i_base, nrun * P2_THREADS);
+                dim3 rgrid((W + TILE - 1) / TILE, (rows + RED_I - 1) / RED_I, B);
+                Prof pr(KK_REDUCE, q);
+                k_reduce<<<rgrid, 256, 0, q>>>(ra);
+            }
+            return check_cuda("reduce");
+        };
+        if (hpipe && last && hio->bands > 1 && nrb > 1) {
+            // row bands on alternating streams; each band's rows go back to the
+            // host while the next band filters
+            const int nbd = std::min(hio->bands, nrb);
+            const int rpb = (nrb + nbd - 1) / nbd;
+            cudaStream_t sd = aux_stream(4);
+            cudaEvent_t e_c = event_get();
+            cudaEventRecord(e_c, s2);  // chain and everything before it
+            for (int rb0 = 0, k = 0; rb0 < nrb; rb0 += rpb, ++k) {
+                cudaStream_t q = aux_stream(2 + (k & 1));
+                cudaStreamWaitEvent(q, e_c, 0);
+                if ((rc = pass2_reduce(rb0, std::min(rpb, nrb - rb0), q))) return rc;
+                cudaEvent_t e_r = event_get();
+                cudaEventRecord(e_r, q);
+                cudaStreamWaitEvent(sd, e_r, 0);
+                const int r0 = rb0 * P2_THREADS;
+                const int r1 = std::min(H, (rb0 + rpb) * P2_THREADS);
+                cudaMemcpy2DAsync(hio->h_out + (size_t)r0 * W, (size_t)H * W * 4, out + (size_t)r0 * W,
+                                  (size_t)H * W * 4, (size_t)(r1 - r0) * W * 4, B, cudaMemcpyDeviceToHost, sd);
+            }
+            cudaEvent_t e_d = event_get();
+            cudaEventRecord(e_d, sd);
+            cudaStreamWaitEvent(st, e_d, 0);  // join (sd waited on every band)
+            if ((rc = check_cuda("device to host"))) return rc;
+            hio = nullptr;  // output delivered
+        } else {
+            if ((rc = pass2_reduce(0, nrb, s2))) return rc;
         }
-        if ((rc = check_cuda("reduce"))) return rc;
         if (s2 != st) {
             ev_done[bi] = event_get();
             cudaEventRecord(ev_done[bi], s2);
         }
     }
     if (s2 != st) cudaStreamWaitEvent(st, ev_done[nb - 1], 0);  // join
+    if (hio && out) {  // host output not yet delivered (no banding)
+        cudaMemcpyAsync(hio->h_out, out, (size_t)B * H * W * 4, cudaMemcpyDeviceToHost, st);
+        if ((rc = check_cuda("device to host"))) return rc;
+    }
     return TBF_OK;
 }
 
@@ -2246,6 +2360,12 @@ int tbf_set_option(int32_t option, int64_t value) {
             return TBF_OK;
         case TBF_OPT_PASS2_TMA:
             g_pass2_tma = (int)std::max<int64_t>(0, std::min<int64_t>(5, value));
+            return TBF_OK;
+        case TBF_OPT_HOST_STRIPS:
+            g_host_strips = (int)std::max<int64_t>(1, std::min<int64_t>(64, value));
+            return TBF_OK;
+        case TBF_OPT_HOST_BANDS:
+            g_host_bands = (int)std::max<int64_t>(1, std::min<int64_t>(64, value));
             return TBF_OK;
         case TBF_OPT_P1_FOLD:
             g_pass1_fold = value != 0;
@@ -2318,6 +2438,20 @@ int tbf_bilateral_trig(const float* f, float* out, int32_t B, int32_t H, int32_t
     }
     return run_terms(f, nullptr, nullptr, out, B, H, W, sp, terms, 0, terms->n_terms, batch_terms,
                      0, workspace, workspace_bytes, d_counters, st);
+}
+
+int tbf_bilateral_trig_host(const float* h_f, float* h_out, int32_t B, int32_t H, int32_t W,
+                            const tbf_spatial* sp, const tbf_terms* terms, int32_t batch_terms,
+                            float* d_io, void* workspace, size_t workspace_bytes,
+                            unsigned long long* d_counters, void* stream) {
+    if (!terms) return fail(TBF_ERR_PARAM, "null terms");
+    if (!h_f || !h_out || !d_io) return fail(TBF_ERR_PARAM, "null host or device buffer");
+    if (B < 1 || H < 1 || W < 1) return fail(TBF_ERR_DIM, "bad shape B=%d H=%d W=%d", B, H, W);
+    HostIO hio{h_f, h_out, g_host_strips, g_host_bands};
+    float* d_f = d_io;
+    float* d_out = d_io + (size_t)B * H * W;
+    return run_terms(d_f, nullptr, nullptr, d_out, B, H, W, sp, terms, 0, terms->n_terms, batch_terms,
+                     0, workspace, workspace_bytes, d_counters, (cudaStream_t)stream, &hio);
 }
 
 int tbf_trig_partial(const float* f, float* num, float* den, int32_t B, int32_t H, int32_t W,

@@ -122,6 +122,7 @@ class TrigFilter:
         nbytes = self.workspace_bytes(self.batch_terms)
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.counters = torch.zeros(2, dtype=torch.int64, device=self.device)
+        self._io = None  # device input/output of run_host, allocated on first use
 
     # -- sizing -----------------------------------------------------------
     def workspace_bytes(self, batch_terms: int) -> int:
@@ -183,6 +184,28 @@ class TrigFilter:
         _native.check(rc)
         return out
 
+    def run_host(self, h_in, h_out):
+        """Host arrays in and out (NumPy arrays or CPU tensors, contiguous
+        float32 with B*H*W samples): tbf_bilateral_trig_host.  Column strips
+        of the input are copied while pass 1 starts on the first ones, and the
+        output returns in row bands (pinned memory overlaps the copies with the
+        filter; pageable memory works).  Stream-ordered: read_counters()
+        (which syncs) before using h_out; keep both arrays alive until then."""
+        torch = _torch()
+        if self.term_range != (0, self.terms.pairs.count):
+            raise ParameterError("plan covers a term shard; use partial() + finalize()")
+        n = self.B * self.H * self.W
+        p_in, p_out = _host_ptr(h_in, n, "input"), _host_ptr(h_out, n, "output")
+        if self._io is None:
+            self._io = torch.empty(2 * n, dtype=torch.float32, device=self.device)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        rc = self.lib.tbf_bilateral_trig_host(
+            p_in, p_out, self.B, self.H, self.W, ctypes.byref(self.sp),
+            ctypes.byref(self.terms.struct), self.batch_terms, self._io.data_ptr(),
+            self.workspace.data_ptr(), self.workspace.numel(), self.counters.data_ptr(), stream)
+        _native.check(rc)
+        return h_out
+
     def partial(self, f, num, den, accumulate: bool = False):
         """num/den (+)= contribution of this plan's term range (sharded path)."""
         torch = _torch()
@@ -219,6 +242,24 @@ class TrigFilter:
     @property
     def spatial_passes(self) -> int:
         return self.terms.pairs.spatial_passes
+
+
+def _host_ptr(a, n: int, what: str) -> int:
+    """Address of a contiguous float32 host array (NumPy or CPU tensor)."""
+    torch = _torch()
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float32 or not a.flags.c_contiguous:
+            raise ParameterError(f"host {what} must be a C-contiguous float32 array")
+        size, ptr = a.size, a.ctypes.data
+    elif isinstance(a, torch.Tensor):
+        if a.is_cuda or a.dtype != torch.float32 or not a.is_contiguous():
+            raise ParameterError(f"host {what} must be a contiguous float32 CPU tensor")
+        size, ptr = a.numel(), a.data_ptr()
+    else:
+        raise DimensionError(f"unsupported host {what} type {type(a).__name__}")
+    if size != n:
+        raise DimensionError(f"host {what} has {size} samples, plan expects {n}")
+    return ptr
 
 
 _PLANS: dict = {}
@@ -297,59 +338,61 @@ def bilateral_trig(img, spatial, kernel, *, workers: int = 1,
     kernel = _check_kernel(kernel)
     spatial = _check_spatial(spatial)
     _require_cuda()
-    kind = "image"
+    if diagnostics is not None:
+        diagnostics.degree = kernel.N
+        diagnostics.workers = workers
+
+    def _finish(plan, shape, lo_hi):
+        bad, guarded = plan.read_counters()  # syncs: results and counters are ready
+        if bad:
+            lo, hi = lo_hi()
+            raise ParameterError(
+                f"samples in [{lo:g}, {hi:g}] exceed the declared range [0, {kernel.T:g}]; "
+                "rescale the input or raise T"
+            )
+        if diagnostics is not None:
+            diagnostics.spatial_passes += plan.spatial_passes * shape[0]
+            diagnostics.guarded_pixels += guarded
+
     if isinstance(img, Image):
         if img.channels != 1:
             raise DimensionError(f"engine expects a single-channel image, got {img.channels} channels")
         host = np.ascontiguousarray(img.samples[0], dtype=np.float32)
-        f = torch.from_numpy(host).cuda()
         shape = (1, img.height, img.width)
-    else:
-        if isinstance(img, np.ndarray):
-            kind = "numpy"
-            t = torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32))
-        elif isinstance(img, torch.Tensor):
-            kind = "cuda" if img.is_cuda else "cpu"
-            t = img
-        else:
-            raise DimensionError(f"unsupported input type {type(img).__name__}")
-        if t.dim() not in (2, 3):
-            raise DimensionError(f"expected [H, W] or [B, H, W], got shape {tuple(t.shape)}")
-        shape = (1, *t.shape) if t.dim() == 2 else tuple(t.shape)
-        if kind == "cpu" and shape[0] >= 4 and t.is_pinned() and t.dtype == torch.float32:
-            _require_cuda()
-            if diagnostics is not None:
-                diagnostics.degree = kernel.N
-                diagnostics.workers = workers
-            return _bilateral_trig_streamed(t, spatial, kernel, diagnostics)
-        f = t.to(device="cuda" if not t.is_cuda else t.device, dtype=torch.float32,
-                 non_blocking=bool(not t.is_cuda and t.is_pinned())).contiguous()
-    if diagnostics is not None:
-        diagnostics.degree = kernel.N
-        diagnostics.workers = workers
-    plan = get_plan(shape, spatial, kernel, device=f.device)
-    out = plan(f)
-    bad, guarded = plan.read_counters()
-    if bad:
-        lo = float(f.min())
-        hi = float(f.max())
-        raise ParameterError(
-            f"samples in [{lo:g}, {hi:g}] exceed the declared range [0, {kernel.T:g}]; "
-            "rescale the input or raise T"
-        )
-    if diagnostics is not None:
-        diagnostics.spatial_passes += plan.spatial_passes * shape[0]
-        diagnostics.guarded_pixels += guarded
-    if kind == "image":
-        res = out.reshape(img.height, img.width).cpu().numpy().astype(np.float64)
-        return Image(img.width, img.height, 1, res)
-    if kind == "cuda":
+        plan = get_plan(shape, spatial, kernel)
+        res = plan.run_host(host, np.empty_like(host))
+        _finish(plan, shape, lambda: (float(host.min()), float(host.max())))
+        return Image(img.width, img.height, 1, res.astype(np.float64))
+    if isinstance(img, np.ndarray):
+        host = np.ascontiguousarray(img, dtype=np.float32)
+        if host.ndim not in (2, 3):
+            raise DimensionError(f"expected [H, W] or [B, H, W], got shape {host.shape}")
+        shape = (1, *host.shape) if host.ndim == 2 else host.shape
+        plan = get_plan(shape, spatial, kernel)
+        res = plan.run_host(host, np.empty_like(host))
+        _finish(plan, shape, lambda: (float(host.min()), float(host.max())))
+        return res
+    if not isinstance(img, torch.Tensor):
+        raise DimensionError(f"unsupported input type {type(img).__name__}")
+    if img.dim() not in (2, 3):
+        raise DimensionError(f"expected [H, W] or [B, H, W], got shape {tuple(img.shape)}")
+    shape = (1, *img.shape) if img.dim() == 2 else tuple(img.shape)
+    if img.is_cuda:  # device in, device out, no copies
+        f = img.to(dtype=torch.float32).contiguous()
+        plan = get_plan(shape, spatial, kernel, device=f.device)
+        out = plan(f)
+        _finish(plan, shape, lambda: (float(f.min()), float(f.max())))
         return out.reshape(img.shape)
-    # device -> host into pinned memory when the caller's buffer was pinned
-    res = torch.empty(tuple(t.shape), dtype=torch.float32,
-                      pin_memory=(kind == "cpu" and t.is_pinned()))
-    res.copy_(out.reshape(t.shape))
-    return res.numpy() if kind == "numpy" else res
+    pinned = img.is_pinned()
+    if shape[0] >= 4 and pinned and img.dtype == torch.float32:
+        # frame batches: sub-batches overlap copies and filtering across frames
+        return _bilateral_trig_streamed(img, spatial, kernel, diagnostics)
+    host = img.to(dtype=torch.float32).contiguous()
+    res = torch.empty(tuple(img.shape), dtype=torch.float32, pin_memory=pinned)
+    plan = get_plan(shape, spatial, kernel)
+    plan.run_host(host, res)
+    _finish(plan, shape, lambda: (float(host.min()), float(host.max())))
+    return res
 
 
 def _bilateral_trig_streamed(t, spatial, kernel, diagnostics, sub: int | None = None):

@@ -365,3 +365,55 @@ def test_pinned_host_batch_streamed_matches_device(tb):
     assert not host.is_cuda and host.shape == pinned.shape
     assert np.max(np.abs(host.numpy() - dev)) < 1e-3
     assert diag.spatial_passes == 9 * (2 * (k.N + 1) - (1 if k.N % 2 == 0 else 0))
+
+
+@pytest.mark.parametrize("shape,strips,bands", [
+    ((1, 512, 768), 4, 4),     # y-chunked pass 1, 4 strips, 4 bands
+    ((1, 300, 1000), 3, 2),    # ragged last tile and last row block
+    ((2, 200, 130), 4, 4),     # two frames, strips of 2 tiles, more bands than row blocks
+    ((1, 2048, 2048), 4, 4),   # the config-2 shape
+])
+def test_host_entry_matches_device(tb, shape, strips, bands):
+    """tbf_bilateral_trig_host (strip-wise copies + pass 1, band-wise pass 2 +
+    copies back) computes exactly what the device-resident call computes:
+    the same kernels over the same columns / rows, only split across launches."""
+    from paper_1105_4204_b200 import _native
+    from paper_1105_4204_b200.workloads import smooth_image
+
+    lib = _native.load()
+    B, H, W = shape
+    fs = np.stack([smooth_image(H, W, 12, seed=7 + s) for s in range(B)]).astype(np.float32)
+    k = tb.make_trig_kernel(20.0)
+    spec = tb.SpatialSpec.gaussian_recursive(8.0)
+    plan = tb.TrigFilter(shape, spec, k)
+    dev = plan(torch.from_numpy(fs).cuda()).cpu().numpy()
+    try:
+        lib.tbf_set_option(_native.TBF_OPT_HOST_STRIPS, strips)
+        lib.tbf_set_option(_native.TBF_OPT_HOST_BANDS, bands)
+        pin_in = torch.from_numpy(fs).pin_memory()
+        pin_out = torch.empty_like(pin_in).pin_memory()
+        plan.run_host(pin_in, pin_out)
+        assert plan.read_counters() == (0, 0)
+        np.testing.assert_array_equal(pin_out.numpy(), dev)
+        page_out = np.empty_like(fs)
+        plan.run_host(fs, page_out)  # pageable host memory
+        plan.read_counters()
+        np.testing.assert_array_equal(page_out, dev)
+    finally:
+        lib.tbf_set_option(_native.TBF_OPT_HOST_STRIPS, 4)
+        lib.tbf_set_option(_native.TBF_OPT_HOST_BANDS, 4)
+
+
+def test_host_entry_range_error(tb):
+    """Out-of-range samples through the host entry raise ParameterError
+    (engines.py:218-225), for NumPy and pinned inputs."""
+    f = np.full((64, 96), 100.0, dtype=np.float32)
+    f[10, 20] = 300.0
+    k = tb.make_trig_kernel(20.0)
+    spec = tb.SpatialSpec.gaussian_recursive(3.0)
+    with pytest.raises(tb.ParameterError):
+        tb.bilateral_trig(f, spec, k)
+    with pytest.raises(tb.ParameterError):
+        tb.bilateral_trig(torch.from_numpy(f).pin_memory(), spec, k)
+    ok = tb.bilateral_trig(np.clip(f, 0, 255), spec, k)  # the plan's counters were reset
+    assert ok.shape == f.shape and np.isfinite(ok).all()
