@@ -158,11 +158,12 @@ TBF_API int tbf_profile_collect(double* ms, long long* launches, int32_t n);
 #define TBF_OPT_P1_YCHUNKS 5 /* default 0 = automatic row chunks per pass-1 column */
 #define TBF_OPT_PASS2_TMA 2 /* pass-2 variant: 0 register prefetch (2 terms/thread), 1|2 TMA bulk
                                copies + mbarriers with a producer warp (3|2 blocks/SM, W % 32 == 0),
-                               3 (default) automatic: 4 when rows x term groups fill a wave, else 0,
+                               3 (default) automatic (currently 6),
                                4 per-thread cp.async staging, 4 terms/thread,
-                               5 per-thread cp.async staging, 2 terms/thread */
-#define TBF_OPT_HOST_STRIPS 7 /* default 4: column strips of tbf_bilateral_trig_host's input copy */
-#define TBF_OPT_HOST_BANDS 8  /* default 4: row bands of tbf_bilateral_trig_host's output copy */
+                               5 per-thread cp.async staging, 2 terms/thread,
+                               6 register prefetch with 4 groups summed per block (4x fewer partials) */
+#define TBF_OPT_HOST_STRIPS 7 /* column strips of tbf_bilateral_trig_host's input copy (0 = auto) */
+#define TBF_OPT_HOST_BANDS 8  /* row bands of tbf_bilateral_trig_host's output copy (0 = auto) */
 #define TBF_OPT_P1_FOLD 6   /* default 1: folds the y-sweep gain into the pass-2 weights
                                (skips 4 multiplies per pixel-term in pass 1 when T/g^4 is safe); 0 scales in pass 1 */
 TBF_API int tbf_set_option(int32_t option, int64_t value);

@@ -819,12 +819,12 @@ __device__ __forceinline__ void p2_load4(const P2Ctx<G>& c, int x0, int mb, floa
     }
 }
 
-template <int G, bool OUT>
+template <int G, bool OUT, bool SM = false>
 __device__ __forceinline__ void p2_step4(const Pass2Args& a, const P2Ctx<G>& c, int x0, int mb,
                                          bool full, const float4 (&fo)[4][G], const float (&fv)[4],
                                          const float (&C)[G][4][4], float (&p1)[G][4],
                                          float (&p2)[G][4], float (&q1)[G][4], float (&q2)[G][4],
-                                         float* pn, float* pd, bool iv) {
+                                         float* pn, float* pd, bool iv, float2* sb = nullptr) {
     const Casc k = a.k;
     float cs[4][G], sn[4][G];
     if (OUT) {
@@ -857,7 +857,9 @@ __device__ __forceinline__ void p2_step4(const Pass2Args& a, const P2Ctx<G>& c, 
                     den = fmaf(c.wt[g], fmaf(cs[q][g], y[0], sn[q][g] * y[1]), den);
                 }
             }
-            if (OUT && iv) {
+            if (OUT && SM) {
+                sb[m * 32] = make_float2(num, den);  // block-level group sum follows
+            } else if (OUT && iv) {
                 const size_t off = (size_t)(x0 + m) * FL_RB;
                 pn[off] = num;
                 pd[off] = den;
@@ -866,10 +868,11 @@ __device__ __forceinline__ void p2_step4(const Pass2Args& a, const P2Ctx<G>& c, 
     }
 }
 
-template <int G, bool OUT>
+template <int G, bool OUT, bool SM = false>
 __device__ __forceinline__ void p2_tile(const Pass2Args& a, const P2Ctx<G>& c, int t,
                                         float (&p1)[G][4], float (&p2)[G][4], float (&q1)[G][4],
-                                        float (&q2)[G][4], float* pn, float* pd, bool iv) {
+                                        float (&q2)[G][4], float* pn, float* pd, bool iv,
+                                        float2* sb = nullptr) {
     const int x0 = t * TILE;
     const int len = min(TILE, a.W - x0);
     float C[G][4][4];
@@ -892,15 +895,15 @@ __device__ __forceinline__ void p2_tile(const Pass2Args& a, const P2Ctx<G>& c, i
 #pragma unroll 1
         for (int mb = TILE - 1; mb >= 7; mb -= 8) {
             p2_load4<G, OUT>(c, x0, mb - 4, fb, vb);
-            p2_step4<G, OUT>(a, c, x0, mb, true, fa, va, C, p1, p2, q1, q2, pn, pd, iv);
+            p2_step4<G, OUT, SM>(a, c, x0, mb, true, fa, va, C, p1, p2, q1, q2, pn, pd, iv, sb);
             p2_load4<G, OUT>(c, x0, mb - 8, fa, va);  // clamped at x0 on the last iteration
-            p2_step4<G, OUT>(a, c, x0, mb - 4, true, fb, vb, C, p1, p2, q1, q2, pn, pd, iv);
+            p2_step4<G, OUT, SM>(a, c, x0, mb - 4, true, fb, vb, C, p1, p2, q1, q2, pn, pd, iv, sb);
         }
     } else {
 #pragma unroll 1
         for (int mb = len - 1; mb >= 0; mb -= 4) {
             p2_load4<G, OUT>(c, x0, mb, fa, va);
-            p2_step4<G, OUT>(a, c, x0, mb, false, fa, va, C, p1, p2, q1, q2, pn, pd, iv);
+            p2_step4<G, OUT, SM>(a, c, x0, mb, false, fa, va, C, p1, p2, q1, q2, pn, pd, iv, sb);
         }
     }
 }
@@ -1392,6 +1395,117 @@ __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_gauss(const __grid_cons
     for (int t = t_hi - 1; t >= t_lo; --t) p2_tile<G, true>(a, c, t, p1, p2, q1, q2, pn, pd, iv);
 }
 
+// Pass 2 with the term groups of a block summed on chip: 4 warps = 32 rows x
+// 4 groups of G terms (warp w = group 4*blockIdx.y + w).  Each warp stages
+// its tile's (num, den) in shared memory; after a barrier the block adds the
+// 4 groups in fixed order (deterministic) and writes one partial pair, so
+// partial traffic (pass-2 writes + reduce reads) drops 4x.
+constexpr int P2R_GR = 4;
+
+template <int G>
+__global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_constant__ Pass2Args a) {
+    __shared__ float2 sbuf[P2R_GR][TILE][32];  // [warp][x in tile][row]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nsb = a.nrb_run * (P2_THREADS / 32);  // 32-row sub-blocks in this launch
+    const int chunk = blockIdx.x / nsb;
+    const int r0 = a.rb0 * P2_THREADS + (blockIdx.x % nsb) * 32;
+    const int H = a.H, W = a.W;
+    if (r0 >= H) return;  // whole block
+    const int i_raw = r0 + lane;
+    const bool iv = i_raw < H;
+    const int i = iv ? i_raw : H - 1;
+    const int grp_raw = blockIdx.y * P2R_GR + w;
+    const bool active = grp_raw < a.ngroups;
+    const int grp = active ? grp_raw : a.ngroups - 1;
+    const int b = blockIdx.z;
+    const int j0 = grp * G;
+    const int nt = min(G, a.t.n - j0);
+    P2Ctx<G> c;
+    c.H = (size_t)H;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const int j = min(j0 + g, a.t.n - 1);
+        c.nu_hi[g] = a.t.nu_hi[j];
+        c.nu_lo[g] = a.t.nu_lo[j];
+        c.wt[g] = g < nt ? a.t.w[j] * a.wscale : 0.f;
+        c.fl[g] = reinterpret_cast<const float4*>(a.floc) +
+                  (((size_t)j * a.B + b) * ((H + FL_RB - 1) / FL_RB) + i / FL_RB) * W * (size_t)FL_RB + (i % FL_RB);
+        c.cr[g] = reinterpret_cast<const float4*>(a.carry) + (((size_t)j * a.B + b) * a.ntx * H + i) * 4;
+    }
+    c.fT = a.fT + xm_index(b, 0, i, W, H);
+    const size_t xpl = xm_plane(a.B, W, H);
+    float* pn = a.part + (size_t)(blockIdx.y * 2 + 0) * xpl + xm_index(b, 0, iv ? i_raw : 0, W, H);
+    float* pd = a.part + (size_t)(blockIdx.y * 2 + 1) * xpl + xm_index(b, 0, iv ? i_raw : 0, W, H);
+    float2* const sb = &sbuf[w][0][lane];
+
+    const int t_lo = chunk * a.tiles_per_chunk;
+    const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
+    float p1[G][4], p2[G][4], q1[G][4], q2[G][4];
+    if (active) {
+        const bool exact_start = t_hi + a.warm_tiles >= a.ntx;
+        if (exact_start) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int j = min(j0 + g, a.t.n - 1);
+                const float4* bs = reinterpret_cast<const float4*>(a.bstate) + (((size_t)j * a.B + b) * H + i) * 4;
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const float4 v = bs[p];
+                    p1[g][p] = v.x;
+                    p2[g][p] = v.y;
+                    q1[g][p] = v.z;
+                    q2[g][p] = v.w;
+                }
+            }
+#pragma unroll 1
+            for (int t = a.ntx - 1; t >= t_hi; --t) p2_tile<G, false>(a, c, t, p1, p2, q1, q2, pn, pd, iv);
+        } else {
+            const int tw = min(a.ntx - 1, t_hi - 1 + a.warm_tiles);
+            const int xs = min(W - 1, tw * TILE + TILE - 1);
+            const int ms = xs - tw * TILE;
+            const float4 h = *reinterpret_cast<const float4*>(&a.Hm[ms][0]);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float4 F = c.fl[g][(size_t)xs * FL_RB];
+                const float fin[4] = {F.x, F.y, F.z, F.w};
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const float4 cv = c.cr[g][(size_t)tw * c.H * 4 + p];
+                    const float v = fmaf(h.x, cv.x, fmaf(h.y, cv.y, fmaf(h.z, cv.z, fmaf(h.w, cv.w, fin[p]))));
+                    csteady(v, p1[g][p], p2[g][p], q1[g][p], q2[g][p], a.k);
+                }
+            }
+#pragma unroll 1
+            for (int t = tw; t >= t_hi; --t) p2_tile<G, false>(a, c, t, p1, p2, q1, q2, pn, pd, iv);
+        }
+    } else {
+#pragma unroll
+        for (int m = 0; m < TILE; ++m) sb[m * 32] = make_float2(0.f, 0.f);
+    }
+#pragma unroll 1
+    for (int t = t_hi - 1; t >= t_lo; --t) {
+        if (active) p2_tile<G, true, true>(a, c, t, p1, p2, q1, q2, pn, pd, iv, sb);
+        __syncthreads();
+        const int x0 = t * TILE;
+        const int len = min(TILE, W - x0);
+        if (iv) {
+            for (int m = w; m < len; m += P2R_GR) {
+                float2 acc = sbuf[0][m][lane];
+#pragma unroll
+                for (int q = 1; q < P2R_GR; ++q) {
+                    const float2 v = sbuf[q][m][lane];
+                    acc.x += v.x;
+                    acc.y += v.y;
+                }
+                const size_t off = (size_t)(x0 + m) * FL_RB;
+                pn[off] = acc.x;
+                pd[off] = acc.y;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Box variant (spatial.py:157-160, box_pass _core.pyx:28-53).  Pass 1 runs the
 // normalised (2r+1) window along y as a running sum per column (fp64 sums;
@@ -1769,8 +1883,8 @@ int g_p2_chunks = 0;    // tbf_set_option(TBF_OPT_P2_CHUNKS): 0 = automatic
 int g_pass2_tma = 3;    // tbf_set_option(TBF_OPT_PASS2_TMA): 0 register prefetch (G=2), 1/2 TMA producer warp, 3 auto (default), 4 cp.async G=4
 int g_pipeline = 0;     // tbf_set_option(TBF_OPT_PIPELINE) (measured: no gain on B200, SMs time-slice)
 int g_auto_batches = 2; // tbf_set_option(TBF_OPT_BATCHES): batches when batch_terms <= 0
-int g_host_strips = 4;  // tbf_set_option(TBF_OPT_HOST_STRIPS): column strips of the host input
-int g_host_bands = 4;   // tbf_set_option(TBF_OPT_HOST_BANDS): row bands of the host output
+int g_host_strips = 0;  // tbf_set_option(TBF_OPT_HOST_STRIPS): column strips of the host input (0 auto)
+int g_host_bands = 0;   // tbf_set_option(TBF_OPT_HOST_BANDS): row bands of the host output (0 auto)
 
 int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, int batch_terms,
                 Layout* L) {
@@ -2177,14 +2291,12 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.ntx = L.ntx;
         p2.k = kc;
         p2.t = td;
-        // pass-2 variant: cp.async with 4 terms/thread when rows x term groups
-        // fill >= 1 wave (configs 3-5), else register prefetch with 2 (1-2)
+        // pass-2 variant: automatic = the block-summed register variant (6),
+        // measured fastest on configs 1-4 against the per-group register (0)
+        // and cp.async G=4 (4) variants
         int p2var = g_pass2_tma;
-        if (!box && p2var == 3) {
-            const long long thr4 = (long long)((H + P2_THREADS - 1) / P2_THREADS) * P2_THREADS *
-                                   ((n + 3) / 4) * B;
-            p2var = thr4 >= 148LL * 12 * 32 / 2 ? 4 : 0;
-        }
+        if (!box && p2var == 3) p2var = 6;
+        const int npart = (!box && p2var == 6) ? (((n + G2 - 1) / G2 + P2R_GR - 1) / P2R_GR) : -1;
         const int g2run = (!box && p2var == 4) ? 4 : G2;  // terms per pass-2 thread this launch
         // (p2var 5: cp.async staging with 2 terms/thread)
         p2.ngroups = (n + g2run - 1) / g2run;
@@ -2233,7 +2345,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         nchunk = (L.ntx + p2.tiles_per_chunk - 1) / p2.tiles_per_chunk;
         ReduceArgs ra;
         ra.part = part;
-        ra.ngroups = p2.ngroups;
+        ra.ngroups = npart > 0 ? npart : p2.ngroups;
         ra.B = B;
         ra.H = H;
         ra.W = W;
@@ -2262,6 +2374,8 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 Prof pr(KK_PASS2, q);
                 if (box)
                     k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, q>>>(p2, sp->radius);
+                else if (p2var == 6)
+                    k_pass2_gr<G2><<<dim3(nrun * (P2_THREADS / 32) * nchunk, npart, B), 32 * P2R_GR, 0, q>>>(p2);
                 else if (p2var == 4)
                     k_pass2_async<4><<<g2, P2_THREADS, p2a_smem_bytes<4>(), q>>>(p2);
                 else if (p2var == 5)
@@ -2359,13 +2473,13 @@ int tbf_set_option(int32_t option, int64_t value) {
             g_p2_chunks = (int)std::max<int64_t>(0, value);
             return TBF_OK;
         case TBF_OPT_PASS2_TMA:
-            g_pass2_tma = (int)std::max<int64_t>(0, std::min<int64_t>(5, value));
+            g_pass2_tma = (int)std::max<int64_t>(0, std::min<int64_t>(6, value));
             return TBF_OK;
         case TBF_OPT_HOST_STRIPS:
-            g_host_strips = (int)std::max<int64_t>(1, std::min<int64_t>(64, value));
+            g_host_strips = (int)std::max<int64_t>(0, std::min<int64_t>(64, value));
             return TBF_OK;
         case TBF_OPT_HOST_BANDS:
-            g_host_bands = (int)std::max<int64_t>(1, std::min<int64_t>(64, value));
+            g_host_bands = (int)std::max<int64_t>(0, std::min<int64_t>(64, value));
             return TBF_OK;
         case TBF_OPT_P1_FOLD:
             g_pass1_fold = value != 0;
@@ -2447,7 +2561,12 @@ int tbf_bilateral_trig_host(const float* h_f, float* h_out, int32_t B, int32_t H
     if (!terms) return fail(TBF_ERR_PARAM, "null terms");
     if (!h_f || !h_out || !d_io) return fail(TBF_ERR_PARAM, "null host or device buffer");
     if (B < 1 || H < 1 || W < 1) return fail(TBF_ERR_DIM, "bad shape B=%d H=%d W=%d", B, H, W);
-    HostIO hio{h_f, h_out, g_host_strips, g_host_bands};
+    // automatic split (measured on configs 1-2): one strip per 16 column tiles
+    // (2..8); 4 output bands once there are >= 8 row blocks of 128, else one
+    const int ntx = (W + TILE - 1) / TILE, nrb = (H + P2_THREADS - 1) / P2_THREADS;
+    const int strips = g_host_strips > 0 ? g_host_strips : std::max(2, std::min(8, ntx / 16));
+    const int bands = g_host_bands > 0 ? g_host_bands : (nrb >= 8 ? 4 : 1);
+    HostIO hio{h_f, h_out, strips, bands};
     float* d_f = d_io;
     float* d_out = d_io + (size_t)B * H * W;
     return run_terms(d_f, nullptr, nullptr, d_out, B, H, W, sp, terms, 0, terms->n_terms, batch_terms,

@@ -1,0 +1,27 @@
+"""Time tbf_bilateral_trig_host over strip/band counts (development aid)."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_1105_4204_b200 as tb
+from paper_1105_4204_b200 import _native, workloads
+
+cfg = workloads.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
+host = workloads.make_input(cfg, frames=1)
+pin = torch.from_numpy(host).pin_memory()
+out = torch.empty_like(pin).pin_memory()
+k = tb.make_trig_kernel(cfg.sigma_r, cfg.T)
+spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
+plan = tb.get_plan(tuple(pin.shape), spec, k)
+lib = _native.load()
+for strips in (1, 2, 4, 8, 16):
+    for bands in (1, 4, 8, 16):
+        lib.tbf_set_option(_native.TBF_OPT_HOST_STRIPS, strips)
+        lib.tbf_set_option(_native.TBF_OPT_HOST_BANDS, bands)
+        ts = []
+        for i in range(13):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            plan.run_host(pin, out)
+            plan.read_counters()
+            ts.append(time.perf_counter() - t)
+        print(f"{cfg.name} strips {strips:2d} bands {bands:2d}  median {1e3*np.median(ts[3:]):.3f} ms  min {1e3*min(ts[3:]):.3f}", flush=True)

@@ -400,8 +400,8 @@ def test_host_entry_matches_device(tb, shape, strips, bands):
         plan.read_counters()
         np.testing.assert_array_equal(page_out, dev)
     finally:
-        lib.tbf_set_option(_native.TBF_OPT_HOST_STRIPS, 4)
-        lib.tbf_set_option(_native.TBF_OPT_HOST_BANDS, 4)
+        lib.tbf_set_option(_native.TBF_OPT_HOST_STRIPS, 0)
+        lib.tbf_set_option(_native.TBF_OPT_HOST_BANDS, 0)
 
 
 def test_host_entry_range_error(tb):
