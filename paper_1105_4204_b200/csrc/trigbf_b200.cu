@@ -351,7 +351,8 @@ struct ChainArgs {
     int n;                // terms in the batch
     const float* edge;    // float4 [n][B][ne][H]
     float* lcarry;        // in: local carries, out: chained carries (state at tile start)
-    float* extbuf;        // float4 [n][B][Ex][H]
+    float Rx[16];         // right extension: bstate = Rx . s(W) + sum_e bx[e] Y(W-2-e)
+    const float4* bx;     // [Ex] (see right_ext_coeffs)
     float* bstate;        // float4 [n][B][H][4 planes] backward start state
 };
 
@@ -759,32 +760,39 @@ __global__ void __launch_bounds__(128) k_chain(const __grid_constant__ ChainArgs
             }
         }
     }
-    // right extension: forward over x = W .. W-1+Ex (input Y(2(W-1)-x)) into
-    // scratch, then backward over it -> backward start state at x = W-1
-    float last[4] = {y1[0], y1[1], y1[2], y1[3]};
-    float4* ext = reinterpret_cast<float4*>(a.extbuf) + (size_t)bt * Ex * H + i;
-    for (int eb = 0; eb < Ex; eb += 8) {
-        float4 u[8];
+    // right extension (forward over x = W .. W-1+Ex on Y(2(W-1)-x), steady
+    // start from its last output, backward back to x = W-1) in closed form:
+    // the map is linear in the state at x = W and the Ex mirrored inputs
+    float p1[4], p2[4], q1[4], q2[4];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) u[q] = ed[(size_t)eidx(max(0, W - 2 - min(eb + q, Ex - 1))) * H];
+    for (int p = 0; p < 4; ++p) {
+        const float s0 = v1[p], s1 = v2[p], s2 = y1[p], s3 = y2[p];
+        p1[p] = fmaf(a.Rx[0], s0, fmaf(a.Rx[4], s1, fmaf(a.Rx[8], s2, a.Rx[12] * s3)));
+        p2[p] = fmaf(a.Rx[1], s0, fmaf(a.Rx[5], s1, fmaf(a.Rx[9], s2, a.Rx[13] * s3)));
+        q1[p] = fmaf(a.Rx[2], s0, fmaf(a.Rx[6], s1, fmaf(a.Rx[10], s2, a.Rx[14] * s3)));
+        q2[p] = fmaf(a.Rx[3], s0, fmaf(a.Rx[7], s1, fmaf(a.Rx[11], s2, a.Rx[15] * s3)));
+    }
+    for (int eb = 0; eb < Ex; eb += 8) {
+        float4 u[8], c[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = min(eb + q, Ex - 1);
+            u[q] = ed[(size_t)eidx(max(0, W - 2 - e)) * H];
+            c[q] = __ldg(a.bx + e);
+        }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             if (eb + q < Ex) {
-                cstep4(u[q], v1, v2, y1, y2, k, last);
-                ext[(size_t)(eb + q) * H] = f4(last[0], last[1], last[2], last[3]);
+                const float uv[4] = {u[q].x, u[q].y, u[q].z, u[q].w};
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    p1[p] = fmaf(c[q].x, uv[p], p1[p]);
+                    p2[p] = fmaf(c[q].y, uv[p], p2[p]);
+                    q1[p] = fmaf(c[q].z, uv[p], q1[p]);
+                    q2[p] = fmaf(c[q].w, uv[p], q2[p]);
+                }
             }
         }
-    }
-    float p1[4], p2[4], q1[4], q2[4];
-#pragma unroll
-    for (int p = 0; p < 4; ++p) csteady(last[p], p1[p], p2[p], q1[p], q2[p], k);
-    for (int eb = Ex - 1; eb >= 0; eb -= 8) {
-        float4 u[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) u[q] = ext[(size_t)max(eb - q, 0) * H];
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-            if (eb - q >= 0) cstep4(u[q], p1, p2, q1, q2, k, o);
     }
     float4* bs = reinterpret_cast<float4*>(a.bstate) + ((size_t)bt * H + i) * 4;
 #pragma unroll
@@ -1858,6 +1866,9 @@ constexpr int G1 = 1;  // terms per pass-1 warp == phasor anchor block R
 constexpr int G2 = 2;  // terms per pass-2 thread (multiple of G1)
 constexpr int R_ANCHOR = G1;
 constexpr int TAB_PAD = 16;  // zero padding past the last term of the table
+// term table [nu_hi | nu_lo | w] (ld = n + TAB_PAD each), then the float4
+// right-extension coefficients bx at a 16-byte aligned offset (in floats)
+inline size_t tab_bx_offset(int nterms) { return ((size_t)3 * (nterms + TAB_PAD) + 3) / 4 * 4; }
 
 size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
@@ -1947,7 +1958,7 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     L->off_den = o;
     if (multi) o = align_up(o + px * 4);
     L->off_tab = o;
-    o = align_up(o + (size_t)3 * (nterms_range + TAB_PAD) * 4);
+    o = align_up(o + (tab_bx_offset(nterms_range) + (size_t)4 * L->Ex) * 4);
     // one slot
     size_t q = 0;
     L->s_ckpt = q;
@@ -1958,8 +1969,7 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     if (!box) q = align_up(q + (size_t)tb * 16 * B * L->ntx * H * 4);
     L->s_edge = q;
     if (!box) q = align_up(q + (size_t)tb * 4 * B * L->ne * H * 4);
-    L->s_ext = q;
-    if (!box) q = align_up(q + (size_t)tb * 4 * B * L->Ex * H * 4);
+    L->s_ext = q;  // (unused: the right x-extension is in closed form)
     L->s_bst = q;
     if (!box) q = align_up(q + (size_t)tb * 16 * B * H * 4);
     L->s_part = q;
@@ -2022,6 +2032,61 @@ void cascade_responses(const tbf_spatial* sp, int steps, double M[16], double (*
         M[kk * 4 + 2] = y1;
         M[kk * 4 + 3] = y2;
     }
+}
+
+// Closed form of the chain's right x-extension (spatial.py:171 mirror pad,
+// _core.pyx:75-92): forward over Ex mirrored samples from the state s at
+// x = W, steady start from the last output, backward over the Ex outputs.
+// Linear in (s, inputs): bstate = Rx . s + sum_e bx[e] * Y(W-2-e), per plane.
+// Evaluated in double with the kernels' pure-cascade steps; cached.
+void right_ext_coeffs(const tbf_spatial* sp, int Ex, double Rx[16], std::vector<float>& bx) {
+    static std::mutex mu;
+    static double key[7] = {0, 0, 0, 0, 0, 0, -1};
+    static double cR[16];
+    static std::vector<float> cb;
+    std::lock_guard<std::mutex> g(mu);
+    const double kk[7] = {sp->a1, sp->a2, sp->b1, sp->b2, sp->g1, sp->g2, (double)Ex};
+    if (std::equal(kk, kk + 7, key)) {
+        std::copy(cR, cR + 16, Rx);
+        bx = cb;
+        return;
+    }
+    const double ig1 = 1.0 / sp->g1, ig = 1.0 / (sp->g1 * sp->g2);
+    std::vector<double> outs(std::max(Ex, 1));
+    bx.assign((size_t)Ex * 4, 0.f);
+    for (int k = 0; k < 4 + Ex; ++k) {
+        double v1 = k == 0, v2 = k == 1, y1 = k == 2, y2 = k == 3;
+        double last = y1;
+        for (int e = 0; e < Ex; ++e) {
+            const double u = (k >= 4 && e == k - 4) ? 1.0 : 0.0;
+            const double v = u + sp->a1 * v1 + sp->a2 * v2;
+            v2 = v1;
+            v1 = v;
+            const double y = v + sp->b1 * y1 + sp->b2 * y2;
+            y2 = y1;
+            y1 = y;
+            outs[e] = last = y;
+        }
+        double p1 = last * ig1, p2 = p1, q1 = last * ig, q2 = q1;
+        for (int e = Ex - 1; e >= 0; --e) {
+            const double v = outs[e] + sp->a1 * p1 + sp->a2 * p2;
+            p2 = p1;
+            p1 = v;
+            const double y = v + sp->b1 * q1 + sp->b2 * q2;
+            q2 = q1;
+            q1 = y;
+        }
+        const double r[4] = {p1, p2, q1, q2};
+        for (int c = 0; c < 4; ++c) {
+            if (k < 4)
+                Rx[k * 4 + c] = r[c];
+            else
+                bx[(size_t)(k - 4) * 4 + c] = (float)r[c];
+        }
+    }
+    std::copy(kk, kk + 7, key);
+    std::copy(Rx, Rx + 16, cR);
+    cb = bx;
 }
 
 Casc to_casc(const tbf_spatial* sp) {
@@ -2107,7 +2172,11 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
 
     // term tables: nu split hi/lo, float weights; zero padded past the end
     const int ld = nrange + TAB_PAD;
-    std::vector<float> h_tab((size_t)3 * ld, 0.f);
+    double Rx[16] = {0};
+    std::vector<float> bx;
+    if (!box) right_ext_coeffs(sp, L.Ex, Rx, bx);
+    std::vector<float> h_tab(tab_bx_offset(nrange) + bx.size(), 0.f);
+    std::copy(bx.begin(), bx.end(), h_tab.begin() + tab_bx_offset(nrange));
     for (int j = 0; j < nrange; ++j) {
         double nu = terms->nu[tbeg + j];
         float hi = (float)nu;
@@ -2182,7 +2251,6 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         float* floc = slot(bi, L.s_floc);
         float* lc = slot(bi, L.s_lc);
         float* edge = slot(bi, L.s_edge);
-        float* ext = slot(bi, L.s_ext);
         float* bst = slot(bi, L.s_bst);
         float* part = slot(bi, L.s_part);
         // the slot is free once batch bi - nslot has finished on s2
@@ -2276,7 +2344,8 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             }
             ca.edge = edge;
             ca.lcarry = lc;
-            ca.extbuf = ext;
+            for (int q = 0; q < 16; ++q) ca.Rx[q] = (float)Rx[q];
+            ca.bx = reinterpret_cast<const float4*>(tab + tab_bx_offset(nrange));
             ca.bstate = bst;
             dim3 gc((H + 127) / 128, n * B);
             { Prof pr(KK_CHAIN, s2); k_chain<<<gc, 128, 0, s2>>>(ca); }

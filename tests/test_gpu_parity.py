@@ -39,10 +39,18 @@ def _spec(tb, kind, param):
     return tb.SpatialSpec.box(param) if kind == "box" else tb.SpatialSpec.gaussian_recursive(param)
 
 
-def _run(tb, f, kind, param, sigma_r, degree=None, **kw):
+def _run(tb, f, kind, param, sigma_r, degree=None, path="device", **kw):
+    """path: "device" (CUDA tensor in/out), "numpy" (host entry, pageable),
+    "pinned" (host entry, pinned: strip/band-overlapped copies)."""
     k = tb.make_trig_kernel(sigma_r, 255.0, degree=degree)
-    out = tb.bilateral_trig(torch.from_numpy(np.ascontiguousarray(f, dtype=np.float32)).cuda(),
-                            _spec(tb, kind, param), k, **kw)
+    f32 = np.ascontiguousarray(f, dtype=np.float32)
+    if path == "numpy":
+        out = tb.bilateral_trig(f32, _spec(tb, kind, param), k, **kw)
+        return np.asarray(out, dtype=np.float64)
+    t = torch.from_numpy(f32)
+    t = t.pin_memory() if path == "pinned" else t.cuda()
+    out = tb.bilateral_trig(t, _spec(tb, kind, param), k, **kw)
+    assert out.is_cuda == (path == "device")
     return out.cpu().numpy().astype(np.float64)
 
 
@@ -50,14 +58,15 @@ def _run(tb, f, kind, param, sigma_r, degree=None, **kw):
 # golden vectors from the real reference
 # ---------------------------------------------------------------------------
 
-def test_small_goldens(tb, small_cases):
+@pytest.mark.parametrize("path", ["device", "numpy", "pinned"])
+def test_small_goldens(tb, small_cases, path):
     worst = 0.0
     for name, c in small_cases.items():
-        got = _run(tb, c["f"], c["kind"], c["param"], c["sigma_r"], c["degree"])
+        got = _run(tb, c["f"], c["kind"], c["param"], c["sigma_r"], c["degree"], path=path)
         err = float(np.max(np.abs(got - c["out"])))
         worst = max(worst, err)
         assert err <= TOL, (name, err)
-    print(f"small goldens: worst max abs err {worst:.3g}")
+    print(f"small goldens ({path}): worst max abs err {worst:.3g}")
 
 
 def test_image_roundtrip_matches_golden(tb, small_cases):
@@ -83,6 +92,10 @@ def test_config_goldens(tb, cfg_id):
     for fi in frames:
         f = torch.from_numpy(workloads.frame(cfg, fi)).cuda()
         out = tb.bilateral_trig(f, spec, k)
+        if cfg_id in (1, 2) and fi == frames[0]:
+            # the host entry (pinned, strip/band overlapped) gives the same bits
+            host = tb.bilateral_trig(f.cpu().pin_memory(), spec, k)
+            assert torch.equal(host, out.cpu())
         sel = g["frame"] == fi
         got = out[torch.from_numpy(g["y"][sel]).cuda(), torch.from_numpy(g["x"][sel]).cuda()]
         err = float(np.max(np.abs(got.double().cpu().numpy() - g["value"][sel])))
