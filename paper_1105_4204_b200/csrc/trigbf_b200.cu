@@ -1410,9 +1410,11 @@ __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_gauss(const __grid_cons
 // partial traffic (pass-2 writes + reduce reads) drops 4x.
 constexpr int P2R_GR = 4;
 
+constexpr int P2R_SMEM = 2 * P2R_GR * TILE * 32 * 8;  // double-buffered float2 [2][warp][x][row]
+
 template <int G>
 __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_constant__ Pass2Args a) {
-    __shared__ float2 sbuf[P2R_GR][TILE][32];  // [warp][x in tile][row]
+    extern __shared__ float2 sdyn[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nsb = a.nrb_run * (P2_THREADS / 32);  // 32-row sub-blocks in this launch
     const int chunk = blockIdx.x / nsb;
@@ -1444,7 +1446,9 @@ __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_consta
     const size_t xpl = xm_plane(a.B, W, H);
     float* pn = a.part + (size_t)(blockIdx.y * 2 + 0) * xpl + xm_index(b, 0, iv ? i_raw : 0, W, H);
     float* pd = a.part + (size_t)(blockIdx.y * 2 + 1) * xpl + xm_index(b, 0, iv ? i_raw : 0, W, H);
-    float2* const sb = &sbuf[w][0][lane];
+    // tile k of this block stages in buffer k & 1: one barrier per tile (the
+    // buffer written next was last read before the previous barrier)
+    auto sbuf = [&](int buf, int q, int m) -> float2& { return sdyn[((buf * P2R_GR + q) * TILE + m) * 32 + lane]; };
 
     const int t_lo = chunk * a.tiles_per_chunk;
     const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
@@ -1488,20 +1492,23 @@ __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_consta
         }
     } else {
 #pragma unroll
-        for (int m = 0; m < TILE; ++m) sb[m * 32] = make_float2(0.f, 0.f);
+        for (int m = 0; m < TILE; ++m) {
+            sbuf(0, w, m) = make_float2(0.f, 0.f);
+            sbuf(1, w, m) = make_float2(0.f, 0.f);
+        }
     }
 #pragma unroll 1
-    for (int t = t_hi - 1; t >= t_lo; --t) {
-        if (active) p2_tile<G, true, true>(a, c, t, p1, p2, q1, q2, pn, pd, iv, sb);
+    for (int t = t_hi - 1, buf = 0; t >= t_lo; --t, buf ^= 1) {
+        if (active) p2_tile<G, true, true>(a, c, t, p1, p2, q1, q2, pn, pd, iv, &sbuf(buf, w, 0));
         __syncthreads();
         const int x0 = t * TILE;
         const int len = min(TILE, W - x0);
         if (iv) {
             for (int m = w; m < len; m += P2R_GR) {
-                float2 acc = sbuf[0][m][lane];
+                float2 acc = sbuf(buf, 0, m);
 #pragma unroll
                 for (int q = 1; q < P2R_GR; ++q) {
-                    const float2 v = sbuf[q][m][lane];
+                    const float2 v = sbuf(buf, q, m);
                     acc.x += v.x;
                     acc.y += v.y;
                 }
@@ -1510,7 +1517,6 @@ __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_consta
                 pd[off] = acc.y;
             }
         }
-        __syncthreads();
     }
 }
 
@@ -1781,16 +1787,28 @@ __global__ void k_range_check(const float* f, long long n, double lo, double hi,
     if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&counters[0], bad);
 }
 
-// f[b][i][x] -> fT[b][x][i]
-__global__ void __launch_bounds__(256) k_transpose(const float* f, float* fT, int H, int W) {
+// f[b][i][x] -> fT[b][x][i]; with counters, also the range check of
+// engines.py:218-225 on the same loads (counters[0] += samples outside
+// [lo, hi] or NaN, as k_range_check)
+__global__ void __launch_bounds__(256) k_transpose(const float* f, float* fT, int H, int W, double lo,
+                                                   double hi, unsigned long long* counters) {
     __shared__ float t[TILE][TILE + 1];
     const int b = blockIdx.z;
     const int x0 = blockIdx.x * TILE, i0 = blockIdx.y * TILE;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const float* src = f + (size_t)b * H * W;
+    unsigned bad = 0;
     for (int r = ty; r < TILE; r += 8) {
         int gi = i0 + r, gx = x0 + tx;
-        t[r][tx] = (gi < H && gx < W) ? src[(size_t)gi * W + gx] : 0.f;
+        const bool in = gi < H && gx < W;
+        const float v = in ? src[(size_t)gi * W + gx] : 0.f;
+        const double dv = (double)v;
+        bad += in && !(dv >= lo && dv <= hi);
+        t[r][tx] = v;
+    }
+    if (counters) {
+        bad = __reduce_add_sync(0xffffffffu, bad);
+        if (tx == 0 && bad) atomicAdd(&counters[0], (unsigned long long)bad);
     }
     __syncthreads();
     for (int r = ty; r < TILE; r += 8) {
@@ -1925,24 +1943,33 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     L->ng2 = tb / G2;
     L->nb = (nterms_range + tb - 1) / tb;
     L->nslot = (g_pipeline && !box && L->nb > 1) ? 2 : 1;
-    // pass-1 y-chunking: split columns into chunks of rows when column tiles x
-    // terms cannot fill ~4 waves of the GPU, keeping the warm-up <= 1/6 of a chunk
+    // pass-1 y-chunking: split columns into chunks of rows (each with ywarm
+    // warm-up rows on its inner sides) to fill the GPU.  Cost model fitted on
+    // B200 sweeps (round 1, configs 1/2/4): a block's time is its row count;
+    // above one wave of blocks the kernel takes (waves + 0.9) block times
+    // (tail), below one wave a single block time.
     L->ywarm = (std::max(sp->ext_y, 1) + TILE - 1) / TILE * TILE;
     L->nyc = 1;
     L->ych_rows = H;
     if (!box) {
-        const long long warps = (long long)L->ntx * tb * B;
-        const long long target = 4LL * 148 * 4 * P1_BLOCKS_PER_SM;
-        int nyc = 1;
-        while (warps * nyc < target) {
-            const int rows = ((H + 2 * nyc - 1) / (2 * nyc) + TILE - 1) / TILE * TILE;
-            // long chunks: warm-up <= 1/6; below one wave of warps (latency-
-            // bound small images) accept warm-up up to the chunk length
-            const bool ok = rows >= 6 * L->ywarm ||
-                            (warps * nyc < 148LL * 4 * P1_BLOCKS_PER_SM && rows >= L->ywarm);
-            if (!ok) break;
-            nyc *= 2;
+        const double slots = 148.0 * P1_BLOCKS_PER_SM;
+        const double blocks1 = (double)L->ntx * ((tb + P1_WARPS - 1) / P1_WARPS) * B;
+        double best = -1.0;
+        int best_n = 1;
+        for (int nyc = 1; nyc <= 16; ++nyc) {
+            const int rows = ((H + nyc - 1) / nyc + TILE - 1) / TILE * TILE;
+            const int n = (H + rows - 1) / rows;
+            if (n != nyc) continue;  // same split as a smaller count
+            if (nyc > 1 && rows < L->ywarm) break;
+            const double len = nyc == 1 ? (double)H + 2.0 * L->Ey : (double)rows + 2.0 * L->ywarm;
+            const double waves = blocks1 * nyc / slots;
+            const double cost = len * (waves <= 1.0 ? 1.0 : waves + 0.9);
+            if (best < 0 || cost < best * 0.98) {  // prefer fewer chunks on near ties
+                best = cost;
+                best_n = nyc;
+            }
         }
+        int nyc = best_n;
         if (g_p1_ychunks > 0) nyc = std::min(g_p1_ychunks, (H + TILE - 1) / TILE);
         L->ych_rows = ((H + nyc - 1) / nyc + TILE - 1) / TILE * TILE;
         L->nyc = (H + L->ych_rows - 1) / L->ych_rows;
@@ -2122,6 +2149,7 @@ void set_p1_smem() {
                          p2t_smem_bytes<G2>());
     cudaFuncSetAttribute(k_pass2_tma<G2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          p2t_smem_bytes<G2>());
+    cudaFuncSetAttribute(k_pass2_gr<G2>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2R_SMEM);
     cudaFuncSetAttribute(k_pass1_gauss<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
     cudaFuncSetAttribute(k_pass1_gauss<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
     cudaFuncSetAttribute(k_pass1_box<G1, R_ANCHOR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2214,16 +2242,15 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         }
         cudaStreamWaitEvent(st, ev_strip.back(), 0);
         if ((rc = check_cuda("host to device"))) return rc;
-        if (counters) {
-            const long long count = (long long)B * H * W;
-            const long long blocks = std::min<long long>((count + 255) / 256, 148LL * 8);
-            Prof pr(KK_RANGE, st);
-            k_range_check<<<(unsigned)blocks, 256, 0, st>>>(f, count, -1e-9, terms->T + 1e-9, counters);
-        }
     }
 
+    // transpose, fused with the input range check in the full filter
+    // (tbf_bilateral_trig / _host); the sharded path checks separately
     dim3 tgrid((W + TILE - 1) / TILE, (H + TILE - 1) / TILE, B);
-    { Prof pr(KK_TRANSPOSE, st); k_transpose<<<tgrid, 256, 0, st>>>(f, fT, H, W); }
+    {
+        Prof pr(KK_TRANSPOSE, st);
+        k_transpose<<<tgrid, 256, 0, st>>>(f, fT, H, W, -1e-9, terms->T + 1e-9, out ? counters : nullptr);
+    }
     if ((rc = check_cuda("transpose"))) return rc;
 
     set_p1_smem();
@@ -2444,7 +2471,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 if (box)
                     k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, q>>>(p2, sp->radius);
                 else if (p2var == 6)
-                    k_pass2_gr<G2><<<dim3(nrun * (P2_THREADS / 32) * nchunk, npart, B), 32 * P2R_GR, 0, q>>>(p2);
+                    k_pass2_gr<G2><<<dim3(nrun * (P2_THREADS / 32) * nchunk, npart, B), 32 * P2R_GR, P2R_SMEM, q>>>(p2);
                 else if (p2var == 4)
                     k_pass2_async<4><<<g2, P2_THREADS, p2a_smem_bytes<4>(), q>>>(p2);
                 else if (p2var == 5)
@@ -2614,11 +2641,7 @@ int tbf_bilateral_trig(const float* f, float* out, int32_t B, int32_t H, int32_t
                        void* stream) {
     if (!terms) return fail(TBF_ERR_PARAM, "null terms");
     cudaStream_t st = (cudaStream_t)stream;
-    int rc;
-    if (d_counters) {
-        rc = tbf_range_check(f, (int64_t)B * H * W, terms->T, d_counters, stream);
-        if (rc) return rc;
-    }
+    // the range check runs inside run_terms (fused with the transpose)
     return run_terms(f, nullptr, nullptr, out, B, H, W, sp, terms, 0, terms->n_terms, batch_terms,
                      0, workspace, workspace_bytes, d_counters, st);
 }

@@ -88,7 +88,10 @@ def summarise_rep(rep, out_md, traffic_json):
                     return float(num.replace(",", "")) * scale.get(unit.strip(), 1.0)
                 rd = nbytes(d["dram__bytes_read.sum"])
                 wr = nbytes(d["dram__bytes_write.sum"])
-                traffic[k.replace("k_", "").replace("_gauss", "")] = rd + wr
+                # profiler kinds: every pass-2 variant is "pass2"
+                kind = k.replace("k_", "").replace("_gauss", "")
+                kind = "pass2" if kind.startswith("pass2") else kind
+                traffic[kind] = rd + wr
             except Exception:
                 pass
         with open(traffic_json, "w") as fh:
