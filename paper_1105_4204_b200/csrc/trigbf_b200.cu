@@ -55,14 +55,26 @@ namespace {
 constexpr int TILE = 32;          // segment length along y == tile width along x == warp size
 constexpr int P1_WARPS = 4;       // warps per pass-1 block (each a different term group)
 constexpr int P2_THREADS = 128;   // rows per pass-2 block
-constexpr int FL_RB = 128;        // row-block height of the x-major tiling (== P2_THREADS)
+constexpr int FL_RB = 32;         // row-block height of the x-major tiling: one pass-2 warp's rows,
+                                  // so a warp streams 512 contiguous bytes per x-step and its
+                                  // consecutive x-steps are adjacent
 
 // x-major per-pixel planes read by pass 2 (fT, partial num/den, and F_loc per
-// term) are row-block tiled: [b][row block of 128][x][128 rows], so a pass-2
-// block streams its rows contiguously as x advances.
+// term) are row-block tiled: [b][row block of 32][x][32 rows], so a pass-2
+// warp streams its rows contiguously as x advances.
 __host__ __device__ __forceinline__ size_t xm_index(int b, int x, int i, int W, int H) {
     const int nrb = (H + FL_RB - 1) / FL_RB;
     return (((size_t)b * nrb + i / FL_RB) * W + x) * FL_RB + (i % FL_RB);
+}
+// Tile-major copy of f read by pass 1: [b][row tile][column tile][32][32],
+// so the 32 rows of a warp's 32 columns are 4 KB contiguous (row loads are
+// coalesced 128 B with immediate offsets from one base address).
+__host__ __device__ __forceinline__ size_t ty_index(int b, int x, int i, int W, int H) {
+    const int nys = (H + 31) / 32, ntx = (W + 31) / 32;
+    return ((((size_t)b * nys + i / 32) * ntx + x / 32) * 32 + (i % 32)) * 32 + (x % 32);
+}
+__host__ __device__ __forceinline__ size_t ty_plane(int B, int W, int H) {
+    return (size_t)B * ((H + 31) / 32) * 32 * ((W + 31) / 32) * 32;
 }
 __host__ __device__ __forceinline__ size_t xm_plane(int B, int W, int H) {
     return (size_t)B * ((H + FL_RB - 1) / FL_RB) * FL_RB * W;
@@ -166,6 +178,15 @@ __device__ __forceinline__ long long mirror_any(long long i, long long n) {
     i %= period;
     if (i < 0) i += period;
     return i >= n ? period - i : i;
+}
+
+// Read-only global load kept in program order relative to the surrounding
+// shared-memory stores (volatile + memory clobber): pins prefetches where the
+// source puts them instead of letting them sink next to their use.
+__device__ __forceinline__ float ldg_pinned(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
 }
 
 // One pure cascade step (state v1,v2 | y1,y2); output scaled by 1/g.
@@ -324,6 +345,7 @@ struct TermDev {
 
 struct Pass1Args {
     const float* f;
+    const float* fY;  // f tile-major (ty_index): a warp's 32-row segment is 4 KB contiguous
     int B, H, W;
     int Ey, nseg;  // y mirror extension; checkpoint segments per y-chunk
     int nyc, ych_rows, ywarm;  // y-chunks of ych_rows output rows; warm-up rows (mult. of 32)
@@ -446,10 +468,9 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     const Casc k = a.k;
     const int Ey = a.Ey;
     const int iend = H + Ey;  // forward runs over extended rows [-Ey, H+Ey)
-    const float* const fcol = a.f + (size_t)b * H * W + xc;
     auto fload = [&](int i) -> float {  // f at extended row i (mirrored), clamped
         i = max(-Ey, min(i, iend - 1));
-        return __ldg(fcol + (size_t)mirror1(i, H) * W);
+        return __ldg(a.fY + ty_index(b, xc, mirror1(i, H), W, H));
     };
     // y-chunk: output rows [R0, R1).  The forward sweep starts at A0 = R0 -
     // ywarm from a steady-state guess (exact -Ey start for the top chunk); the
@@ -541,42 +562,36 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                 y2[p] = ckn[p].w;
             }
         }
-        // the next step's f rows (and its checkpoint in phase B) are prefetched
-        // into the register ring seg_f: each 8-row slot is refilled as soon as
-        // this step has consumed it (no register shifts)
+        // the next step's checkpoint (phase B) and f rows are loaded at the
+        // start of this step, one whole segment ahead of their use
         const int ns = step + 1 < nseg ? step + 1 : max(nsteps - 2 - step, 0);
         const int rn = R0 + ns * TILE;
-        const bool rn_interior = rn >= 0 && rn + TILE <= H;
-        const float* const fpn = fcol + (size_t)max(rn, 0) * W;
-        auto refill = [&](int q0) {  // rows rn + q0 .. rn + q0 + 7 into slot q0
-            if (rn_interior) {
-#pragma unroll
-                for (int q = 0; q < 8; ++q) seg_f[q0 + q] = __ldg(fpn + (size_t)(q0 + q) * W);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 8; ++q) seg_f[q0 + q] = fload(rn + q0 + q);
-            }
-        };
         if (step + 1 >= nseg && step + 1 < nsteps) {  // checkpoint first (before the f burst)
             const float4* ck = ck0 + (size_t)ns * cks;  // after this step's store (same thread)
 #pragma unroll
             for (int p = 0; p < 4; ++p) ckn[p] = ck[p];
         }
+        float nxt[TILE];
+        if (rn >= 0 && rn + TILE <= H) {
+            // interior: the segment is one 32x32 tile of fY (rn is a multiple
+            // of 32): row q of this lane's column at base + 32 q (immediate offsets)
+            const float* const fpn = a.fY + ty_index(b, x0 + lane, rn, W, H);
+#pragma unroll
+            for (int q = 0; q < TILE; ++q) nxt[q] = ldg_pinned(fpn + q * 32);
+        } else {
+#pragma unroll
+            for (int q = 0; q < TILE; ++q) nxt[q] = fload(rn + q);
+        }
         // forward over the segment into the smem tile (own column); the first
         // phase-B step finds the tile already filled by the last phase-A step
         const bool full = step != nseg && len == TILE;
         if (full) {
-            // 4 x 8 samples, unrolled over the ring slots (one shared copy for
-            // phases A and B keeps the instruction footprint in L1.5)
+            // 4 x 8 samples (unrolled; one shared copy for phases A and B keeps
+            // the instruction footprint in L1.5)
 #pragma unroll
-            for (int q0 = 0; q0 < TILE; q0 += 8) {
+            for (int q0 = 0; q0 < TILE; q0 += 8)
                 p1_fwd8<true>(*reinterpret_cast<const float(*)[8]>(&seg_f[q0]), nu_hi, nu_lo, k, v1, v2,
                               y1, y2, bl + q0 * BUF_LD);
-                refill(q0);
-            }
-        } else {
-#pragma unroll
-            for (int q0 = 0; q0 < TILE; q0 += 8) refill(q0);
         }
         if (step != nseg && !full) {
             {
@@ -592,6 +607,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                 }
             }
         }
+#pragma unroll
+        for (int q = 0; q < TILE; ++q) seg_f[q] = nxt[q];
         if (!phaseB) continue;
         if (seg == nseg - 1) {
             // backward start = steady state of the last forward output (_core.pyx:85-87)
@@ -1020,6 +1037,7 @@ __global__ void __launch_bounds__(P2T_THREADS, MINB) k_pass2_tma(const __grid_co
             }
             const float* fTrow = a.fT + xm_index(b, 0, i0, W, H);
             const uint32_t bytes = (uint32_t)(P2T_STEPS * (G * nrow * 16 + nrow4 * 4));
+            const size_t sbs = (size_t)W * FL_RB;  // stride between 32-row blocks
             for (int blk = 0; blk < nblk; ++blk) {
                 const int st = blk % P2T_NST;
                 if (blk >= P2T_NST) mbar_wait(&empty[st], ((blk / P2T_NST) - 1) & 1);
@@ -1028,12 +1046,17 @@ __global__ void __launch_bounds__(P2T_THREADS, MINB) k_pass2_tma(const __grid_co
 #pragma unroll
                 for (int q = 0; q < P2T_STEPS; ++q) {
                     const int x = xs - q;
+                    // one bulk copy per 32-row block of the block's rows
+                    for (int r0 = 0; r0 < nrow; r0 += FL_RB) {
+                        const int rows = min(FL_RB, nrow - r0);
+                        const size_t src = (size_t)(r0 / FL_RB) * sbs + (size_t)x * FL_RB;
 #pragma unroll
-                    for (int g = 0; g < G; ++g)
-                        bulk_g2s(Fb + ((st * P2T_STEPS + q) * G + g) * P2_THREADS, flrow[g] + (size_t)x * FL_RB,
-                                 (uint32_t)nrow * 16, &full[st]);
-                    bulk_g2s(Tb + (st * P2T_STEPS + q) * P2_THREADS, fTrow + (size_t)x * FL_RB,
-                             (uint32_t)nrow4 * 4, &full[st]);
+                        for (int g = 0; g < G; ++g)
+                            bulk_g2s(Fb + ((st * P2T_STEPS + q) * G + g) * P2_THREADS + r0, flrow[g] + src,
+                                     (uint32_t)rows * 16, &full[st]);
+                        bulk_g2s(Tb + (st * P2T_STEPS + q) * P2_THREADS + r0, fTrow + src,
+                                 (uint32_t)((rows + 3) / 4 * 4) * 4, &full[st]);
+                    }
                 }
             }
         }
@@ -1790,13 +1813,15 @@ __global__ void k_range_check(const float* f, long long n, double lo, double hi,
 // f[b][i][x] -> fT[b][x][i]; with counters, also the range check of
 // engines.py:218-225 on the same loads (counters[0] += samples outside
 // [lo, hi] or NaN, as k_range_check)
-__global__ void __launch_bounds__(256) k_transpose(const float* f, float* fT, int H, int W, double lo,
-                                                   double hi, unsigned long long* counters) {
+__global__ void __launch_bounds__(256) k_transpose(const float* f, float* fT, float* fY, int H, int W,
+                                                   double lo, double hi, unsigned long long* counters,
+                                                   int tx0) {
     __shared__ float t[TILE][TILE + 1];
     const int b = blockIdx.z;
-    const int x0 = blockIdx.x * TILE, i0 = blockIdx.y * TILE;
+    const int x0 = (tx0 + blockIdx.x) * TILE, i0 = blockIdx.y * TILE;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const float* src = f + (size_t)b * H * W;
+    float* const ytile = fY + ty_index(b, x0, i0, W, H);  // whole 32x32 tile (padding zeroed)
     unsigned bad = 0;
     for (int r = ty; r < TILE; r += 8) {
         int gi = i0 + r, gx = x0 + tx;
@@ -1805,6 +1830,7 @@ __global__ void __launch_bounds__(256) k_transpose(const float* f, float* fT, in
         const double dv = (double)v;
         bad += in && !(dv >= lo && dv <= hi);
         t[r][tx] = v;
+        ytile[r * 32 + tx] = v;
     }
     if (counters) {
         bad = __reduce_add_sync(0xffffffffu, bad);
@@ -1898,7 +1924,7 @@ struct Layout {
     int nb;     // batches
     int nslot;  // batch buffer sets (2 = pass 1 of batch k+1 overlaps the rest of batch k)
     // shared buffers
-    size_t off_fT, off_num, off_den, off_tab;
+    size_t off_fT, off_fY, off_num, off_den, off_tab;
     // per-slot buffers (offsets relative to the slot base)
     size_t off_slot, slot_bytes;
     size_t s_ckpt, s_floc, s_lc, s_edge, s_ext, s_bst, s_part;
@@ -1979,6 +2005,8 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     size_t o = 0;
     L->off_fT = o;
     o = align_up(o + xm_plane(B, W, H) * 4);
+    L->off_fY = o;
+    o = align_up(o + ty_plane(B, W, H) * 4);
     const bool multi = L->nb > 1;
     L->off_num = o;
     if (multi) o = align_up(o + px * 4);
@@ -2183,6 +2211,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         return fail(TBF_ERR_WORKSPACE, "workspace too small: need %zu have %zu", L.total, ws_bytes);
     char* w8 = (char*)ws;
     float* fT = (float*)(w8 + L.off_fT);
+    float* fY = (float*)(w8 + L.off_fY);
     float* tab = (float*)(w8 + L.off_tab);
     auto slot = [&](int k, size_t off) { return (float*)(w8 + L.off_slot + (size_t)(k % L.nslot) * L.slot_bytes + off); };
     const bool box = sp->kind == TBF_SPATIAL_BOX;
@@ -2245,11 +2274,14 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
     }
 
     // transpose, fused with the input range check in the full filter
-    // (tbf_bilateral_trig / _host); the sharded path checks separately
-    dim3 tgrid((W + TILE - 1) / TILE, (H + TILE - 1) / TILE, B);
-    {
+    // (tbf_bilateral_trig / _host); the sharded path checks separately.  With
+    // host strips, each strip is transposed on its own stream before its pass 1.
+    const bool strip_p1 = hpipe && ev_strip.size() > 1;
+    unsigned long long* const rc_counters = out ? counters : nullptr;
+    if (!strip_p1) {
+        dim3 tgrid((W + TILE - 1) / TILE, (H + TILE - 1) / TILE, B);
         Prof pr(KK_TRANSPOSE, st);
-        k_transpose<<<tgrid, 256, 0, st>>>(f, fT, H, W, -1e-9, terms->T + 1e-9, out ? counters : nullptr);
+        k_transpose<<<tgrid, 256, 0, st>>>(f, fT, fY, H, W, -1e-9, terms->T + 1e-9, rc_counters, 0);
     }
     if ((rc = check_cuda("transpose"))) return rc;
 
@@ -2292,6 +2324,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
 
         Pass1Args p1;
         p1.f = f;
+        p1.fY = fY;
         p1.B = B;
         p1.H = H;
         p1.W = W;
@@ -2315,14 +2348,20 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p1.edge = edge;
         dim3 g1(L.ntx * (box ? 1 : L.nyc), (p1.ngroups + P1_WARPS - 1) / P1_WARPS, B);
         const int p1smem = g_p1_occ == 2 ? P1_SMEM_OCC2 : P1_SMEM;
-        if (hpipe && bi == 0 && ev_strip.size() > 1) {
-            // strip s on alternating streams, after its copy; joined before the chain
+        if (strip_p1 && bi == 0) {
+            // strip s on alternating streams, after its copy: transpose (+
+            // range check), then pass 1; joined before the chain
             for (size_t s = 0; s < ev_strip.size(); ++s) {
                 cudaStream_t ps = aux_stream(2 + (int)(s & 1));
                 cudaStreamWaitEvent(ps, e_ready, 0);
                 cudaStreamWaitEvent(ps, ev_strip[s], 0);
                 p1.tile0 = (int)s * tps;
                 p1.ntx_run = std::min(tps, L.ntx - p1.tile0);
+                {
+                    dim3 tg(p1.ntx_run, (H + TILE - 1) / TILE, B);
+                    Prof pr(KK_TRANSPOSE, ps);
+                    k_transpose<<<tg, 256, 0, ps>>>(f, fT, fY, H, W, -1e-9, terms->T + 1e-9, rc_counters, p1.tile0);
+                }
                 dim3 gs(p1.ntx_run * L.nyc, g1.y, B);
                 {
                     Prof pr(KK_PASS1, ps);
