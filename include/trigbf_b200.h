@@ -126,6 +126,21 @@ TBF_API int tbf_finalize(const float* num, const float* den, const float* f, flo
 TBF_API int tbf_range_check(const float* f, int64_t count, double T, unsigned long long* d_counters,
                     void* stream);
 
+/* Brute-force bilateral filter in fp64 (engines.py:120-151 bilateral_direct):
+ * the reference's validation engine, used here to report the trig filter's
+ * error against brute-force Gaussian bilateral on every config.  f is
+ * [B][H][W] fp32 on the device; taps (device, 2*radius+1 doubles) are the
+ * separable window (engines.py:96-106: uniform for box, truncated Gaussian
+ * FIR otherwise).  range_kind 0: Gaussian exp(-s^2 / 2 range_param^2);
+ * 1: raised cosine cos(range_param * s)^degree (= trig_eval).  samples:
+ * NULL for every pixel (out[B*H*W]), else n (b, y, x) int32 triples
+ * (out[n]).  Borders reflect as np.pad(mode="reflect"); den < 1e-12 gives
+ * the centre sample and counts d_counters[1] (if non-NULL). */
+TBF_API int tbf_bilateral_direct(const float* f, int32_t B, int32_t H, int32_t W, const int32_t* samples,
+                         int64_t n, const double* taps, int32_t radius, int32_t range_kind,
+                         double range_param, int32_t degree, double* out, unsigned long long* d_counters,
+                         void* stream);
+
 /* Plugin-level twins of the reference's compiled core, fp64 like the
  * reference.  recursive_smooth filters along axis 0 of a[h][w] with `pad`
  * mirrored rows per side and replicate start-up; scratch holds

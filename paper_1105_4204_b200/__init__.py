@@ -11,6 +11,7 @@ from .engines import (
     EngineDiagnostics,
     TrigFilter,
     bilateral_color,
+    bilateral_direct,
     bilateral_trig,
     bilateral_trig_color,
     clear_plans,
@@ -20,6 +21,7 @@ from .errors import DimensionError, NativeUnavailableError, ParameterError, Trig
 from .image import ErrorStats, Image, error_stats, image_from_planes
 from .kernels import (
     DEGREE_TABLE_8BIT,
+    GaussianRange,
     TermPairs,
     TrigKernel,
     degree_estimate,
@@ -34,17 +36,19 @@ from .spatial import (
     SpatialKind,
     SpatialSpec,
     decay_length,
+    gaussian_taps,
     recursive_biquads,
     recursive_coeffs,
+    window_taps,
 )
 
 __version__ = "0.1.0"
 
 __all__ = [
     "Boundary", "DEGREE_TABLE_8BIT", "DimensionError", "ETA_GUARD", "EngineDiagnostics",
-    "ErrorStats", "Image", "NativeUnavailableError", "ParameterError", "SpatialKind",
+    "ErrorStats", "GaussianRange", "Image", "NativeUnavailableError", "ParameterError", "SpatialKind",
     "SpatialSpec", "TermPairs", "TrigFilter", "TrigKernel", "TrigbfError", "bilateral_color",
-    "bilateral_trig", "bilateral_trig_color", "clear_plans", "decay_length", "degree_estimate", "error_stats",
-    "gaussian_eval", "get_plan", "image_from_planes", "make_trig_kernel", "recursive_biquads",
-    "recursive_coeffs", "select_degree", "term_pairs", "trig_eval",
+    "bilateral_direct", "bilateral_trig", "bilateral_trig_color", "clear_plans", "decay_length", "degree_estimate", "error_stats",
+    "gaussian_eval", "gaussian_taps", "get_plan", "image_from_planes", "make_trig_kernel", "recursive_biquads",
+    "recursive_coeffs", "select_degree", "term_pairs", "trig_eval", "window_taps",
 ]

@@ -41,6 +41,7 @@ EXPORTS = (
     "tbf_workspace_bytes",
     "tbf_bilateral_trig",
     "tbf_bilateral_trig_host",
+    "tbf_bilateral_direct",
     "tbf_trig_partial",
     "tbf_finalize",
     "tbf_range_check",
@@ -108,6 +109,10 @@ def _declare(lib):
     lib.tbf_bilateral_trig_host.argtypes = [
         _vp, _vp, _i32, _i32, _i32, ctypes.POINTER(TbfSpatial), ctypes.POINTER(TbfTerms), _i32,
         _vp, _vp, _sz, _vp, _vp,
+    ]
+    lib.tbf_bilateral_direct.restype = ctypes.c_int
+    lib.tbf_bilateral_direct.argtypes = [
+        _vp, _i32, _i32, _i32, _vp, _i64, _vp, _i32, _i32, _f64, _i32, _vp, _vp, _vp,
     ]
     lib.tbf_trig_partial.restype = ctypes.c_int
     lib.tbf_trig_partial.argtypes = [

@@ -1875,6 +1875,79 @@ __global__ void k_recursive_smooth_f64(const double* a, double* out, int h, int 
     for (int r = 0; r < h; ++r) out[(long long)r * w + xcol] = S(pad + r + 4);
 }
 
+// Brute-force bilateral filter (engines.py:120-151 bilateral_direct), fp64:
+// out = sum_w w*nb / sum_w w over the (2r+1)^2 window with weights
+// taps[dy] taps[dx] range(nb - center), np.pad(mode="reflect") borders
+// (repeated whole-sample reflection = mirror_any) and the guarded ratio
+// (engines.py:109-117).  One block per output pixel; the block reduction has
+// a fixed shape, so results are deterministic.  range kind 0: Gaussian
+// exp(-s^2/(2 sigma^2)) (kernels.py:174-182); 1: raised cosine cos(omega s)^N
+// (= trig_eval, kernels.py:161-171).
+constexpr int BF_THREADS = 256;
+
+__global__ void __launch_bounds__(BF_THREADS) k_bilateral_direct(const float* f, int B, int H, int W,
+                                                                const int32_t* samples, long long n,
+                                                                const double* taps, int r, int kind,
+                                                                double param, int degree, double* out,
+                                                                unsigned long long* guarded) {
+    __shared__ double sn[BF_THREADS], sd[BF_THREADS];
+    for (long long s = blockIdx.x; s < n; s += gridDim.x) {
+        int b, y, x;
+        if (samples) {
+            b = samples[3 * s];
+            y = samples[3 * s + 1];
+            x = samples[3 * s + 2];
+        } else {
+            b = (int)(s / ((long long)H * W));
+            const long long rem = s - (long long)b * H * W;
+            y = (int)(rem / W);
+            x = (int)(rem - (long long)y * W);
+        }
+        const float* F = f + (size_t)b * H * W;
+        const double c = (double)F[(size_t)y * W + x];
+        const int win = 2 * r + 1;
+        const long long taps2 = (long long)win * win;
+        double num = 0.0, den = 0.0;
+        const double inv2s2 = kind == 0 ? 1.0 / (2.0 * param * param) : 0.0;
+        for (long long t = threadIdx.x; t < taps2; t += BF_THREADS) {
+            const int dy = (int)(t / win) - r, dx = (int)(t % win) - r;
+            const long long yy = mirror_any((long long)y + dy, H), xx = mirror_any((long long)x + dx, W);
+            const double nb = (double)F[(size_t)yy * W + xx];
+            const double d = nb - c;
+            double rw;
+            if (kind == 0) {
+                rw = exp(-(d * d) * inv2s2);
+            } else {
+                double base = cos(param * d);
+                rw = 1.0;
+                for (int e = degree; e > 0; e >>= 1) {  // base^degree by squaring
+                    if (e & 1) rw *= base;
+                    base *= base;
+                }
+            }
+            const double wgt = taps[dy + r] * taps[dx + r] * rw;
+            num += wgt * nb;
+            den += wgt;
+        }
+        sn[threadIdx.x] = num;
+        sd[threadIdx.x] = den;
+        __syncthreads();
+        for (int o = BF_THREADS / 2; o > 0; o >>= 1) {
+            if (threadIdx.x < o) {
+                sn[threadIdx.x] += sn[threadIdx.x + o];
+                sd[threadIdx.x] += sd[threadIdx.x + o];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const bool gd = sd[0] < 1e-12;
+            out[s] = gd ? c : sn[0] / sd[0];
+            if (gd && guarded) atomicAdd(guarded, 1ULL);
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void k_box_pass_f64(const double* a, double* out, int h, int w, int radius) {
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= h) return;
@@ -2733,6 +2806,24 @@ int tbf_recursive_smooth_f64(const double* a, double* out, int32_t h, int32_t w,
     k_recursive_smooth_f64<<<(w + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
         a, out, h, w, scale, c1, c2, c3, c4, pad, scratch);
     return check_cuda("recursive_smooth_f64");
+}
+
+int tbf_bilateral_direct(const float* f, int32_t B, int32_t H, int32_t W, const int32_t* samples,
+                         int64_t n, const double* taps, int32_t radius, int32_t range_kind,
+                         double range_param, int32_t degree, double* out, unsigned long long* d_counters,
+                         void* stream) {
+    if (B < 1 || H < 1 || W < 1) return fail(TBF_ERR_DIM, "bad shape B=%d H=%d W=%d", B, H, W);
+    if (radius < 0 || !taps) return fail(TBF_ERR_PARAM, "bad window (radius %d)", radius);
+    if (range_kind != 0 && range_kind != 1) return fail(TBF_ERR_PARAM, "unknown range kind %d", range_kind);
+    if (range_kind == 0 && !(range_param > 0.0)) return fail(TBF_ERR_PARAM, "sigma_r must be positive");
+    if (range_kind == 1 && degree < 0) return fail(TBF_ERR_PARAM, "degree must be >= 0");
+    const long long count = samples ? (long long)n : (long long)B * H * W;
+    if (count <= 0) return fail(TBF_ERR_DIM, "no output pixels");
+    const unsigned grid = (unsigned)std::min<long long>(count, 148LL * 16);
+    k_bilateral_direct<<<grid, BF_THREADS, 0, (cudaStream_t)stream>>>(
+        f, B, H, W, samples, count, taps, radius, range_kind, range_param, degree, out,
+        d_counters ? d_counters + 1 : nullptr);
+    return check_cuda("bilateral_direct");
 }
 
 int tbf_box_pass_f64(const double* a, double* out, int32_t h, int32_t w, int32_t radius,

@@ -26,8 +26,8 @@ import numpy as np
 from . import _native
 from .errors import DimensionError, NativeUnavailableError, ParameterError
 from .image import Image
-from .kernels import TrigKernel, term_pairs
-from .spatial import SpatialKind, SpatialSpec, decay_length, recursive_biquads
+from .kernels import GaussianRange, TrigKernel, term_pairs
+from .spatial import SpatialKind, SpatialSpec, decay_length, recursive_biquads, window_taps
 
 ETA_GUARD = 1e-12  # engines.py:36
 WORKSPACE_FRACTION = 0.80  # of free device memory a plan may take
@@ -393,6 +393,81 @@ def bilateral_trig(img, spatial, kernel, *, workers: int = 1,
     plan.run_host(host, res)
     _finish(plan, shape, lambda: (float(host.min()), float(host.max())))
     return res
+
+
+def bilateral_direct(img, spatial, range_fn, *, samples=None,
+                     diagnostics: EngineDiagnostics | None = None):
+    """Brute-force bilateral filter on the GPU in fp64 (engines.py:120-151).
+
+    The reference's validation engine: every window sample is weighted by
+    taps[dy] * taps[dx] * range(nb - centre) (window_taps: uniform for box,
+    the truncated FIR Gaussian otherwise), borders reflect as np.pad
+    "reflect", and the guarded ratio applies.  ``range_fn`` is a TrigKernel
+    (raised cosine, = trig_eval) or a GaussianRange / positive float sigma
+    (Gaussian, = gaussian_eval); arbitrary callables are not evaluated on the
+    device.  ``samples`` = None filters every pixel and returns the input's
+    container type (Image, NumPy fp64, or a fp64 CUDA tensor); otherwise an
+    int array of (b, y, x) rows (or (y, x) rows for one frame) and the fp64
+    values at those pixels are returned as NumPy.
+    """
+    torch = _torch()
+    spatial = _check_spatial(spatial)
+    _require_cuda()
+    lib = _native.load()
+    if isinstance(range_fn, TrigKernel) or hasattr(range_fn, "coeffs"):
+        k = _check_kernel(range_fn)
+        kind, param, degree = 1, float(k.omega), int(k.N)
+    else:
+        sigma = range_fn.sigma if isinstance(range_fn, GaussianRange) else range_fn
+        if not isinstance(sigma, (int, float)) or sigma <= 0:
+            raise ParameterError("range_fn must be a TrigKernel, a GaussianRange or a positive sigma")
+        kind, param, degree = 0, float(sigma), 0
+    if isinstance(img, Image):
+        if img.channels != 1:
+            raise DimensionError(f"engine expects a single-channel image, got {img.channels} channels")
+        f = torch.from_numpy(np.ascontiguousarray(img.samples[0], dtype=np.float32)).cuda()
+    elif isinstance(img, np.ndarray):
+        f = torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32)).cuda()
+    elif isinstance(img, torch.Tensor):
+        f = img.to(device="cuda" if not img.is_cuda else img.device, dtype=torch.float32).contiguous()
+    else:
+        raise DimensionError(f"unsupported input type {type(img).__name__}")
+    if f.dim() not in (2, 3):
+        raise DimensionError(f"expected [H, W] or [B, H, W], got shape {tuple(f.shape)}")
+    B, H, W = (1, *f.shape) if f.dim() == 2 else tuple(f.shape)
+    taps = torch.from_numpy(window_taps(spatial)).to(f.device)
+    radius = (taps.numel() - 1) // 2
+    counters = torch.zeros(2, dtype=torch.int64, device=f.device)
+    d_s = None
+    if samples is not None:
+        sm = np.asarray(samples, dtype=np.int64)
+        if sm.ndim != 2 or sm.shape[1] not in (2, 3):
+            raise DimensionError("samples must be (n, 3) (b, y, x) or (n, 2) (y, x) rows")
+        if sm.shape[1] == 2:
+            sm = np.concatenate([np.zeros((sm.shape[0], 1), np.int64), sm], axis=1)
+        if sm.size and ((sm < 0).any() or (sm[:, 0] >= B).any() or (sm[:, 1] >= H).any()
+                        or (sm[:, 2] >= W).any()):
+            raise DimensionError("sample coordinates outside the image")
+        d_s = torch.from_numpy(np.ascontiguousarray(sm, dtype=np.int32)).to(f.device)
+        out = torch.empty(sm.shape[0], dtype=torch.float64, device=f.device)
+        n = sm.shape[0]
+    else:
+        out = torch.empty((B, H, W), dtype=torch.float64, device=f.device)
+        n = B * H * W
+    stream = torch.cuda.current_stream(f.device).cuda_stream
+    _native.check(lib.tbf_bilateral_direct(
+        f.data_ptr(), B, H, W, d_s.data_ptr() if d_s is not None else None, n, taps.data_ptr(),
+        radius, kind, param, degree, out.data_ptr(), counters.data_ptr(), stream))
+    guarded = int(counters[1].item())  # syncs
+    if diagnostics is not None:
+        diagnostics.guarded_pixels += guarded
+    if samples is not None:
+        return out.cpu().numpy()
+    if isinstance(img, Image):
+        return Image(img.width, img.height, 1, out.reshape(1, H, W).cpu().numpy())
+    if isinstance(img, np.ndarray):
+        return out.reshape(img.shape).cpu().numpy()
+    return out.reshape(img.shape)
 
 
 def _bilateral_trig_streamed(t, spatial, kernel, diagnostics, sub: int | None = None):

@@ -116,6 +116,22 @@ def trig_eval(k: TrigKernel, s):
     return float(vals) if arr.ndim == 0 else vals
 
 
+@dataclass(frozen=True)
+class GaussianRange:
+    """Gaussian range kernel exp(-s^2 / 2 sigma^2) as a value the GPU
+    brute-force engine can evaluate (the reference passes
+    ``lambda s: gaussian_eval(sigma, s)``)."""
+
+    sigma: float
+
+    def __post_init__(self):
+        if self.sigma <= 0.0:
+            raise ParameterError(f"sigma must be positive, got {self.sigma}")
+
+    def __call__(self, s):
+        return gaussian_eval(self.sigma, s)
+
+
 def gaussian_eval(sigma: float, s):
     """exp(-s^2 / 2 sigma^2) (kernels.py:174-182)."""
     if sigma <= 0.0:

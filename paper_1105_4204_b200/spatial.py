@@ -23,6 +23,8 @@ import enum
 import math
 from dataclasses import dataclass
 
+import numpy as np
+
 from .errors import ParameterError
 
 MIN_RECURSIVE_SIGMA = 0.5  # spatial.py:28
@@ -73,6 +75,26 @@ class SpatialSpec:
     @staticmethod
     def gaussian_fir(sigma_s: float) -> "SpatialSpec":
         return SpatialSpec(SpatialKind.GAUSSIAN_FIR, sigma_s=sigma_s)
+
+
+def gaussian_taps(sigma_s: float) -> np.ndarray:
+    """Discretized Gaussian truncated at +-ceil(4 sigma), renormalised to unit
+    DC gain (spatial.py:77-88)."""
+    if sigma_s <= 0.0:
+        raise ParameterError(f"sigma_s must be positive, got {sigma_s}")
+    r = math.ceil(4.0 * sigma_s)
+    i = np.arange(-r, r + 1, dtype=np.float64)
+    taps = np.exp(-(i * i) / (2.0 * sigma_s * sigma_s))
+    return taps / taps.sum()
+
+
+def window_taps(spatial: SpatialSpec) -> np.ndarray:
+    """1-D taps of the brute-force window (engines.py:96-106): uniform for box,
+    the truncated FIR Gaussian for both Gaussian kinds."""
+    if spatial.kind is SpatialKind.BOX:
+        n = 2 * spatial.radius + 1
+        return np.full(n, 1.0 / n)
+    return gaussian_taps(spatial.sigma_s)
 
 
 # spatial.py:95-98 -- prototype poles (radius, angle) of the two pairs.

@@ -125,3 +125,15 @@ def test_fp32_cascade_design_model():
             rec[t0 + i] = loc[i] + yh
         s = tuple(a + c for a, c in zip(h, z))
     assert np.max(np.abs(rec - full_fwd)) < 1e-9
+
+
+def test_window_taps_match_oracle():
+    """FIR/box window taps (spatial.py:77-88, engines.py:96-106)."""
+    from oracle import trigbf_oracle as orc
+    from paper_1105_4204_b200 import SpatialSpec, gaussian_taps, window_taps
+
+    for s in (0.5, 1.0, 3.0, 8.0, 32.0):
+        np.testing.assert_allclose(gaussian_taps(s), orc.gaussian_taps(s), rtol=0, atol=1e-15)
+        np.testing.assert_allclose(window_taps(SpatialSpec.gaussian_fir(s)), orc.window_taps("gauss-fir", s))
+    for r in (0, 1, 7):
+        np.testing.assert_array_equal(window_taps(SpatialSpec.box(r)), orc.window_taps("box", r))
