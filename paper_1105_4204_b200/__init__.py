@@ -17,8 +17,9 @@ from .engines import (
     clear_plans,
     get_plan,
 )
-from .errors import DimensionError, NativeUnavailableError, ParameterError, TrigbfError
+from .errors import DimensionError, NativeUnavailableError, ParameterError, PnmParseError, TrigbfError
 from .image import ErrorStats, Image, error_stats, image_from_planes
+from .pnm import read_pnm, write_pnm
 from .kernels import (
     DEGREE_TABLE_8BIT,
     GaussianRange,
@@ -46,9 +47,9 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Boundary", "DEGREE_TABLE_8BIT", "DimensionError", "ETA_GUARD", "EngineDiagnostics",
-    "ErrorStats", "GaussianRange", "Image", "NativeUnavailableError", "ParameterError", "SpatialKind",
+    "ErrorStats", "GaussianRange", "Image", "NativeUnavailableError", "ParameterError", "PnmParseError", "SpatialKind",
     "SpatialSpec", "TermPairs", "TrigFilter", "TrigKernel", "TrigbfError", "bilateral_color",
     "bilateral_direct", "bilateral_trig", "bilateral_trig_color", "clear_plans", "decay_length", "degree_estimate", "error_stats",
     "gaussian_eval", "gaussian_taps", "get_plan", "image_from_planes", "make_trig_kernel", "recursive_biquads",
-    "recursive_coeffs", "select_degree", "term_pairs", "trig_eval", "window_taps",
+    "read_pnm", "recursive_coeffs", "select_degree", "term_pairs", "trig_eval", "window_taps", "write_pnm",
 ]

@@ -8,6 +8,11 @@ Outputs (committed, small):
                        images (recursive Gaussian and box spatial, even/odd N,
                        degenerate shapes), plus plugin-level recursive_smooth /
                        box_pass vectors.
+  pnm_cases.npz     -- PNM round trips through the reference's pnm module:
+                       input bytes (with comments / odd whitespace), the parsed
+                       planes, the re-written canonical bytes, quantisation of
+                       half-way and out-of-range samples, and the byte offsets
+                       of parse errors for malformed headers.
   config_<k>.npz    -- for each BASELINE config: sampled pixel positions and
                        the reference output there.  Configs 1, 2 and frames
                        of 4 are full reference runs; configs 3 and 5 use crops
@@ -172,11 +177,50 @@ def make_config(cfg_id: int, path: str, pool) -> None:
     print(f"cfg{cfg_id}: {time.time() - t0:.1f}s -> {path}", flush=True)
 
 
+sys.path.insert(0, os.path.dirname(HERE))
+from pnm_bad_cases import PNM_BAD  # noqa: E402  (shared with tests/test_pnm_cli.py)
+
+
+def make_pnm(path: str) -> None:
+    from trigbf import pnm as rpnm
+
+    rng = np.random.default_rng(77)
+    out = {}
+    good = [
+        b"P5\n# comment\n3 2\n255\n" + bytes(rng.integers(0, 256, 6, dtype=np.uint8)),
+        b"P5 4\t1 #x\n255\r" + bytes(rng.integers(0, 256, 4, dtype=np.uint8)),
+        b"P6\n2 2\n255\n" + bytes(rng.integers(0, 256, 12, dtype=np.uint8)),
+    ]
+    for i, data in enumerate(good):
+        img = rpnm.read_pnm(data)
+        out[f"good{i}_in"] = np.frombuffer(data, np.uint8)
+        out[f"good{i}_planes"] = img.samples
+        out[f"good{i}_out"] = np.frombuffer(rpnm.write_pnm(img), np.uint8)
+    # quantisation: halves, negatives, out of range
+    q = np.array([[[-0.5, 0.49999, 0.5, 1.5, 2.5, 254.5, 255.4, 300.0, -7.0, 127.5]]])
+    img = trigbf.Image(10, 1, 1, q)
+    out["quant_in"] = q
+    out["quant_out"] = np.frombuffer(rpnm.write_pnm(img), np.uint8)
+    offs = []
+    for data in PNM_BAD:
+        try:
+            rpnm.read_pnm(data)
+            offs.append(-1)
+        except trigbf.PnmParseError as e:
+            offs.append(e.offset)
+    out["bad_offsets"] = np.array(offs, np.int64)
+    np.savez_compressed(path, **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="", help="comma list of config ids to (re)generate")
     ap.add_argument("--small", action="store_true")
+    ap.add_argument("--pnm", action="store_true")
     args = ap.parse_args()
+    if args.pnm:
+        make_pnm(os.path.join(HERE, "pnm_cases.npz"))
+        print("pnm cases written")
     if args.small:
         make_small(os.path.join(HERE, "small_cases.npz"))
         print("small cases written")
