@@ -395,7 +395,7 @@ def main():
     z_shard = n_shard - nz_shard
     round_trip = 16 * nz_shard + 4 * z_shard  # one write (pass1) or one read (pass2) of the planes
     alg_kernel = {"pass1": (4 + round_trip) * px_rank, "pass2": (4 + round_trip) * px_rank,
-                  "reduce": 8 * px_rank, "transpose": 8 * px_rank, "range_check": 4 * px_rank,
+                  "reduce": 8 * px_rank, "transpose": 12 * px_rank, "range_check": 4 * px_rank,
                   "finalize": 12 * px_rank, "chain": 0}
     roofline = None
     if dom is not None:

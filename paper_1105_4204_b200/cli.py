@@ -4,10 +4,14 @@
     python -m paper_1105_4204_b200 filter in.pgm --output out.pgm --sigma-s 8 --sigma-r 20
     python -m paper_1105_4204_b200 compare in.pgm --sigma-s 3 --sigma-r 30
 
+    python -m paper_1105_4204_b200 bench --csv grid.csv
+
 Engines: ``trig`` (the constant-time filter; colour images go through one
 batched call, channels as frames) and ``direct`` (GPU brute force with the
-Gaussian range kernel).  The reference's ``poly`` engine and its ``bench``
-and ``kernel`` subcommands are not on the B200 path.  Exit codes as the
+Gaussian range kernel).  ``bench`` times the reference's grid (cli.py:178-223:
+sigma_s 10/100 x sigma_r 10..100 on a 720x540 seeded noise image, the
+paper's Table setting) through the public call, host image in and out.  The
+reference's ``poly`` engine and ``kernel`` subcommand are not on the B200 path.  Exit codes as the
 reference: 0 ok, 1 usage/parameter error, 2 I/O or PNM parse error.
 Outputs are written to a temporary file and renamed into place.
 """
@@ -19,6 +23,8 @@ import os
 import sys
 import tempfile
 import time
+
+import numpy as np
 
 from .engines import EngineDiagnostics, bilateral_color, bilateral_direct, bilateral_trig, bilateral_trig_color
 from .errors import NativeUnavailableError, ParameterError, PnmParseError, TrigbfError
@@ -106,12 +112,66 @@ def cmd_compare(args) -> int:
     return OK
 
 
+NOISE_SEED = 20260515  # the reference's synthetic benchmark image (bench.py:12-21)
+
+
+def synthesize_noise(width: int = 720, height: int = 540, seed: int = NOISE_SEED) -> Image:
+    """Seeded uniform byte noise, the reference CLI's default bench input."""
+    px = np.random.default_rng(seed).integers(0, 256, size=(1, height, width))
+    return Image(width, height, 1, px.astype(np.float64))
+
+
+def _median_ms(fn, reps: int) -> float:
+    ts = []
+    for _ in range(max(1, reps)):
+        t0 = time.perf_counter()
+        fn()
+        ts.append((time.perf_counter() - t0) * 1e3)
+    return float(np.median(ts))
+
+
+def cmd_bench(args) -> int:
+    if args.engine == "poly":
+        print("tbf: error: the poly engine is not on the B200 path (use trig or direct)", file=sys.stderr)
+        return USAGE
+    img = _read(args.input) if args.input else synthesize_noise()
+    if img.channels == 3:
+        img = img.channel(0)
+    rows = []
+    if args.engine == "trig":
+        kind = SpatialKind(args.spatial)
+        for sigma_s in (10.0, 100.0):
+            spatial = SpatialSpec(kind, sigma_s=sigma_s, radius=round(sigma_s))
+            for sigma_r in (10.0, 20.0, 30.0, 40.0, 50.0, 60.0, 70.0, 80.0, 90.0, 100.0):
+                k = make_trig_kernel(sigma_r, args.range_max, degree=args.degree)
+                bilateral_trig(img, spatial, k)  # plan + workspace (cached)
+                ms = _median_ms(lambda: bilateral_trig(img, spatial, k), args.reps)
+                rows.append((sigma_s, sigma_r, k.N, "trig", ms))
+    else:
+        rng = GaussianRange(args.sigma_r)
+        for sigma_s in (3.0, 5.0, 10.0):
+            spatial = SpatialSpec.gaussian_fir(sigma_s)
+            bilateral_direct(img, spatial, rng)
+            ms = _median_ms(lambda: bilateral_direct(img, spatial, rng), args.reps)
+            rows.append((sigma_s, args.sigma_r, 0, "direct", ms))
+    lines = ["sigma_s,sigma_r,N,engine,median_ms"]
+    lines += [f"{a:g},{b:g},{n},{e},{ms:.3f}" for a, b, n, e, ms in rows]
+    text = "\n".join(lines) + "\n"
+    if args.csv in (None, "-"):
+        sys.stdout.write(text)
+    else:
+        _write_atomic(args.csv, text.encode("ascii"))
+    print(f"bench done: engine={args.engine} reps={args.reps} backend=b200-sm100a", file=sys.stderr)
+    return OK
+
+
 def build_parser() -> argparse.ArgumentParser:
     p = _Parser(prog="tbf", description="B200 constant-time bilateral filter")
     sub = p.add_subparsers(dest="command", required=True)
 
-    def common(sp):
-        sp.add_argument("input", help="binary PGM/PPM input")
+    def common(sp, needs_input=True):
+        if needs_input:
+            sp.add_argument("input", help="binary PGM/PPM input")
         sp.add_argument("--sigma-s", type=float, default=15.0, dest="sigma_s")
         sp.add_argument("--sigma-r", type=float, default=80.0, dest="sigma_r")
         sp.add_argument("--range-max", type=float, default=255.0, dest="range_max")
@@ -130,6 +190,13 @@ def build_parser() -> argparse.ArgumentParser:
     c.add_argument("--reference-range", choices=["gaussian", "cosine"], default="gaussian",
                    dest="reference_range")
     c.set_defaults(func=cmd_compare)
+    b = sub.add_parser("bench", help="wall-time grid (CSV)")
+    common(b, needs_input=False)
+    b.add_argument("input", nargs="?", default=None, help="optional PNM (default: 720x540 noise)")
+    b.add_argument("--engine", choices=["direct", "trig", "poly"], default="trig")
+    b.add_argument("--reps", type=int, default=5)
+    b.add_argument("--csv", default=None, help="CSV path (default stdout)")
+    b.set_defaults(func=cmd_bench)
     return p
 
 
@@ -143,6 +210,8 @@ def _check(args) -> None:
         raise ParameterError("--terms must be >= 1")
     if args.degree is not None and args.degree < 0:
         raise ParameterError("--degree must be >= 0")
+    if getattr(args, "reps", 1) < 1:
+        raise ParameterError("--reps must be >= 1")
 
 
 def main(argv=None) -> int:

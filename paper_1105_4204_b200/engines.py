@@ -123,6 +123,7 @@ class TrigFilter:
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.counters = torch.zeros(2, dtype=torch.int64, device=self.device)
         self._io = None  # device input/output of run_host, allocated on first use
+        self._pin = None  # pinned host staging (in, out) for pageable callers
 
     # -- sizing -----------------------------------------------------------
     def workspace_bytes(self, batch_terms: int) -> int:
@@ -205,6 +206,36 @@ class TrigFilter:
             self.workspace.data_ptr(), self.workspace.numel(), self.counters.data_ptr(), stream)
         _native.check(rc)
         return h_out
+
+    PIN_LIMIT = 1 << 32  # bytes per staging buffer; larger inputs copy pageable
+
+    def run_staged(self, src, dst):
+        """Pageable host arrays (NumPy, any float dtype; e.g. an Image's fp64
+        planes) through pinned staging buffers cached in the plan: a
+        multi-threaded dtype-converting copy into pinned memory, the
+        strip/band-overlapped host entry, and a multi-threaded copy back into
+        ``dst``.  Synchronous; returns (samples out of range, guarded)."""
+        torch = _torch()
+        n = self.B * self.H * self.W
+        if src.size != n or dst.size != n:
+            raise DimensionError(f"host arrays must hold {n} samples")
+        if 4 * n > self.PIN_LIMIT:
+            s32 = np.ascontiguousarray(src, dtype=np.float32)
+            o32 = dst if (dst.dtype == np.float32 and dst.flags.c_contiguous) else np.empty(s32.shape, np.float32)
+            self.run_host(s32, o32)
+            counts = self.read_counters()
+            if o32 is not dst:
+                np.copyto(dst, o32.reshape(dst.shape))
+            return counts
+        if self._pin is None:
+            self._pin = (torch.empty(n, dtype=torch.float32, pin_memory=True),
+                         torch.empty(n, dtype=torch.float32, pin_memory=True))
+        pin_in, pin_out = self._pin
+        pin_in.copy_(torch.from_numpy(np.ascontiguousarray(src).reshape(-1)))
+        self.run_host(pin_in, pin_out)
+        counts = self.read_counters()  # syncs: pin_out is complete
+        torch.from_numpy(dst.reshape(-1)).copy_(pin_out)
+        return counts
 
     def partial(self, f, num, den, accumulate: bool = False):
         """num/den (+)= contribution of this plan's term range (sharded path)."""
@@ -342,8 +373,8 @@ def bilateral_trig(img, spatial, kernel, *, workers: int = 1,
         diagnostics.degree = kernel.N
         diagnostics.workers = workers
 
-    def _finish(plan, shape, lo_hi):
-        bad, guarded = plan.read_counters()  # syncs: results and counters are ready
+    def _finish(plan, shape, lo_hi, counts=None):
+        bad, guarded = plan.read_counters() if counts is None else counts  # (syncs)
         if bad:
             lo, hi = lo_hi()
             raise ParameterError(
@@ -357,20 +388,22 @@ def bilateral_trig(img, spatial, kernel, *, workers: int = 1,
     if isinstance(img, Image):
         if img.channels != 1:
             raise DimensionError(f"engine expects a single-channel image, got {img.channels} channels")
-        host = np.ascontiguousarray(img.samples[0], dtype=np.float32)
+        host = img.samples[0]  # fp64 planes: converted inside the staging copy
         shape = (1, img.height, img.width)
         plan = get_plan(shape, spatial, kernel)
-        res = plan.run_host(host, np.empty_like(host))
-        _finish(plan, shape, lambda: (float(host.min()), float(host.max())))
-        return Image(img.width, img.height, 1, res.astype(np.float64))
+        res = np.empty((1, img.height, img.width), dtype=np.float64)
+        counts = plan.run_staged(host, res)
+        _finish(plan, shape, lambda: (float(host.min()), float(host.max())), counts)
+        return Image(img.width, img.height, 1, res)
     if isinstance(img, np.ndarray):
-        host = np.ascontiguousarray(img, dtype=np.float32)
-        if host.ndim not in (2, 3):
-            raise DimensionError(f"expected [H, W] or [B, H, W], got shape {host.shape}")
+        if img.ndim not in (2, 3):
+            raise DimensionError(f"expected [H, W] or [B, H, W], got shape {img.shape}")
+        host = img if img.dtype in (np.float32, np.float64) else img.astype(np.float32)
         shape = (1, *host.shape) if host.ndim == 2 else host.shape
         plan = get_plan(shape, spatial, kernel)
-        res = plan.run_host(host, np.empty_like(host))
-        _finish(plan, shape, lambda: (float(host.min()), float(host.max())))
+        res = np.empty(host.shape, dtype=np.float32)
+        counts = plan.run_staged(host, res)
+        _finish(plan, shape, lambda: (float(host.min()), float(host.max())), counts)
         return res
     if not isinstance(img, torch.Tensor):
         raise DimensionError(f"unsupported input type {type(img).__name__}")

@@ -82,3 +82,7 @@ def test_cli_filter_on_gpu(tmp_path, capsys):
     assert cli.main(["filter", str(rgb), "--output", str(tmp_path / "o.ppm"), "--engine", "direct",
                      "--spatial", "box", "--sigma-s", "1"]) == 0
     assert tb.read_pnm((tmp_path / "o.ppm").read_bytes()).channels == 3
+    csv = tmp_path / "grid.csv"
+    assert cli.main(["bench", str(src), "--reps", "1", "--csv", str(csv)]) == 0
+    rows = csv.read_text().splitlines()
+    assert rows[0] == "sigma_s,sigma_r,N,engine,median_ms" and len(rows) == 21
