@@ -6,10 +6,12 @@
 //
 // Pipeline per term batch (see DESIGN.md for the derivation and roofline):
 //
-//   k_pass1_gauss  one warp = 32 adjacent columns x one group of G1 terms.
-//                  The four auxiliary planes of each term (cos, sin, f*cos,
-//                  f*sin of nu*f) are generated in registers from f and run
-//                  through the forward/backward biquad cascade along y.  The
+//   k_transpose    f -> fT (x-major, for pass 2) and fY (tile-major, for
+//                  pass 1), fused with the input range check.
+//   k_pass1_gauss  one warp = 32 adjacent columns x one term.  The four
+//                  auxiliary planes of the term (cos, sin, f*cos, f*sin of
+//                  nu*f) are generated in registers from f and run through
+//                  the forward/backward biquad cascade along y.  The
 //                  causal->anticausal dependency is broken with per-32-row
 //                  checkpoints of the forward state (phase A) and a segment-
 //                  wise recompute into shared memory (phase B).  The segment
@@ -17,14 +19,17 @@
 //                  zero-state forward recursion along x is run over the 32
 //                  columns of the tile ("tile-local forward"), which is what is
 //                  written to HBM (one fp32 round trip of the 4 planes).
-//   k_chain        per (row, plane): chains the 4-state carries of the tiles
-//                  along x (s' = M s + L), handles the mirrored x-extension,
-//                  and produces the backward start state.
-//   k_pass2_gauss  one thread = one row x G2 terms, tiles right to left:
-//                  exact forward output = tile-local + H[m] . carry, then the
-//                  backward cascade, demodulation and num/den accumulation in
-//                  registers (fused; no second round trip).
-//   k_reduce       folds the per-group partial num/den, transposes back to
+//   k_chain        per (row, term): chains the 4-state carries of the tiles
+//                  along x (s' = M s + L), handles the mirrored x-extension
+//                  (the right one in closed form), and produces the backward
+//                  start state.
+//   k_pass2_gr     one warp = 32 rows x G2 terms, 4 warps (term groups) per
+//                  block, tiles right to left: exact forward output =
+//                  tile-local + H[m] . carry, then the backward cascade,
+//                  demodulation and num/den accumulation in registers; the
+//                  block sums its 4 groups in shared memory (fixed order).
+//                  (k_pass2_gauss / _async / _tma: per-group variants, options)
+//   k_reduce       folds the per-block partial num/den, transposes back to
 //                  row-major and applies the guarded ratio (engines.py:109-117).
 //
 // No tensor cores: the path is a set of first/second-order linear
@@ -528,8 +533,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     // forward code (instruction-cache footprint); phase A also writes the
     // tile, which is harmless.  f and checkpoints are prefetched one step ahead.
     float p1[4], p2[4], q1[4], q2[4];
-    // F_loc layout: float4 [term][b][row block of 128][x][128 rows] (row-block
-    // tiled so pass 2 streams each block's rows contiguously along x)
+    // F_loc layout: float4 [term][b][row block of 32][x][32 rows] (row-block
+    // tiled so a pass-2 warp streams its rows contiguously along x)
     const int nrbk = (H + FL_RB - 1) / FL_RB;
     float4* const fl0 = reinterpret_cast<float4*>(a.floc) + ((size_t)term * a.B + b) * nrbk * W * (size_t)FL_RB;
     float4* const ed0 = reinterpret_cast<float4*>(a.edge) + ((size_t)term * a.B + b) * a.ne * (size_t)H;
@@ -2091,7 +2096,7 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     size_t q = 0;
     L->s_ckpt = q;
     if (!box) q = align_up(q + (size_t)L->nyc * L->nseg * tb * 16 * B * W * 4);
-    L->s_floc = q;  // gauss: row-block tiled (padded to whole 128-row blocks); box: planar
+    L->s_floc = q;  // row-block tiled like xm_index (padded to whole FL_RB-row blocks)
     q = align_up(q + (size_t)tb * 4 * B * W * ((size_t)(H + FL_RB - 1) / FL_RB * FL_RB) * 4);
     L->s_lc = q;
     if (!box) q = align_up(q + (size_t)tb * 16 * B * L->ntx * H * 4);

@@ -1,0 +1,24 @@
+"""e2e of the frame-streamed path (config 4) vs sub-batch size (development aid)."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_1105_4204_b200 as tb
+from paper_1105_4204_b200 import workloads
+from paper_1105_4204_b200.engines import _bilateral_trig_streamed
+
+cfg = workloads.CONFIGS[4]
+host = workloads.make_input(cfg)
+pin = torch.from_numpy(host).pin_memory()
+k = tb.make_trig_kernel(cfg.sigma_r, cfg.T)
+spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
+for sub in (8, 4, 2, 16):
+    for _ in range(2):
+        _bilateral_trig_streamed(pin, spec, k, None, sub=sub)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        t = time.perf_counter()
+        _bilateral_trig_streamed(pin, spec, k, None, sub=sub)
+        ts.append(time.perf_counter() - t)
+    ms = 1e3 * float(np.median(ts))
+    print(f"sub {sub:2d}: {ms:.2f} ms  {cfg.pixels / ms / 1e3:.0f} Mpx/s", flush=True)
