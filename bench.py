@@ -354,30 +354,45 @@ def main():
     torch.cuda.synchronize(dev)
     bad, guarded = counters_plan.read_counters()
 
-    # ---- timed region ----
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
-        barrier()
-        torch.cuda.synchronize(dev)
-        wall0 = time.perf_counter()
-        with _native.KernelProfiler() as prof:
-            for i in range(args.steps):
-                flush.zero_()
-                evs[i][0].record(stream)
-                step()
-                evs[i][1].record(stream)
+    # ---- timed region (re-measured once if the clocks were throttled) ----
+    def timed_region():
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        with ClockSampler(local) as clk:
+            barrier()
             torch.cuda.synchronize(dev)
-        barrier()
-        wall = time.perf_counter() - wall0
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    t_rank = sum(step_ms) / 1e3
-    if world > 1:
-        tt = torch.tensor([t_rank], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_job = float(tt.item())
-    else:
-        t_job = t_rank
+            wall0 = time.perf_counter()
+            with _native.KernelProfiler() as prof:
+                for i in range(args.steps):
+                    flush.zero_()
+                    evs[i][0].record(stream)
+                    step()
+                    evs[i][1].record(stream)
+                torch.cuda.synchronize(dev)
+            barrier()
+            wall = time.perf_counter() - wall0
+        t_rank = sum(a.elapsed_time(b) for a, b in evs) / 1e3
+        if world > 1:
+            tt = torch.tensor([t_rank], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_rank = float(tt.item())
+        return t_rank, wall, clk, prof
+
+    def throttled(clk) -> bool:
+        c = clk.summary()
+        hot = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(c["reasons"])
+        stuck = (c["sm_mhz"] is not None and c["sm_max_mhz"] and not c["reasons"]
+                 and c["sm_mhz"] < 0.8 * c["sm_max_mhz"])
+        flag = torch.tensor([1.0 if (hot or stuck) else 0.0], device=dev)
+        if world > 1:
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        return bool(flag.item())
+
+    t_job, wall, clk, prof = timed_region()
+    remeasured = False
+    if throttled(clk):
+        t_job, wall, clk, prof = timed_region()
+        remeasured = True
     bad2, guarded2 = counters_plan.read_counters()
     if bad or bad2:
         raise SystemExit(f"range violations in benchmark input: {bad + bad2}")
@@ -426,6 +441,17 @@ def main():
                     for k, v in kt.items()}
     launches_total = sum(v[1] for v in kt.values())
 
+    # ---- compute-side view of the dominant kernel: pass 1 is neither HBM- nor
+    # FP32-throughput-bound; algorithmic FP32 work = 4 sweeps
+    # (y forward twice, y backward, x-local forward) x 4 planes x 4 FMA per
+    # pixel-term, against 148 SMs x 128 lanes x 2 flop x the sampled SM clock
+    fp32 = None
+    if dom == "pass1" and "pass1" in kt:
+        ms_total, launches = kt["pass1"]
+        flop = 2 * 64 * n_shard * px_rank * args.steps
+        ach_t = flop / (ms_total / 1e3) / 1e12
+        fp32 = {"kernel": "pass1", "algorithmic_flop_per_px_term": 128,
+                "achieved": round(ach_t, 2), "unit": "TFLOP/s"}
     # ---- e2e through the public API with pinned host buffers ----
     e2e = None
     if not args.no_e2e and mode != "terms":
@@ -456,6 +482,10 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": repr(e)}
 
     if rank == 0:
+        clocks = clk.summary()
+        if fp32 is not None and clocks.get("sm_max_mhz"):
+            fp32["peak"] = round(148 * 128 * 2 * clocks["sm_max_mhz"] / 1e6, 1)  # non-tensor FP32
+            fp32["frac"] = round(fp32["achieved"] / fp32["peak"], 4)
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
@@ -469,11 +499,12 @@ def main():
                        "l2": f"flushed before each timed step ({args.flush_mb} MiB write, outside the step events)"},
             "roofline": roofline,
             "pipeline_roofline": pipeline,
+            "fp32_pass1": fp32,
             "kernels": kernel_share,
             "gpu_launches": launches_total,
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "clocks": clk.summary(),
+            "clocks": dict(clocks, remeasured=remeasured),
             "wall_s_timed_region": round(wall, 4),
             "guarded_pixels_per_step": guarded2 // max(1, args.steps),
         }

@@ -205,6 +205,23 @@ def test_workers_and_repeats_bit_identical(tb):
     assert np.array_equal(a, b) and np.array_equal(a, c)
 
 
+def test_full_size_runs_bit_identical(tb):
+    """Determinism at the config-2 size, through both entries: repeated device
+    calls, a fresh plan, and the pinned host entry give the same bits (fixed
+    term order, fixed-shape block sums, no float atomics)."""
+    from paper_1105_4204_b200 import workloads
+
+    cfg = workloads.CONFIGS[2]
+    f = torch.from_numpy(workloads.frame(cfg, 0)).cuda()
+    k = tb.make_trig_kernel(cfg.sigma_r)
+    spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
+    a = tb.bilateral_trig(f, spec, k).clone()
+    b = tb.bilateral_trig(f, spec, k)
+    c = tb.TrigFilter(tuple(f.shape), spec, k)(f)
+    d = tb.bilateral_trig(f.cpu().pin_memory(), spec, k)
+    assert torch.equal(a, b) and torch.equal(a, c) and torch.equal(a.cpu(), d)
+
+
 def test_edge_sharper_than_blur(tb, orc):
     # test_engines.py:186-198
     plane = np.where(np.arange(40) < 20, 0.0, 200.0)[None, :].repeat(40, axis=0).astype(np.float32)
