@@ -2266,6 +2266,22 @@ void set_p1_smem() {
 // Core driver: pairs [tbeg, tend) in batches of L.tb terms.  Either
 // accumulates into caller num/den (row-major), or (out != null) writes the
 // guarded ratio.
+// Split [0, n) into k parts with quadratically growing (grow = true) or
+// shrinking sizes: the first input strip / last output band are small, so
+// the copies left exposed at the two ends of the host pipeline are short.
+std::vector<int> quad_split(int n, int k, bool grow) {
+    std::vector<int> b{0};
+    k = std::max(1, std::min(k, n));
+    for (int i = 1; i < k; ++i) {
+        const double u = (double)i / k;
+        const double frac = grow ? u * u : 1.0 - (1.0 - u) * (1.0 - u);
+        const int v = std::max(b.back() + 1, std::min(n - (k - i), (int)std::lround(frac * n)));
+        b.push_back(v);
+    }
+    b.push_back(n);
+    return b;
+}
+
 // Host-buffer I/O of tbf_bilateral_trig_host: f and out are device buffers,
 // h_f / h_out the caller's host arrays.
 struct HostIO {
@@ -2326,7 +2342,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
     // in pass 1), the range check and transpose once the whole input is in
     const bool hpipe = hio && !box && L.nslot == 1 && out;
     std::vector<cudaEvent_t> ev_strip;
-    int tps = L.ntx;  // column tiles per strip
+    std::vector<int> sb{0, L.ntx};  // strip boundaries in column tiles
     cudaEvent_t e_ready = nullptr;
     if (hio) {
         cudaStream_t sh = aux_stream(1);
@@ -2334,14 +2350,11 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         e_ready = event_get();
         cudaEventRecord(e_ready, st);  // term table queued, earlier users of f done
         cudaStreamWaitEvent(sh, e_ready, 0);
-        if (hpipe) {
-            const int ns = std::max(1, std::min(hio->strips, L.ntx));
-            tps = (L.ntx + ns - 1) / ns;
-        }
+        if (hpipe) sb = quad_split(L.ntx, hio->strips, true);
         float* df = const_cast<float*>(f);
-        for (int t0 = 0; t0 < L.ntx; t0 += tps) {
-            const int x0 = t0 * TILE;
-            const int cols = std::min(W, (t0 + tps) * TILE) - x0;
+        for (size_t s = 0; s + 1 < sb.size(); ++s) {
+            const int x0 = sb[s] * TILE;
+            const int cols = std::min(W, sb[s + 1] * TILE) - x0;
             cudaMemcpy2DAsync(df + x0, (size_t)W * 4, hio->h_f + x0, (size_t)W * 4, (size_t)cols * 4,
                               (size_t)B * H, cudaMemcpyHostToDevice, sh);
             ev_strip.push_back(event_get());
@@ -2433,8 +2446,8 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 cudaStream_t ps = aux_stream(2 + (int)(s & 1));
                 cudaStreamWaitEvent(ps, e_ready, 0);
                 cudaStreamWaitEvent(ps, ev_strip[s], 0);
-                p1.tile0 = (int)s * tps;
-                p1.ntx_run = std::min(tps, L.ntx - p1.tile0);
+                p1.tile0 = sb[s];
+                p1.ntx_run = sb[s + 1] - sb[s];
                 {
                     dim3 tg(p1.ntx_run, (H + TILE - 1) / TILE, B);
                     Prof pr(KK_TRANSPOSE, ps);
@@ -2614,20 +2627,20 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         if (hpipe && last && hio->bands > 1 && nrb > 1) {
             // row bands on alternating streams; each band's rows go back to the
             // host while the next band filters
-            const int nbd = std::min(hio->bands, nrb);
-            const int rpb = (nrb + nbd - 1) / nbd;
+            const std::vector<int> bb = quad_split(nrb, hio->bands, false);  // in 128-row blocks
             cudaStream_t sd = aux_stream(4);
             cudaEvent_t e_c = event_get();
             cudaEventRecord(e_c, s2);  // chain and everything before it
-            for (int rb0 = 0, k = 0; rb0 < nrb; rb0 += rpb, ++k) {
-                cudaStream_t q = aux_stream(2 + (k & 1));
+            for (size_t k = 0; k + 1 < bb.size(); ++k) {
+                const int rb0 = bb[k], nrun = bb[k + 1] - bb[k];
+                cudaStream_t q = aux_stream(2 + (int)(k & 1));
                 cudaStreamWaitEvent(q, e_c, 0);
-                if ((rc = pass2_reduce(rb0, std::min(rpb, nrb - rb0), q))) return rc;
+                if ((rc = pass2_reduce(rb0, nrun, q))) return rc;
                 cudaEvent_t e_r = event_get();
                 cudaEventRecord(e_r, q);
                 cudaStreamWaitEvent(sd, e_r, 0);
                 const int r0 = rb0 * P2_THREADS;
-                const int r1 = std::min(H, (rb0 + rpb) * P2_THREADS);
+                const int r1 = std::min(H, (rb0 + nrun) * P2_THREADS);
                 cudaMemcpy2DAsync(hio->h_out + (size_t)r0 * W, (size_t)H * W * 4, out + (size_t)r0 * W,
                                   (size_t)H * W * 4, (size_t)(r1 - r0) * W * 4, B, cudaMemcpyDeviceToHost, sd);
             }

@@ -13,8 +13,8 @@ k = tb.make_trig_kernel(cfg.sigma_r, cfg.T)
 spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
 plan = tb.get_plan(tuple(pin.shape), spec, k)
 lib = _native.load()
-for strips in (1, 2, 4, 8, 16):
-    for bands in (1, 4, 8, 16):
+for strips in (0, 2, 3, 4, 6, 8):
+    for bands in (0, 2, 3, 4, 6, 8):
         lib.tbf_set_option(_native.TBF_OPT_HOST_STRIPS, strips)
         lib.tbf_set_option(_native.TBF_OPT_HOST_BANDS, bands)
         ts = []
