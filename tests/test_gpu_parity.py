@@ -205,6 +205,19 @@ def test_workers_and_repeats_bit_identical(tb):
     assert np.array_equal(a, b) and np.array_equal(a, c)
 
 
+@pytest.mark.parametrize("T,sigma_r,sigma_s", [(1.0, 0.08, 3.0), (4095.0, 300.0, 5.0), (255.0, 12.0, 1.5)])
+def test_other_intensity_ranges_match_oracle(tb, orc, T, sigma_r, sigma_s):
+    """Normalised (T=1) and 12-bit (T=4095) inputs: same relative tolerance
+    1e-3*T against the float64 oracle (the phase range and the fold
+    condition depend on T)."""
+    rng = np.random.default_rng(int(T))
+    f = (rng.uniform(0, 1, (70, 90)) * T).astype(np.float32)
+    k = tb.make_trig_kernel(sigma_r, T)
+    got = tb.bilateral_trig(f, tb.SpatialSpec.gaussian_recursive(sigma_s), k)
+    ref, _ = orc.bilateral_trig(f.astype(np.float64), "gauss-recursive", sigma_s, orc.make_trig_kernel(sigma_r, T))
+    assert np.max(np.abs(got - ref)) <= 1e-3 * T, (T, np.max(np.abs(got - ref)))
+
+
 def test_full_size_runs_bit_identical(tb):
     """Determinism at the config-2 size, through both entries: repeated device
     calls, a fresh plan, and the pinned host entry give the same bits (fixed
