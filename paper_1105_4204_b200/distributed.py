@@ -97,18 +97,22 @@ def bilateral_trig_term_sharded(f, spatial, kernel, *, partial_fn=None, finalize
     t0, t1 = term_range(pairs.count, pairs.has_zero, world, rank)
     num = torch.zeros_like(f)
     den = torch.zeros_like(f)
+    plan_for_checks = None
     if partial_fn is None or finalize_fn is None:
         from .engines import TrigFilter
 
         plan = TrigFilter(tuple(f.shape), spatial, kernel, term_range=(t0, t1)) if t1 > t0 else None
+        if plan is not None:
+            plan_for_checks = plan
+        elif rank == 0:  # the root finalises even without terms of its own
+            plan_for_checks = TrigFilter(tuple(f.shape), spatial, kernel)
 
         def partial_fn(f_, n_, d_, a, b):
             if plan is not None:
                 plan.partial(f_, n_, d_, accumulate=False)
 
         def finalize_fn(n_, d_, f_, o_):
-            fin = plan if plan is not None else TrigFilter(tuple(f.shape), spatial, kernel)
-            return fin.finalize(n_, d_, f_, o_)
+            return plan_for_checks.finalize(n_, d_, f_, o_)
 
     if t1 > t0:
         partial_fn(f, num, den, t0, t1)
@@ -117,4 +121,42 @@ def bilateral_trig_term_sharded(f, spatial, kernel, *, partial_fn=None, finalize
         return None
     out = torch.empty_like(f)
     finalize_fn(num, den, f, out)
+    if plan_for_checks is not None:
+        # engines.py:218-225 on the root's copy of the input (every rank holds
+        # the same f); read once, after the filter (one sync)
+        plan_for_checks.range_check(f)
+        bad, _ = plan_for_checks.read_counters()
+        if bad:
+            from .errors import ParameterError
+
+            raise ParameterError(f"samples exceed the declared range [0, {kernel.T:g}]; "
+                                 "rescale the input or raise T")
     return out
+
+
+def bilateral_trig_frame_sharded(frames, spatial, kernel, *, gather: bool = False, group=None):
+    """Frame batches split across ranks with no collective (SURVEY 8(e),
+    config 4): rank r filters frames frame_range(B, world, r) of ``frames``
+    ([B, H, W], host or device; every rank passes the same batch).  Returns
+    this rank's filtered frames, or with ``gather=True`` the whole batch on
+    every rank (all_gather of equal-size shards, padded)."""
+    import torch
+    import torch.distributed as dist
+
+    from .engines import bilateral_trig
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    B = int(frames.shape[0])
+    f0, f1 = frame_range(B, world, rank)
+    mine = bilateral_trig(frames[f0:f1].contiguous(), spatial, kernel) if f1 > f0 else frames[0:0]
+    if not gather:
+        return mine
+    dev = torch.device("cuda", torch.cuda.current_device())
+    per = max(frame_range(B, world, r)[1] - frame_range(B, world, r)[0] for r in range(world))
+    buf = torch.zeros((per, *frames.shape[1:]), dtype=torch.float32, device=dev)
+    if f1 > f0:
+        buf[: f1 - f0].copy_(torch.as_tensor(mine).to(dev))
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    return torch.cat([parts[r][: frame_range(B, world, r)[1] - frame_range(B, world, r)[0]]
+                      for r in range(world)])

@@ -535,3 +535,38 @@ def test_host_entry_range_error(tb):
         tb.bilateral_trig(torch.from_numpy(f).pin_memory(), spec, k)
     ok = tb.bilateral_trig(np.clip(f, 0, 255), spec, k)  # the plan's counters were reset
     assert ok.shape == f.shape and np.isfinite(ok).all()
+
+
+def test_sharded_paths_over_nccl_world1(tb):
+    """The multi-GPU entry points over a real NCCL process group (world size
+    1 on this box): term sharding (partial + NCCL reduce + finalize) and frame
+    sharding (+ all_gather) reproduce the single-GPU filter.  Multi-rank
+    partitioning and the reduce arithmetic are covered by the gloo tests."""
+    import socket
+
+    import torch.distributed as dist
+    from paper_1105_4204_b200 import distributed as tdist
+    from paper_1105_4204_b200.workloads import rects_image
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        f = torch.from_numpy(rects_image(300, 260, 8, seed=4)).cuda()
+        k = tb.make_trig_kernel(15.0)
+        spec = tb.SpatialSpec.gaussian_recursive(6.0)
+        ref = tb.bilateral_trig(f, spec, k)
+        out = tdist.bilateral_trig_term_sharded(f[None], spec, k)
+        assert float((out[0] - ref).abs().max()) < 1e-3
+        frames = torch.stack([f, f.flip(0), f.flip(1)])
+        got = tdist.bilateral_trig_frame_sharded(frames, spec, k, gather=True)
+        assert got.shape == frames.shape
+        assert float((got[0] - ref).abs().max()) < 1e-3
+        bad = f[None].clone()
+        bad[0, 3, 4] = 1000.0
+        with pytest.raises(tb.ParameterError):
+            tdist.bilateral_trig_term_sharded(bad, spec, k)
+    finally:
+        dist.destroy_process_group()
