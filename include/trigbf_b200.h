@@ -159,6 +159,11 @@ TBF_API int tbf_profile_enable(int32_t on);
 TBF_API int32_t tbf_profile_kinds(void);
 TBF_API const char* tbf_kernel_name(int32_t kind);
 TBF_API int tbf_profile_collect(double* ms, long long* launches, int32_t n);
+/* Alternative to collect: the recorded launches in order, start offsets
+ * relative to the first one (ms), durations and kinds; returns the count
+ * (at most cap) and clears the records.  Host-entry copies are recorded as
+ * kinds "h2d" / "d2h". */
+TBF_API int32_t tbf_profile_timeline(double* start_ms, double* dur_ms, int32_t* kind, int32_t cap);
 
 /* Process-wide tuning options.
  *   TBF_OPT_PIPELINE (default 0): with several term batches, run pass 1 of

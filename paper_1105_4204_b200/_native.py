@@ -53,6 +53,7 @@ EXPORTS = (
     "tbf_profile_kinds",
     "tbf_kernel_name",
     "tbf_profile_collect",
+    "tbf_profile_timeline",
     "tbf_set_option",
 )
 ABI_VERSION = 1
@@ -135,6 +136,9 @@ def _declare(lib):
     lib.tbf_profile_kinds.argtypes = []
     lib.tbf_kernel_name.restype = ctypes.c_char_p
     lib.tbf_kernel_name.argtypes = [_i32]
+    lib.tbf_profile_timeline.restype = _i32
+    lib.tbf_profile_timeline.argtypes = [ctypes.POINTER(_f64), ctypes.POINTER(_f64),
+                                         ctypes.POINTER(_i32), _i32]
     lib.tbf_profile_collect.restype = ctypes.c_int
     lib.tbf_profile_collect.argtypes = [ctypes.POINTER(_f64), ctypes.POINTER(ctypes.c_longlong), _i32]
     lib.tbf_box_pass_f64.restype = ctypes.c_int

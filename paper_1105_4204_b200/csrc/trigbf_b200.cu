@@ -108,10 +108,11 @@ int check_cuda(const char* what) {
 // Optional per-kernel timing: CUDA events recorded on the launch stream around
 // every launch (tbf_profile_enable / tbf_profile_collect).
 enum KernelKind {
-    KK_TRANSPOSE = 0, KK_RANGE, KK_PASS1, KK_CHAIN, KK_PASS2, KK_REDUCE, KK_FINALIZE, KK_COUNT
+    KK_TRANSPOSE = 0, KK_RANGE, KK_PASS1, KK_CHAIN, KK_PASS2, KK_REDUCE, KK_FINALIZE, KK_H2D, KK_D2H,
+    KK_COUNT
 };
 const char* const kKernelNames[KK_COUNT] = {"transpose", "range_check", "pass1", "chain",
-                                            "pass2", "reduce", "finalize"};
+                                            "pass2", "reduce", "finalize", "h2d", "d2h"};
 
 struct ProfRec {
     int kind;
@@ -2355,8 +2356,11 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         for (size_t s = 0; s + 1 < sb.size(); ++s) {
             const int x0 = sb[s] * TILE;
             const int cols = std::min(W, sb[s + 1] * TILE) - x0;
-            cudaMemcpy2DAsync(df + x0, (size_t)W * 4, hio->h_f + x0, (size_t)W * 4, (size_t)cols * 4,
-                              (size_t)B * H, cudaMemcpyHostToDevice, sh);
+            {
+                Prof pr(KK_H2D, sh);
+                cudaMemcpy2DAsync(df + x0, (size_t)W * 4, hio->h_f + x0, (size_t)W * 4, (size_t)cols * 4,
+                                  (size_t)B * H, cudaMemcpyHostToDevice, sh);
+            }
             ev_strip.push_back(event_get());
             cudaEventRecord(ev_strip.back(), sh);
         }
@@ -2641,6 +2645,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 cudaStreamWaitEvent(sd, e_r, 0);
                 const int r0 = rb0 * P2_THREADS;
                 const int r1 = std::min(H, (rb0 + nrun) * P2_THREADS);
+                Prof pr(KK_D2H, sd);
                 cudaMemcpy2DAsync(hio->h_out + (size_t)r0 * W, (size_t)H * W * 4, out + (size_t)r0 * W,
                                   (size_t)H * W * 4, (size_t)(r1 - r0) * W * 4, B, cudaMemcpyDeviceToHost, sd);
             }
@@ -2721,6 +2726,30 @@ int tbf_set_option(int32_t option, int64_t value) {
 
 const char* tbf_kernel_name(int32_t kind) {
     return (kind >= 0 && kind < KK_COUNT) ? kKernelNames[kind] : "";
+}
+
+int32_t tbf_profile_timeline(double* start_ms, double* dur_ms, int32_t* kind, int32_t cap) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    int32_t n = 0;
+    cudaEvent_t t0 = g_prof.empty() ? nullptr : g_prof.front().a;
+    for (auto& r : g_prof) {
+        float t = 0.f, s0 = 0.f;
+        cudaEventSynchronize(r.b);
+        cudaEventElapsedTime(&t, r.a, r.b);
+        cudaEventElapsedTime(&s0, t0, r.a);
+        if (n < cap) {
+            start_ms[n] = s0;
+            dur_ms[n] = t;
+            kind[n] = r.kind;
+            ++n;
+        }
+    }
+    for (auto& r : g_prof) {
+        g_ev_pool.push_back(r.a);
+        g_ev_pool.push_back(r.b);
+    }
+    g_prof.clear();
+    return n;
 }
 
 int tbf_profile_collect(double* ms, long long* launches, int32_t n) {
