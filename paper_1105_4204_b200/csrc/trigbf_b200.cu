@@ -399,6 +399,7 @@ struct Pass2Args {
     const float* carry;   // chained carries float4 [n][B][ntx][H][4]
     const float* bstate;  // float4 [n][B][H][4]
     float* part;          // [ngroups*2][B][W][H]
+    int order;            // k_pass2_gr block order (TBF_OPT_P2_ORDER)
 };
 
 struct ReduceArgs {
@@ -1446,8 +1447,22 @@ __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_consta
     extern __shared__ float2 sdyn[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nsb = a.nrb_run * (P2_THREADS / 32);  // 32-row sub-blocks in this launch
-    const int chunk = blockIdx.x / nsb;
-    const int r0 = a.rb0 * P2_THREADS + (blockIdx.x % nsb) * 32;
+    const int nch = gridDim.x / nsb;
+    int chunk, rsb;
+    if (a.order == 1) {  // x-chunk fastest: both chunks of a row block together
+        chunk = blockIdx.x % nch;
+        rsb = blockIdx.x / nch;
+    } else if (a.order == 2) {  // rows reversed within a chunk
+        chunk = blockIdx.x / nsb;
+        rsb = nsb - 1 - blockIdx.x % nsb;
+    } else if (a.order == 3) {  // chunks reversed (rightmost, exact-start chunk first)
+        chunk = nch - 1 - blockIdx.x / nsb;
+        rsb = blockIdx.x % nsb;
+    } else {
+        chunk = blockIdx.x / nsb;
+        rsb = blockIdx.x % nsb;
+    }
+    const int r0 = a.rb0 * P2_THREADS + rsb * 32;
     const int H = a.H, W = a.W;
     if (r0 >= H) return;  // whole block
     const int i_raw = r0 + lane;
@@ -2017,6 +2032,7 @@ int g_p2_chunks = 0;    // tbf_set_option(TBF_OPT_P2_CHUNKS): 0 = automatic
 int g_pass2_tma = 3;    // tbf_set_option(TBF_OPT_PASS2_TMA): 0 register prefetch (G=2), 1/2 TMA producer warp, 3 auto (default), 4 cp.async G=4
 int g_pipeline = 0;     // tbf_set_option(TBF_OPT_PIPELINE) (measured: no gain on B200, SMs time-slice)
 int g_auto_batches = 2; // tbf_set_option(TBF_OPT_BATCHES): batches when batch_terms <= 0
+int g_p2_order = 1;     // tbf_set_option(TBF_OPT_P2_ORDER): block order of the block-summed pass 2 (1: x-chunk fastest, measured best)
 int g_host_strips = 0;  // tbf_set_option(TBF_OPT_HOST_STRIPS): column strips of the host input (0 auto)
 int g_host_bands = 0;   // tbf_set_option(TBF_OPT_HOST_BANDS): row bands of the host output (0 auto)
 
@@ -2540,6 +2556,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.carry = lc;
         p2.bstate = bst;
         p2.part = part;
+        p2.order = g_p2_order;
         // x-chunking of pass-2 rows when rows x groups cannot fill the GPU
         const int nrb = (H + P2_THREADS - 1) / P2_THREADS;
         int nchunk = 1;
@@ -2711,6 +2728,9 @@ int tbf_set_option(int32_t option, int64_t value) {
             return TBF_OK;
         case TBF_OPT_HOST_BANDS:
             g_host_bands = (int)std::max<int64_t>(0, std::min<int64_t>(64, value));
+            return TBF_OK;
+        case TBF_OPT_P2_ORDER:
+            g_p2_order = (int)std::max<int64_t>(0, std::min<int64_t>(3, value));
             return TBF_OK;
         case TBF_OPT_P1_FOLD:
             g_pass1_fold = value != 0;
