@@ -33,6 +33,7 @@ TBF_OPT_P1_FOLD = 6
 TBF_OPT_HOST_STRIPS = 7
 TBF_OPT_HOST_BANDS = 8
 TBF_OPT_P2_ORDER = 9
+TBF_OPT_P1_ORDER = 10
 
 TBF_SPATIAL_RECURSIVE = 0
 TBF_SPATIAL_BOX = 1

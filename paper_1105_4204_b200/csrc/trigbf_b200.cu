@@ -357,6 +357,7 @@ struct Pass1Args {
     int nyc, ych_rows, ywarm;  // y-chunks of ych_rows output rows; warm-up rows (mult. of 32)
     int Ex, ne, edge_all, ntx;
     int tile0, ntx_run;  // column tiles [tile0, tile0 + ntx_run) in this launch
+    int order, ngb;      // block order (TBF_OPT_P1_ORDER); term-group blocks
     Casc k;
     TermDev t;
     int ngroups;    // ceil(t.n / G1)
@@ -454,12 +455,30 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     extern __shared__ float smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int term = blockIdx.y * P1_WARPS + warp;
+    // block order (a.order): 0 column tile fastest, then y-chunk, term group;
+    // 1 term group fastest (the groups sharing a column tile's f run
+    // together), then column tile, y-chunk; 2 y-chunk fastest
+    int gblk, tile_r, chunk;
+    if (a.order == 1) {
+        int idx = blockIdx.x;
+        gblk = idx % a.ngb;
+        idx /= a.ngb;
+        tile_r = idx % a.ntx_run;
+        chunk = idx / a.ntx_run;
+    } else if (a.order == 2) {
+        chunk = blockIdx.x % a.nyc;
+        tile_r = blockIdx.x / a.nyc;
+        gblk = blockIdx.y;
+    } else {
+        tile_r = blockIdx.x % a.ntx_run;
+        chunk = blockIdx.x / a.ntx_run;
+        gblk = blockIdx.y;
+    }
+    const int term = gblk * P1_WARPS + warp;
     if (term >= a.t.n) return;  // whole warp; no block-level barriers below
     const int b = blockIdx.z;
     const int H = a.H, W = a.W;
-    const int tile_x = a.tile0 + blockIdx.x % a.ntx_run;
-    const int chunk = blockIdx.x / a.ntx_run;
+    const int tile_x = a.tile0 + tile_r;
     const int x0 = tile_x * TILE;
     const int x = x0 + lane;
     const bool xv = x < W;
@@ -2032,6 +2051,7 @@ int g_p2_chunks = 0;    // tbf_set_option(TBF_OPT_P2_CHUNKS): 0 = automatic
 int g_pass2_tma = 3;    // tbf_set_option(TBF_OPT_PASS2_TMA): 0 register prefetch (G=2), 1/2 TMA producer warp, 3 auto (default), 4 cp.async G=4
 int g_pipeline = 0;     // tbf_set_option(TBF_OPT_PIPELINE) (measured: no gain on B200, SMs time-slice)
 int g_auto_batches = 2; // tbf_set_option(TBF_OPT_BATCHES): batches when batch_terms <= 0
+int g_p1_order = -1;    // tbf_set_option(TBF_OPT_P1_ORDER): block order of pass 1 (-1 auto)
 int g_p2_order = 1;     // tbf_set_option(TBF_OPT_P2_ORDER): block order of the block-summed pass 2 (1: x-chunk fastest, measured best)
 int g_host_strips = 0;  // tbf_set_option(TBF_OPT_HOST_STRIPS): column strips of the host input (0 auto)
 int g_host_bands = 0;   // tbf_set_option(TBF_OPT_HOST_BANDS): row bands of the host output (0 auto)
@@ -2458,6 +2478,15 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p1.lcarry = lc;
         p1.edge = edge;
         dim3 g1(L.ntx * (box ? 1 : L.nyc), (p1.ngroups + P1_WARPS - 1) / P1_WARPS, B);
+        p1.ngb = (int)g1.y;
+        // automatic: term groups fastest when many groups share a column
+        // tile's f (measured: -2.1% on config 3 with 34 groups, flat with 9,
+        // +0.3% with 6)
+        p1.order = box ? 0 : (g_p1_order >= 0 ? g_p1_order : (p1.ngb >= 12 ? 1 : 0));
+        auto p1grid = [&](int ntx_run) {  // launch shape for the block order
+            return p1.order == 1 ? dim3(ntx_run * L.nyc * p1.ngb, 1, B) : dim3(ntx_run * L.nyc, p1.ngb, B);
+        };
+        if (!box) g1 = p1grid(L.ntx);
         const int p1smem = g_p1_occ == 2 ? P1_SMEM_OCC2 : P1_SMEM;
         if (strip_p1 && bi == 0) {
             // strip s on alternating streams, after its copy: transpose (+
@@ -2473,7 +2502,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                     Prof pr(KK_TRANSPOSE, ps);
                     k_transpose<<<tg, 256, 0, ps>>>(f, fT, fY, H, W, -1e-9, terms->T + 1e-9, rc_counters, p1.tile0);
                 }
-                dim3 gs(p1.ntx_run * L.nyc, g1.y, B);
+                dim3 gs = p1grid(p1.ntx_run);
                 {
                     Prof pr(KK_PASS1, ps);
                     if (fold)
@@ -2728,6 +2757,9 @@ int tbf_set_option(int32_t option, int64_t value) {
             return TBF_OK;
         case TBF_OPT_HOST_BANDS:
             g_host_bands = (int)std::max<int64_t>(0, std::min<int64_t>(64, value));
+            return TBF_OK;
+        case TBF_OPT_P1_ORDER:
+            g_p1_order = (int)std::max<int64_t>(-1, std::min<int64_t>(2, value));
             return TBF_OK;
         case TBF_OPT_P2_ORDER:
             g_p2_order = (int)std::max<int64_t>(0, std::min<int64_t>(3, value));

@@ -11,9 +11,9 @@ f = torch.from_numpy(workloads.make_input(cfg, frames=min(cfg.frames, 8))).cuda(
 k = tb.make_trig_kernel(cfg.sigma_r, cfg.T)
 spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
 flush = torch.empty(128 << 20, device="cuda")
-variants = [("default", {}), ("order1", {9: 1}), ("order2", {9: 2}), ("order3", {9: 3})]
+variants = [("default", {}), ("p1o1", {10: 1}), ("p1o2", {10: 2})]
 for name, opts in variants:
-    for o, v in {0: 0, 2: 3, 3: 0, 4: 3, 1: 2, 5: 0, 6: 1, 9: 1}.items():
+    for o, v in {0: 0, 2: 3, 3: 0, 4: 3, 1: 2, 5: 0, 6: 1, 9: 1, 10: -1}.items():
         lib.tbf_set_option(o, v)
     for o, v in opts.items():
         lib.tbf_set_option(o, v)
