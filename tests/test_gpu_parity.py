@@ -572,3 +572,63 @@ def test_sharded_paths_over_nccl_world1(tb):
             tdist.bilateral_trig_term_sharded(bad, spec, k)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shape,kind,param,sigma_r", [
+    ((1, 1, 1), "gauss-recursive", 3.0, 30.0),
+    ((1, 1, 37), "gauss-recursive", 2.0, 60.0),
+    ((1, 37, 1), "gauss-recursive", 2.0, 60.0),
+    ((1, 33, 65), "gauss-recursive", 8.0, 20.0),
+    ((2, 100, 200), "gauss-recursive", 5.0, 25.0),
+    ((1, 70, 45), "box", 0, 40.0),
+    ((1, 70, 45), "box", 9, 40.0),
+    ((3, 129, 257), "gauss-recursive", 16.0, 10.0),
+])
+def test_no_writes_outside_buffers(tb, shape, kind, param, sigma_r):
+    """Out-of-bounds write check without a sanitizer: every buffer handed to
+    the C ABI (workspace, output, counters, the host entry's device buffer)
+    sits between canary margins that must survive, and the const input must
+    be unchanged; odd shapes, batches, both spatial kinds."""
+    import ctypes
+
+    from paper_1105_4204_b200 import _native
+    from paper_1105_4204_b200.engines import _TermsHolder, spatial_struct
+
+    lib = _native.load()
+    B, H, W = shape
+    n = B * H * W
+    M = 1 << 16  # canary margin (bytes)
+    spec = _spec(tb, kind, param)
+    k = tb.make_trig_kernel(sigma_r, 255.0)
+    sp, terms = spatial_struct(spec), _TermsHolder(k)
+    wsb = lib.tbf_workspace_bytes(B, H, W, ctypes.byref(sp), 0, terms.struct.n_terms, 0)
+
+    def guarded(nbytes):
+        buf = torch.full((nbytes + 2 * M,), 0xA5, dtype=torch.uint8, device="cuda")
+        return buf, buf.data_ptr() + M
+
+    def intact(buf):
+        return bool((buf[:M] == 0xA5).all()) and bool((buf[-M:] == 0xA5).all())
+
+    f = torch.from_numpy(np.random.default_rng(n).uniform(0, 255, shape).astype(np.float32)).cuda()
+    f_copy = f.clone()
+    ws, ws_p = guarded(wsb)
+    out, out_p = guarded(4 * n)
+    ctr, ctr_p = guarded(16)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream().cuda_stream
+    _native.check(lib.tbf_bilateral_trig(f.data_ptr(), out_p, B, H, W, ctypes.byref(sp),
+                                         ctypes.byref(terms.struct), 0, ws_p, wsb, ctr_p, stream))
+    torch.cuda.synchronize()
+    assert intact(ws) and intact(out) and intact(ctr)
+    assert torch.equal(f, f_copy)
+    # the host entry with its device buffer
+    io, io_p = guarded(8 * n)
+    h_in = f.cpu().pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    _native.check(lib.tbf_bilateral_trig_host(h_in.data_ptr(), h_out.data_ptr(), B, H, W, ctypes.byref(sp),
+                                              ctypes.byref(terms.struct), 0, io_p, ws_p, wsb, ctr_p, stream))
+    torch.cuda.synchronize()
+    assert intact(ws) and intact(io) and intact(ctr)
+    dev_out = out[M:M + 4 * n].view(torch.float32).reshape(shape).cpu()
+    assert torch.equal(h_out, dev_out)
