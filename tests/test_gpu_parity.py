@@ -585,10 +585,11 @@ def test_sharded_paths_over_nccl_world1(tb):
     ((3, 129, 257), "gauss-recursive", 16.0, 10.0),
 ])
 def test_no_writes_outside_buffers(tb, shape, kind, param, sigma_r):
-    """Out-of-bounds write check without a sanitizer: every buffer handed to
+    """Out-of-bounds checks without a sanitizer: every buffer handed to
     the C ABI (workspace, output, counters, the host entry's device buffer)
     sits between canary margins that must survive, and the const input must
-    be unchanged; odd shapes, batches, both spatial kinds."""
+    be unchanged; a NaN-filled workspace must not change the result (no
+    reads of unwritten workspace); odd shapes, batches, both spatial kinds."""
     import ctypes
 
     from paper_1105_4204_b200 import _native
@@ -632,3 +633,12 @@ def test_no_writes_outside_buffers(tb, shape, kind, param, sigma_r):
     assert intact(ws) and intact(io) and intact(ctr)
     dev_out = out[M:M + 4 * n].view(torch.float32).reshape(shape).cpu()
     assert torch.equal(h_out, dev_out)
+    # reads of workspace that was never written: a NaN-filled workspace must
+    # give the same result (0xFF bytes are NaN as fp32)
+    ws[M:M + wsb].fill_(0xFF)
+    ctr[M:M + 16].zero_()
+    _native.check(lib.tbf_bilateral_trig(f.data_ptr(), out_p, B, H, W, ctypes.byref(sp),
+                                         ctypes.byref(terms.struct), 0, ws_p, wsb, ctr_p, stream))
+    torch.cuda.synchronize()
+    again = out[M:M + 4 * n].view(torch.float32).reshape(shape).cpu()
+    assert torch.isfinite(again).all() and torch.equal(again, dev_out)
