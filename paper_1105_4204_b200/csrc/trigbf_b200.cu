@@ -2052,7 +2052,7 @@ int g_pass2_tma = 3;    // tbf_set_option(TBF_OPT_PASS2_TMA): 0 register prefetc
 int g_pipeline = 0;     // tbf_set_option(TBF_OPT_PIPELINE) (measured: no gain on B200, SMs time-slice)
 int g_auto_batches = 2; // tbf_set_option(TBF_OPT_BATCHES): batches when batch_terms <= 0
 int g_p1_order = -1;    // tbf_set_option(TBF_OPT_P1_ORDER): block order of pass 1 (-1 auto)
-int g_p2_order = 1;     // tbf_set_option(TBF_OPT_P2_ORDER): block order of the block-summed pass 2 (1: x-chunk fastest, measured best)
+int g_p2_order = 0;     // tbf_set_option(TBF_OPT_P2_ORDER): block order of the block-summed pass 2 (same-box A/B: orders 0 and 1 equal)
 int g_host_strips = 0;  // tbf_set_option(TBF_OPT_HOST_STRIPS): column strips of the host input (0 auto)
 int g_host_bands = 0;   // tbf_set_option(TBF_OPT_HOST_BANDS): row bands of the host output (0 auto)
 

@@ -11,7 +11,7 @@ f = torch.from_numpy(workloads.make_input(cfg, frames=min(cfg.frames, 8))).cuda(
 k = tb.make_trig_kernel(cfg.sigma_r, cfg.T)
 spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
 flush = torch.empty(128 << 20, device="cuda")
-variants = [("default", {}), ("p1o1", {10: 1}), ("p1o2", {10: 2})]
+variants = [("default", {}), ("p2c1", {3: 1}), ("p2c2", {3: 2}), ("p2c3", {3: 3}), ("p2c4", {3: 4}), ("yc2", {5: 2}), ("yc3", {5: 3}), ("yc4", {5: 4})]
 for name, opts in variants:
     for o, v in {0: 0, 2: 3, 3: 0, 4: 3, 1: 2, 5: 0, 6: 1, 9: 1, 10: -1}.items():
         lib.tbf_set_option(o, v)

@@ -433,7 +433,7 @@ def test_options_match_default(tb):
 
     lib = _native.load()
     DEFAULTS = {_native.TBF_OPT_PASS2_TMA: 3, _native.TBF_OPT_PIPELINE: 0, _native.TBF_OPT_P2_CHUNKS: 0,
-                _native.TBF_OPT_P1_FOLD: 1, _native.TBF_OPT_P1_ORDER: -1, _native.TBF_OPT_P2_ORDER: 1}
+                _native.TBF_OPT_P1_FOLD: 1, _native.TBF_OPT_P1_ORDER: -1, _native.TBF_OPT_P2_ORDER: 0}
     cfg = workloads.CONFIGS[2]
     f = torch.from_numpy(workloads.frame(cfg, 0)[:512, :768].copy()).cuda()
     k = tb.make_trig_kernel(cfg.sigma_r)
@@ -444,7 +444,7 @@ def test_options_match_default(tb):
                      {_native.TBF_OPT_PIPELINE: 1}, {_native.TBF_OPT_P2_CHUNKS: 1},
                      {_native.TBF_OPT_PASS2_TMA: 5}, {_native.TBF_OPT_P1_FOLD: 0},
                      {_native.TBF_OPT_P1_ORDER: 1}, {_native.TBF_OPT_P1_ORDER: 2},
-                     {_native.TBF_OPT_P2_ORDER: 0}, {_native.TBF_OPT_P2_ORDER: 3}):
+                     {_native.TBF_OPT_P2_ORDER: 1}, {_native.TBF_OPT_P2_ORDER: 3}):
             for o, v in opts.items():
                 lib.tbf_set_option(o, v)
             out = tb.TrigFilter(tuple(f.shape), spec, k)(f)
