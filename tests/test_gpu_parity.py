@@ -642,3 +642,31 @@ def test_no_writes_outside_buffers(tb, shape, kind, param, sigma_r):
     torch.cuda.synchronize()
     again = out[M:M + 4 * n].view(torch.float32).reshape(shape).cpu()
     assert torch.isfinite(again).all() and torch.equal(again, dev_out)
+
+
+@pytest.mark.parametrize("shape,sigma_s", [((1, 3, 1500), 4.0), ((1, 1500, 3), 4.0), ((1, 2, 4000), 2.0)])
+def test_extreme_aspect_ratios(tb, orc, shape, sigma_s):
+    """Very wide / very tall images (thousands of column tiles or rows, x- or
+    y-chunking at the limits) against the oracle."""
+    f = np.random.default_rng(shape[2]).uniform(0, 255, shape[1:]).astype(np.float32)
+    k = tb.make_trig_kernel(30.0, 255.0)
+    got = tb.bilateral_trig(f, tb.SpatialSpec.gaussian_recursive(sigma_s), k)
+    ref, _ = orc.bilateral_trig(f.astype(np.float64), "gauss-recursive", sigma_s, orc.make_trig_kernel(30.0, 255.0))
+    assert np.max(np.abs(got - ref)) <= TOL
+
+
+def test_large_batch_of_small_frames(tb, orc):
+    """300 frames of 20x30 in one call (grid z = frames; host staging path for
+    NumPy input) equal per-frame oracle results."""
+    rng = np.random.default_rng(300)
+    fs = rng.uniform(0, 255, (300, 20, 30)).astype(np.float32)
+    k = tb.make_trig_kernel(25.0, 255.0)
+    spec = tb.SpatialSpec.gaussian_recursive(2.0)
+    got = tb.bilateral_trig(fs, spec, k)
+    assert got.shape == fs.shape
+    okern = orc.make_trig_kernel(25.0, 255.0)
+    for i in (0, 1, 137, 299):
+        ref, _ = orc.bilateral_trig(fs[i].astype(np.float64), "gauss-recursive", 2.0, okern)
+        assert np.max(np.abs(got[i] - ref)) <= TOL, i
+    dev = tb.bilateral_trig(torch.from_numpy(fs).cuda(), spec, k).cpu().numpy()
+    np.testing.assert_array_equal(dev, got)
