@@ -2372,7 +2372,28 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         h_tab[ld + j] = (float)(nu - (double)hi);
         h_tab[2 * ld + j] = (float)terms->weight[tbeg + j];
     }
-    cudaMemcpyAsync(tab, h_tab.data(), h_tab.size() * 4, cudaMemcpyHostToDevice, st);
+    // the table is copied from a persistent pinned buffer per distinct table
+    // content (never modified or freed), so a call captured in a CUDA graph
+    // replays the copy of exactly the table it was captured with
+    {
+        static std::mutex mu;
+        static std::vector<std::pair<std::vector<float>, float*>> pinned;
+        const float* src = nullptr;
+        {
+            std::lock_guard<std::mutex> g(mu);
+            for (const auto& e : pinned)
+                if (e.first == h_tab) src = e.second;
+            if (!src) {
+                float* p = nullptr;
+                if (cudaHostAlloc(&p, h_tab.size() * 4, cudaHostAllocDefault) != cudaSuccess)
+                    return fail(TBF_ERR_CUDA, "pinned term table: %s", cudaGetErrorString(cudaGetLastError()));
+                std::copy(h_tab.begin(), h_tab.end(), p);
+                pinned.emplace_back(h_tab, p);
+                src = p;
+            }
+        }
+        cudaMemcpyAsync(tab, src, h_tab.size() * 4, cudaMemcpyHostToDevice, st);
+    }
 
     // host input: column strips copied on an internal stream; pass 1 of the
     // first batch runs strip by strip as they land (columns are independent
