@@ -1241,7 +1241,7 @@ __device__ __forceinline__ void cp_async_wait() {
 
 template <int G>
 __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_async(const __grid_constant__ Pass2Args a) {
-    extern __shared__ __align__(16) unsigned char sm[];
+    extern __shared__ __align__(128) unsigned char sm[];  // same declaration as the TMA variant
     float4* Fs = reinterpret_cast<float4*>(sm);                                  // [DEPTH][G][128]
     float* Ts = reinterpret_cast<float*>(Fs + P2A_DEPTH * G * P2_THREADS);       // [DEPTH][128]
     const int tid = threadIdx.x;
