@@ -3,15 +3,19 @@
  * bilateral filter (arXiv 1105.4204 hot path).
  *
  * All pointers named d_* / f / out / num / den / workspace are DEVICE
- * pointers (CUDA global memory on the current device); `stream` is a
- * cudaStream_t passed as void*.  Every entry point is asynchronous on
- * `stream` and returns a status code for errors detectable at launch time.
- * No torch / C++ types cross this boundary.
+ * pointers (CUDA global memory on the current device); h_* are host
+ * pointers; `stream` is a cudaStream_t passed as void*.  Every entry point
+ * is asynchronous on `stream` and returns a status code for errors
+ * detectable at launch time.  No torch / C++ types cross this boundary.
  *
  * What each entry replaces in the reference package (/root/reference/pkg):
  *
+ *   tbf_bilateral_trig_host
+ *                        engines.py:228-306  bilateral_trig(img, spatial, kernel)
+ *                        end to end on host arrays (the NumPy-level call)
  *   tbf_bilateral_trig   engines.py:228-306  bilateral_trig(img, spatial, kernel)
  *                        (term loop + smooth_plane + demodulate + _guarded_ratio)
+ *                        on device buffers
  *   tbf_trig_partial     engines.py:249-300  the term loop restricted to the
  *                        pairs [term_begin, term_end): accumulates num/den only
  *                        (term-sharded multi-GPU path; NCCL reduce sits between
@@ -24,6 +28,11 @@
  *                        _backend.py:38-39)
  *   tbf_box_pass_f64     _core.pyx:28-53     box_pass(a, radius)
  *                        (_backend.box_pass, _backend.py:38)
+ *   tbf_bilateral_direct engines.py:120-151  bilateral_direct(img, spatial, range_fn)
+ *                        (fp64 brute force; Gaussian kernels.py:174-182 or
+ *                        raised cosine kernels.py:161-171 range kernel)
+ *   tbf_workspace_bytes, tbf_set_option, tbf_profile_*, tbf_last_error,
+ *   tbf_abi_version      (new: sizing, tuning, per-kernel timing, errors)
  */
 #ifndef TRIGBF_B200_H
 #define TRIGBF_B200_H
