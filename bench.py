@@ -413,6 +413,7 @@ def main():
                   "reduce": 8 * px_rank, "transpose": 12 * px_rank, "range_check": 4 * px_rank,
                   "finalize": 12 * px_rank, "chain": 0}
     roofline = None
+    issue = None
     if dom is not None:
         ms_total, launches = kt[dom]
         avg_s = ms_total / launches / 1e3
@@ -428,6 +429,11 @@ def main():
                 with open(prof_path) as fh:
                     tr = json.load(fh)
                 roofline["traffic"] = tr.get(dom)
+                inst = tr.get("_inst", {}).get(dom)
+                if inst:  # issue-rate view: warp instructions per launch (ncu) / live launch time
+                    issue = {"kernel": dom, "warp_instructions_per_launch": inst,
+                             "achieved": round(inst / avg_s / 1e12, 4), "unit": "T warp-instr/s",
+                             "source": os.path.relpath(prof_path, ROOT)}
             except Exception:
                 pass
     alg_step = algorithmic_bytes_per_px(pairs) * cfg.pixels * (world if mode == "replica" else 1)
@@ -483,6 +489,10 @@ def main():
 
     if rank == 0:
         clocks = clk.summary()
+        if issue is not None and clocks.get("sm_max_mhz"):
+            # 148 SMs x 4 schedulers x 1 warp-instruction per clock
+            issue["peak"] = round(148 * 4 * clocks["sm_max_mhz"] / 1e6, 4)
+            issue["frac"] = round(issue["achieved"] / issue["peak"], 4)
         if fp32 is not None and clocks.get("sm_max_mhz"):
             fp32["peak"] = round(148 * 128 * 2 * clocks["sm_max_mhz"] / 1e6, 1)  # non-tensor FP32
             fp32["frac"] = round(fp32["achieved"] / fp32["peak"], 4)
@@ -500,6 +510,7 @@ def main():
             "roofline": roofline,
             "pipeline_roofline": pipeline,
             "fp32_pass1": fp32,
+            "issue_roofline": issue,
             "kernels": kernel_share,
             "gpu_launches": launches_total,
             "e2e": e2e,

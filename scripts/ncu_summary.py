@@ -92,6 +92,9 @@ def summarise_rep(rep, out_md, traffic_json):
                 kind = k.replace("k_", "").replace("_gauss", "")
                 kind = "pass2" if kind.startswith("pass2") else kind
                 traffic[kind] = rd + wr
+                if "smsp__inst_executed.sum" in d:  # warp instructions per launch
+                    inst = float(d["smsp__inst_executed.sum"].split(" ", 1)[0].replace(",", ""))
+                    traffic.setdefault("_inst", {})[kind] = inst
             except Exception:
                 pass
         with open(traffic_json, "w") as fh:
