@@ -48,7 +48,7 @@
 #include <vector>
 
 #ifndef TBF_PHASOR_SFU
-#define TBF_PHASOR_SFU 1  // 0: FMA-pipe polynomial phasors (see sincos_fma)
+#define TBF_PHASOR_SFU 2  // 1: SFU after an explicit 2*pi reduction; 0: FMA-pipe polynomial (see sincos_fma)
 #endif
 
 #include "trigbf_b200.h"
@@ -215,17 +215,24 @@ __device__ __forceinline__ void csteady(float u, float& v1, float& v2, float& y1
     y1 = y2 = u * k.ig;
 }
 
-// sin and cos of x for |x| < ~1e5.  TBF_PHASOR_SFU=1 (default): SFU after a
-// 2*pi reduction.  TBF_PHASOR_SFU=0: FMA pipe only (no SFU, no slow-path
-// branch): Cody-Waite reduction by pi/2 in three parts (exact products inside
+// sin and cos of x for |x| < ~1e5.  TBF_PHASOR_SFU=2 (default): SFU directly;
+// 1: SFU after an explicit 2*pi reduction; 0: FMA pipe only (no SFU, no
+// slow-path branch): Cody-Waite reduction by pi/2 in three parts (exact products inside
 // the FMAs), then the Cephes minimax polynomials on [-pi/4, pi/4] (about 1 ulp).
 // Arguments here are nu*f <= ~420 rad.
 __device__ __forceinline__ void sincos_fma(float x, float* sp, float* cp) {
-#if TBF_PHASOR_SFU
-    // default: Cody-Waite reduction by 2*pi in two parts (q*6.28125 exact for
+#if TBF_PHASOR_SFU == 2
+    // default: the SFU directly (FMUL.RZ by 1/(2 pi), MUFU.SIN/COS take the
+    // fraction of the turn count themselves).  Phase error ~1 ulp of
+    // x/(2 pi) (~1e-5 rad at config 2's largest phase, ~5e-5 at config 3's)
+    // instead of ~1 ulp of x; 5 instructions instead of 9, measured 2-3%
+    // faster end to end with parity unchanged
+    __sincosf(x, sp, cp);
+#elif TBF_PHASOR_SFU
+    // Cody-Waite reduction by 2*pi in two parts (q*6.28125 exact for
     // q < 2^15), then the SFU (MUFU.SIN/COS, abs error ~2^-21 on [-pi, pi]).
-    // 9 instructions instead of ~24; measured +10% end to end on configs
-    // 2/3/5 with unchanged parity
+    // 9 instructions instead of ~24 for the polynomial; measured +10% end to
+    // end on configs 2/3/5 with unchanged parity
     const float t = fmaf(x, 0.159154943091895336f, 12582912.0f);
     const float q = t - 12582912.0f;
     float r = fmaf(q, -6.28125f, x);
