@@ -215,6 +215,20 @@ __device__ __forceinline__ void csteady(float u, float& v1, float& v2, float& y1
     y1 = y2 = u * k.ig;
 }
 
+// Phase nu * f with nu split hi/lo (TBF_PHASE_HILO=1, default: correctly
+// rounded) or nu_hi * f alone (0).
+#ifndef TBF_PHASE_HILO
+#define TBF_PHASE_HILO 1
+#endif
+__device__ __forceinline__ float phase(float nu_hi, float nu_lo, float f) {
+#if TBF_PHASE_HILO
+    return fmaf(nu_hi, f, nu_lo * f);
+#else
+    (void)nu_lo;
+    return nu_hi * f;
+#endif
+}
+
 // sin and cos of x for |x| < ~1e5.  TBF_PHASOR_SFU=2 (default): SFU directly;
 // 1: SFU after an explicit 2*pi reduction; 0: FMA pipe only (no SFU, no
 // slow-path branch): Cody-Waite reduction by pi/2 in three parts (exact products inside
@@ -280,7 +294,7 @@ __device__ __forceinline__ void phasors(float fv, const float (&nu_hi)[G], const
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         if (g % R == 0) {
-            sincos_fma(fmaf(nu_hi[g], fv, nu_lo[g] * fv), &s, &c);
+            sincos_fma(phase(nu_hi[g], nu_lo[g], fv), &s, &c);
         } else {
             float cn = fmaf(c, sc, -s * ss);
             float snn = fmaf(s, sc, c * ss);
@@ -443,7 +457,7 @@ __device__ __forceinline__ void p1_fwd8(const float (&fv)[8], float nu_hi, float
                                         float (&y1)[4], float (&y2)[4], float4* row) {
     float cs[8], sn[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) sincos_fma(fmaf(nu_hi, fv[q], nu_lo * fv[q]), &sn[q], &cs[q]);
+    for (int q = 0; q < 8; ++q) sincos_fma(phase(nu_hi, nu_lo, fv[q]), &sn[q], &cs[q]);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const float u[4] = {cs[q], sn[q], fv[q] * cs[q], fv[q] * sn[q]};
@@ -522,7 +536,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     {
         const float f0 = fload(A0);
         float s0, c0;
-        sincos_fma(fmaf(nu_hi, f0, nu_lo * f0), &s0, &c0);
+        sincos_fma(phase(nu_hi, nu_lo, f0), &s0, &c0);
         const float u[4] = {c0, s0, f0 * c0, f0 * s0};
 #pragma unroll
         for (int p = 0; p < 4; ++p) csteady(u[p], v1[p], v2[p], y1[p], y2[p], k);
@@ -532,7 +546,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     auto step1 = [&](int i) {
         const float fs = fload(i);
         float s0, c0;
-        sincos_fma(fmaf(nu_hi, fs, nu_lo * fs), &s0, &c0);
+        sincos_fma(phase(nu_hi, nu_lo, fs), &s0, &c0);
         const float u[4] = {c0, s0, fs * c0, fs * s0};
 #pragma unroll
         for (int p = 0; p < 4; ++p) cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
@@ -631,7 +645,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                 for (int r = 0; r < len; ++r) {
                     const float fs = fload(i0 + r);
                     float s0, c0;
-                    sincos_fma(fmaf(nu_hi, fs, nu_lo * fs), &s0, &c0);
+                    sincos_fma(phase(nu_hi, nu_lo, fs), &s0, &c0);
                     const float u[4] = {c0, s0, fs * c0, fs * s0};
                     float o[4];
 #pragma unroll
@@ -890,7 +904,7 @@ __device__ __forceinline__ void p2_step4(const Pass2Args& a, const P2Ctx<G>& c, 
         for (int q = 0; q < 4; ++q)
 #pragma unroll
             for (int g = 0; g < G; ++g)
-                sincos_fma(fmaf(c.nu_hi[g], fv[q], c.nu_lo[g] * fv[q]), &sn[q][g], &cs[q][g]);
+                sincos_fma(phase(c.nu_hi[g], c.nu_lo[g], fv[q]), &sn[q][g], &cs[q][g]);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -1202,7 +1216,7 @@ __global__ void __launch_bounds__(P2T_THREADS, MINB) k_pass2_tma(const __grid_co
                     }
                     if (out) {
                         float sn, cs;
-                        sincos_fma(fmaf(nu_hi[g], fv, nu_lo[g] * fv), &sn, &cs);
+                        sincos_fma(phase(nu_hi[g], nu_lo[g], fv), &sn, &cs);
                         num = fmaf(wt[g], fmaf(cs, y[2], sn * y[3]), num);
                         den = fmaf(wt[g], fmaf(cs, y[0], sn * y[1]), den);
                     }
@@ -1373,7 +1387,7 @@ __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_async(const __grid_cons
             }
             if (out) {
                 float sn, cs;
-                sincos_fma(fmaf(nu_hi[g], fv, nu_lo[g] * fv), &sn, &cs);
+                sincos_fma(phase(nu_hi[g], nu_lo[g], fv), &sn, &cs);
                 num = fmaf(wt[g], fmaf(cs, y[2], sn * y[3]), num);
                 den = fmaf(wt[g], fmaf(cs, y[0], sn * y[1]), den);
             }
@@ -1602,7 +1616,7 @@ __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_consta
 
 __device__ __forceinline__ float4 modulate4(float fv, float nu_hi, float nu_lo) {
     float s0, c0;
-    sincos_fma(fmaf(nu_hi, fv, nu_lo * fv), &s0, &c0);
+    sincos_fma(phase(nu_hi, nu_lo, fv), &s0, &c0);
     return make_float4(c0, s0, fv * c0, fv * s0);
 }
 
