@@ -503,7 +503,8 @@ def bilateral_direct(img, spatial, range_fn, *, samples=None,
     return out.reshape(img.shape)
 
 
-def _bilateral_trig_streamed(t, spatial, kernel, diagnostics, sub: int | None = None):
+def _bilateral_trig_streamed(t, spatial, kernel, diagnostics, sub: int | None = None,
+                             edges: bool = True):
     """Pinned host batch [B, H, W]: frames flow through the device in
     sub-batches so host->device copies, filtering and device->host copies of
     different sub-batches overlap (copy engines run beside the SMs).  Same
@@ -512,7 +513,19 @@ def _bilateral_trig_streamed(t, spatial, kernel, diagnostics, sub: int | None = 
     B, H, W = t.shape
     if sub is None:
         sub = max(1, min(B, (B + 7) // 8))  # ~8 sub-batches
-    nsub = (B + sub - 1) // sub
+    # sub-batch boundaries: with edges=True the first and last sub-batches are
+    # single frames, so the copy-in before the first filter and the copy-out
+    # after the last one (the parts no filtering overlaps) are one frame each
+    bounds = [0]
+    if edges and B >= 2 * sub + 2:
+        bounds += [1]
+        while bounds[-1] < B - 1:
+            bounds.append(min(B - 1, bounds[-1] + sub))
+        bounds.append(B)
+    else:
+        while bounds[-1] < B:
+            bounds.append(min(B, bounds[-1] + sub))
+    nsub = len(bounds) - 1
     dev = torch.device("cuda", torch.cuda.current_device())
     comp = torch.cuda.current_stream(dev)
     h2d = torch.cuda.Stream(dev)
@@ -525,7 +538,7 @@ def _bilateral_trig_streamed(t, spatial, kernel, diagnostics, sub: int | None = 
     ev_comp = [torch.cuda.Event() for _ in range(nsub)]
     ev_out = [torch.cuda.Event() for _ in range(nsub)]
     for kk in range(nsub):
-        b0, b1 = kk * sub, min(B, (kk + 1) * sub)
+        b0, b1 = bounds[kk], bounds[kk + 1]
         nb = b1 - b0
         slot = kk % 2
         with torch.cuda.stream(h2d):
