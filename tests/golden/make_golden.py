@@ -8,6 +8,8 @@ Outputs (committed, small):
                        images (recursive Gaussian and box spatial, even/odd N,
                        degenerate shapes), plus plugin-level recursive_smooth /
                        box_pass vectors.
+  config_2_box.npz  -- the config-2 image through the reference's box
+                       spatial path (radius 8, full run), sampled pixels.
   pnm_cases.npz     -- PNM round trips through the reference's pnm module:
                        input bytes (with comments / odd whitespace), the parsed
                        planes, the re-written canonical bytes, quantisation of
@@ -212,12 +214,32 @@ def make_pnm(path: str) -> None:
     np.savez_compressed(path, **out)
 
 
+def make_box_config(path: str, radius: int = 8) -> None:
+    """The config-2 image through the reference's box spatial path (full
+    2048^2 run, N = 66): the box kernels at a BASELINE size."""
+    cfg = workloads.CONFIGS[2]
+    f = workloads.frame(cfg, 0)
+    t = time.time()
+    out = ref_filter(f, "box", radius, cfg.sigma_r)
+    rng = np.random.default_rng(2024)
+    ys, xs = _sample((0, f.shape[0], 0, f.shape[1]), SAMPLES, rng)
+    # plus the four borders, where the mirror indexing matters
+    ys = np.concatenate([ys, [0, 0, f.shape[0] - 1, f.shape[0] - 1, 0, 1023, 2047, 5]])
+    xs = np.concatenate([xs, [0, f.shape[1] - 1, 0, f.shape[1] - 1, 1023, 0, 700, 2047]])
+    np.savez_compressed(path, frame=np.zeros(ys.size, np.int64), y=ys, x=xs, value=out[ys, xs],
+                        radius=radius, sigma_r=cfg.sigma_r, reference_backend=trigbf.backend_name())
+    print(f"box cfg2: {time.time() - t:.1f}s -> {path}", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="", help="comma list of config ids to (re)generate")
     ap.add_argument("--small", action="store_true")
     ap.add_argument("--pnm", action="store_true")
+    ap.add_argument("--box-config", action="store_true")
     args = ap.parse_args()
+    if args.box_config:
+        make_box_config(os.path.join(HERE, "config_2_box.npz"))
     if args.pnm:
         make_pnm(os.path.join(HERE, "pnm_cases.npz"))
         print("pnm cases written")

@@ -106,6 +106,26 @@ def test_config_goldens(tb, cfg_id):
     assert worst <= TOL
 
 
+def test_config2_box_golden(tb):
+    """The box spatial path at a BASELINE size: the config-2 image with a
+    radius-8 box window (N = 66) against the reference's full run, at
+    sampled pixels and the four borders; device and host entries."""
+    from paper_1105_4204_b200 import workloads
+
+    g = np.load(os.path.join(GOLDEN, "config_2_box.npz"))
+    cfg = workloads.CONFIGS[2]
+    f = torch.from_numpy(workloads.frame(cfg, 0)).cuda()
+    k = tb.make_trig_kernel(float(g["sigma_r"]), cfg.T)
+    spec = tb.SpatialSpec.box(int(g["radius"]))
+    out = tb.bilateral_trig(f, spec, k)
+    ys, xs = torch.from_numpy(g["y"]).cuda(), torch.from_numpy(g["x"]).cuda()
+    err = float(np.max(np.abs(out[ys, xs].double().cpu().numpy() - g["value"])))
+    host = tb.bilateral_trig(f.cpu().pin_memory(), spec, k)
+    err_h = float(np.max(np.abs(host[g["y"], g["x"]].double().numpy() - g["value"])))
+    print(f"config 2 box r={int(g['radius'])}: worst max abs err {err:.3g} (host entry {err_h:.3g})")
+    assert err <= TOL and err_h <= TOL
+
+
 def test_batched_frames_equal_single_calls(tb):
     """Config-4 style batch: frames are independent (batch == per-frame calls)."""
     from paper_1105_4204_b200.workloads import rects_image
