@@ -446,6 +446,18 @@ def test_gauss_odd_shapes_with_chunking(tb, orc, h, w, s, sr):
     assert np.max(np.abs(got - ref)) <= TOL
 
 
+@pytest.mark.parametrize("h,w,s,sr", [(300, 200, 100.0, 80.0), (540, 720, 100.0, 80.0), (64, 900, 300.0, 20.0),
+                                      (900, 64, 60.0, 30.0)])
+def test_gauss_large_sigma_s(tb, orc, h, w, s, sr):
+    """Large sigma_s: the truncated mirror extension saturates at n-1 (the
+    reference's full extension) in one or both directions, the decay length
+    exceeds the y-chunk and x-chunk sizes."""
+    f = np.random.default_rng(h + w).uniform(0, 255, (h, w)).astype(np.float32)
+    got = _run(tb, f, "gauss-recursive", s, sr)
+    ref, _ = orc.bilateral_trig(f.astype(np.float64), "gauss-recursive", s, orc.make_trig_kernel(sr, 255.0))
+    assert np.max(np.abs(got - ref)) <= TOL
+
+
 def test_options_match_default(tb):
     """The optional pass-2 TMA variants and the two-stream pipeline compute the
     same filter (up to fp32 reassociation)."""
