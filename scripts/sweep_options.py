@@ -12,8 +12,10 @@ k = tb.make_trig_kernel(cfg.sigma_r, cfg.T)
 spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
 flush = torch.empty(128 << 20, device="cuda")
 variants = [("default", {}), ("p2c1", {3: 1}), ("p2c2", {3: 2}), ("p2c3", {3: 3}), ("p2c4", {3: 4}), ("yc2", {5: 2}), ("yc3", {5: 3}), ("yc4", {5: 4})]
+if len(sys.argv) > 2:  # variants as JSON: [["name", {"option": value}], ...]
+    variants = [(n, {int(o): v for o, v in d.items()}) for n, d in json.loads(sys.argv[2])]
 for name, opts in variants:
-    for o, v in {0: 0, 2: 3, 3: 0, 4: 3, 1: 2, 5: 0, 6: 1, 9: 1, 10: -1}.items():
+    for o, v in {0: 0, 2: 3, 3: 0, 4: 3, 1: 2, 5: 0, 6: 1, 9: 0, 10: -1}.items():
         lib.tbf_set_option(o, v)
     for o, v in opts.items():
         lib.tbf_set_option(o, v)
