@@ -34,6 +34,8 @@ TBF_OPT_HOST_STRIPS = 7
 TBF_OPT_HOST_BANDS = 8
 TBF_OPT_P2_ORDER = 9
 TBF_OPT_P1_ORDER = 10
+TBF_OPT_LPT_SPLIT = 11  # bits 1/2: planned y-/x-chunks (device entry); 4/8: also in the host entry
+TBF_LPT_DEFAULT = 3
 
 TBF_SPATIAL_RECURSIVE = 0
 TBF_SPATIAL_BOX = 1

@@ -38,11 +38,15 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
+#include <queue>
+#include <tuple>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -84,6 +88,8 @@ __host__ __device__ __forceinline__ size_t ty_plane(int B, int W, int H) {
 __host__ __device__ __forceinline__ size_t xm_plane(int B, int W, int H) {
     return (size_t)B * ((H + FL_RB - 1) / FL_RB) * FL_RB * W;
 }
+constexpr int TBF_MAX_YCH = 16;      // most y-chunks per pass-1 column
+constexpr int TBF_MAX_XCH = 64;      // most x-chunks per pass-2 row
 constexpr int P1_BLOCKS_PER_SM = 3;  // smem-limited residency of pass-1 blocks (4 warps, 67.6 KB)
 constexpr int BUF_LD = TILE + 1;  // padded leading dimension of the smem tile
 
@@ -375,7 +381,8 @@ struct Pass1Args {
     const float* fY;  // f tile-major (ty_index): a warp's 32-row segment is 4 KB contiguous
     int B, H, W;
     int Ey, nseg;  // y mirror extension; checkpoint segments per y-chunk
-    int nyc, ych_rows, ywarm;  // y-chunks of ych_rows output rows; warm-up rows (mult. of 32)
+    int nyc, ych_rows, ywarm;  // y-chunks (at most ych_rows output rows each); warm-up rows (mult. of 32)
+    int ychb[TBF_MAX_YCH + 1];  // chunk c covers output rows [ychb[c], ychb[c+1]) (multiples of 32)
     int Ex, ne, edge_all, ntx;
     int tile0, ntx_run;  // column tiles [tile0, tile0 + ntx_run) in this launch
     int order, ngb;      // block order (TBF_OPT_P1_ORDER); term-group blocks
@@ -416,6 +423,9 @@ struct Pass2Args {
     float wscale;      // g^2: undoes the two pure x sweeps (1 for box)
     int rb0, nrb_run;     // 128-row blocks [rb0, rb0 + nrb_run) in this launch
     int tiles_per_chunk;  // x-chunking of rows (gauss); == ntx for one chunk
+    int nxc;              // x-chunks (k_pass2_gr: chunk c covers tiles [xcb[c], xcb[c+1]))
+    int xcb[TBF_MAX_XCH + 1];
+    int xord[TBF_MAX_XCH];  // k_pass2_gr order 4: dispatch rank -> chunk (costliest first)
     int warm_tiles;       // warm-up tiles of a chunk's backward sweep
     const float* floc;
     const float* carry;   // chained carries float4 [n][B][ntx][H][4]
@@ -490,6 +500,12 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
         chunk = blockIdx.x % a.nyc;
         tile_r = blockIdx.x / a.nyc;
         gblk = blockIdx.y;
+    } else if (a.order == 3) {  // column tile fastest, then term group; y-chunk slowest
+        int idx = blockIdx.x;
+        tile_r = idx % a.ntx_run;
+        idx /= a.ntx_run;
+        gblk = idx % a.ngb;
+        chunk = idx / a.ngb;
     } else {
         tile_r = blockIdx.x % a.ntx_run;
         chunk = blockIdx.x / a.ntx_run;
@@ -523,8 +539,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     // ywarm from a steady-state guess (exact -Ey start for the top chunk); the
     // backward starts at Bend = R1 + ywarm (exact H+Ey end for the bottom
     // chunk).  ywarm >= the decay length K, so guesses fade below eps.
-    const int R0 = chunk * a.ych_rows;
-    const int R1 = min(H, R0 + a.ych_rows);
+    const int R0 = a.ychb[chunk];
+    const int R1 = a.ychb[chunk + 1];
     const int A0 = R0 - a.ywarm <= 0 ? -Ey : R0 - a.ywarm;
     const int Bend = R1 + a.ywarm >= iend ? iend : R1 + a.ywarm;
     // checkpoints: float4 per plane, [chunk*nseg + local seg][term][b][x][4]
@@ -1487,9 +1503,17 @@ __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_consta
     extern __shared__ float2 sdyn[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nsb = a.nrb_run * (P2_THREADS / 32);  // 32-row sub-blocks in this launch
-    const int nch = gridDim.x / nsb;
+    const int nch = a.nxc;
     int chunk, rsb;
-    if (a.order == 1) {  // x-chunk fastest: both chunks of a row block together
+    int gy = blockIdx.y;  // group block
+    if (a.order == 4) {  // 1-D grid, chunk slowest (in xord order), then group block, row sub-block
+        const int npb = (a.ngroups + P2R_GR - 1) / P2R_GR;
+        int idx = blockIdx.x;
+        rsb = idx % nsb;
+        idx /= nsb;
+        gy = idx % npb;
+        chunk = a.xord[idx / npb];
+    } else if (a.order == 1) {  // x-chunk fastest: both chunks of a row block together
         chunk = blockIdx.x % nch;
         rsb = blockIdx.x / nch;
     } else if (a.order == 2) {  // rows reversed within a chunk
@@ -1497,6 +1521,9 @@ __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_consta
         rsb = nsb - 1 - blockIdx.x % nsb;
     } else if (a.order == 3) {  // chunks reversed (rightmost, exact-start chunk first)
         chunk = nch - 1 - blockIdx.x / nsb;
+        rsb = blockIdx.x % nsb;
+    } else if (a.order == 5) {  // default grid, chunks in xord order (costliest first)
+        chunk = a.xord[blockIdx.x / nsb];
         rsb = blockIdx.x % nsb;
     } else {
         chunk = blockIdx.x / nsb;
@@ -1508,7 +1535,7 @@ __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_consta
     const int i_raw = r0 + lane;
     const bool iv = i_raw < H;
     const int i = iv ? i_raw : H - 1;
-    const int grp_raw = blockIdx.y * P2R_GR + w;
+    const int grp_raw = gy * P2R_GR + w;
     const bool active = grp_raw < a.ngroups;
     const int grp = active ? grp_raw : a.ngroups - 1;
     const int b = blockIdx.z;
@@ -1528,14 +1555,14 @@ __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_consta
     }
     c.fT = a.fT + xm_index(b, 0, i, W, H);
     const size_t xpl = xm_plane(a.B, W, H);
-    float* pn = a.part + (size_t)(blockIdx.y * 2 + 0) * xpl + xm_index(b, 0, iv ? i_raw : 0, W, H);
-    float* pd = a.part + (size_t)(blockIdx.y * 2 + 1) * xpl + xm_index(b, 0, iv ? i_raw : 0, W, H);
+    float* pn = a.part + (size_t)(gy * 2 + 0) * xpl + xm_index(b, 0, iv ? i_raw : 0, W, H);
+    float* pd = a.part + (size_t)(gy * 2 + 1) * xpl + xm_index(b, 0, iv ? i_raw : 0, W, H);
     // tile k of this block stages in buffer k & 1: one barrier per tile (the
     // buffer written next was last read before the previous barrier)
     auto sbuf = [&](int buf, int q, int m) -> float2& { return sdyn[((buf * P2R_GR + q) * TILE + m) * 32 + lane]; };
 
-    const int t_lo = chunk * a.tiles_per_chunk;
-    const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
+    const int t_lo = a.xcb[chunk];
+    const int t_hi = a.xcb[chunk + 1];  // exclusive
     float p1[G][4], p2[G][4], q1[G][4], q2[G][4];
     if (active) {
         const bool exact_start = t_hi + a.warm_tiles >= a.ntx;
@@ -2053,6 +2080,8 @@ size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 struct Layout {
     int B, H, W, Ey, Ex, nseg, ntx, ne, edge_all;
     int nyc, ych_rows, ywarm;  // pass-1 y-chunking (nseg = checkpoint segments per chunk)
+    int ychb[TBF_MAX_YCH + 1];  // chunk boundaries (ych_rows = the largest chunk)
+    bool ych_lpt;               // chunks of unequal size, dispatched largest first
     int tb;     // terms per batch (multiple of G2)
     int ng2;    // pass-2 groups per batch
     int nb;     // batches
@@ -2067,6 +2096,8 @@ struct Layout {
 
 int g_pass1_fold = 1;   // tbf_set_option(TBF_OPT_P1_FOLD); see run_terms
 int g_p1_ychunks = 0;   // tbf_set_option(TBF_OPT_P1_YCHUNKS): 0 = automatic
+int g_lpt_split = 3;    // tbf_set_option(TBF_OPT_LPT_SPLIT): bits 1/2 = planned unequal y-/x-chunks for few-wave launches,
+                        // 4/8 = also in the host entry's strip/band launches
 int g_p1_occ = 3;       // tbf_set_option(TBF_OPT_P1_OCC): pass-1 blocks per SM (2 leaves room for a pass-2 block)
 int g_p2_chunks = 0;    // tbf_set_option(TBF_OPT_P2_CHUNKS): 0 = automatic
 int g_pass2_tma = 3;    // tbf_set_option(TBF_OPT_PASS2_TMA): 0 register prefetch (G=2), 1/2 TMA producer warp, 3 auto (default), 4 cp.async G=4
@@ -2077,8 +2108,130 @@ int g_p2_order = 0;     // tbf_set_option(TBF_OPT_P2_ORDER): block order of the 
 int g_host_strips = 0;  // tbf_set_option(TBF_OPT_HOST_STRIPS): column strips of the host input (0 auto)
 int g_host_bands = 0;   // tbf_set_option(TBF_OPT_HOST_BANDS): row bands of the host output (0 auto)
 
+// Pass-1 y-chunk planner for launches of a few waves.  Blocks of one chunk
+// level all cost the same; the levels are dispatched largest first (block
+// order with the chunk index slowest), and the makespan is that of list
+// scheduling onto the resident block slots.  Block cost = instructions per
+// row of the phases it runs: phase A (forward, ~24 per row), phase B
+// (forward recompute + backward, ~43) and the epilogue (~18 per output row),
+// from the ncu source page (profiles/ DESIGN.md 9).  Measured on config 2
+// (B200): the simulated best split (1408 + 640 rows) was also the measured
+// best, 6% less pass-1 time than two equal chunks (tail wave at partial
+// occupancy).
+double lpt_makespan(std::vector<double> d, long long per_level, int slots) {
+    std::sort(d.begin(), d.end(), std::greater<double>());  // costliest level first
+    std::priority_queue<double, std::vector<double>, std::greater<double>> q;
+    for (int s = 0; s < slots; ++s) q.push(0.0);
+    double mk = 0.0;
+    for (double dl : d)
+        for (long long j = 0; j < per_level; ++j) {
+            const double t = q.top() + dl;
+            q.pop();
+            q.push(t);
+            mk = std::max(mk, t);
+        }
+    return mk;
+}
+
+double p1_makespan(const std::vector<int>& bnd, int H, int Ey, int ywarm, long long per_chunk, int slots) {
+    std::vector<double> d;
+    for (size_t c = 0; c + 1 < bnd.size(); ++c) {
+        const int R0 = bnd[c], R1 = bnd[c + 1];
+        const int A0 = R0 - ywarm <= 0 ? -Ey : R0 - ywarm;
+        const int Bend = R1 + ywarm >= H + Ey ? H + Ey : R1 + ywarm;
+        d.push_back(24.0 * (Bend - A0) + 43.0 * (Bend - R0) + 18.0 * (R1 - R0));
+    }
+    return lpt_makespan(d, per_chunk, slots);
+}
+
+// Pass-2 x-chunk cost: tiles walked, including the warm-up tiles of every
+// chunk but the rightmost (exact start).
+double p2_chunk_cost(int t0, int t1, int ntx, int warm) {
+    return (double)((t1 + warm >= ntx ? ntx : t1 + warm) - t0);
+}
+
+// Best split of the ntx column tiles of a pass-2 row into x-chunks (1..3,
+// dispatched costliest first) by lpt_makespan, against the equal split of
+// `uniform` chunks (kept on near ties).  Cached per shape.  Measured on config 2
+// (B200): 48 + 16 tiles, costliest first, took 9% less pass-2 time than the
+// 4 x 16 equal split; pass 2 streams HBM, so a tail wave at partial occupancy
+// runs below bandwidth.
+std::vector<int> p2_plan_split(int ntx, int warm, int uniform, long long per_chunk, int slots) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, long long, int>, std::vector<int>> cache;
+    const auto key = std::make_tuple(ntx, warm, uniform, per_chunk, slots);
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    auto eval = [&](const std::vector<int>& b) {
+        std::vector<double> d;
+        for (size_t c = 0; c + 1 < b.size(); ++c) d.push_back(p2_chunk_cost(b[c], b[c + 1], ntx, warm));
+        return lpt_makespan(d, per_chunk, slots);
+    };
+    const int tpc = (ntx + uniform - 1) / uniform;
+    std::vector<int> best{0};
+    for (int c = 1; c * tpc < ntx + tpc; ++c) best.push_back(std::min(ntx, c * tpc));
+    best.back() = ntx;
+    double best_mk = eval(best);
+    auto consider = [&](std::vector<int> b) {
+        const double mk = eval(b);
+        if (mk < best_mk * 0.97) {
+            best_mk = mk;
+            best = b;
+        }
+    };
+    for (int a = 1; a < ntx; ++a) consider({0, a, ntx});
+    const int st = std::max(1, ntx / 32);
+    for (int a = 1; a < ntx; a += st)
+        for (int b2 = a + 1; b2 < ntx; b2 += st) consider({0, a, b2, ntx});
+    std::lock_guard<std::mutex> g(mu);
+    cache[key] = best;
+    return best;
+}
+
+// Best split of H rows (multiples of TILE, each >= minr, non-increasing) into
+// 1..3 chunks by p1_makespan; cached per shape.  Returns the boundaries.
+std::vector<int> p1_plan_split(int H, int Ey, int ywarm, long long per_chunk, int slots) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, long long, int>, std::vector<int>> cache;
+    const auto key = std::make_tuple(H, Ey, ywarm, per_chunk, slots);
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    const int units = (H + TILE - 1) / TILE;  // 32-row units (the last may be partial)
+    const int minu = std::max(2, (ywarm + TILE - 1) / TILE);
+    std::vector<int> best{0, H};
+    double best_mk = p1_makespan(best, H, Ey, ywarm, per_chunk, slots);
+    auto consider = [&](std::vector<int> u) {  // chunk sizes in units, largest first
+        std::vector<int> b{0};
+        for (size_t i = 0; i < u.size(); ++i) b.push_back(i + 1 == u.size() ? H : std::min(H, b.back() + u[i] * TILE));
+        const double mk = p1_makespan(b, H, Ey, ywarm, per_chunk, slots);
+        if (mk < best_mk * 0.99) {  // fewer chunks on near ties (candidates come in increasing count)
+            best_mk = mk;
+            best = b;
+        }
+    };
+    for (int a = (units + 1) / 2; a <= units - minu; ++a) consider({a, units - a});
+    const int step3 = std::max(1, units / 24);
+    for (int a = (units + 2) / 3; a <= units - 2 * minu; a += step3)
+        for (int b2 = minu; b2 <= std::min(a, units - a - minu); b2 += step3) {
+            const int c = units - a - b2;
+            if (c < minu || c > b2) continue;
+            consider({a, b2, c});
+        }
+    std::lock_guard<std::mutex> g(mu);
+    cache[key] = best;
+    return best;
+}
+
+// lpt: allow the planned unequal y-chunks (full-image launches; the host
+// entry's strip-wise pass 1 keeps equal chunks)
 int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, int batch_terms,
-                Layout* L) {
+                Layout* L, bool lpt = true) {
     if (B < 1 || H < 1 || W < 1) return fail(TBF_ERR_DIM, "bad shape B=%d H=%d W=%d", B, H, W);
     if (!sp) return fail(TBF_ERR_PARAM, "null spatial");
     L->B = B;
@@ -2135,6 +2288,49 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
         if (g_p1_ychunks > 0) nyc = std::min(g_p1_ychunks, (H + TILE - 1) / TILE);
         L->ych_rows = ((H + nyc - 1) / nyc + TILE - 1) / TILE * TILE;
         L->nyc = (H + L->ych_rows - 1) / L->ych_rows;
+    }
+    for (int c = 0; c <= L->nyc; ++c) L->ychb[c] = std::min(H, c * L->ych_rows);
+    L->ych_lpt = false;
+    if (!box && g_p1_ychunks <= 0 && (g_lpt_split & 1) && lpt) {
+        // few waves: plan unequal chunks, largest first (p1_plan_split)
+        const int slots = 148 * P1_BLOCKS_PER_SM;
+        const long long per_chunk = (long long)L->ntx * ((tb + P1_WARPS - 1) / P1_WARPS) * B;
+        // (not for short columns: config 1, 512 rows, was 6% slower with the
+        // planned 3-way split; its launches are latency-bound)
+        if (per_chunk < 6LL * slots && H >= 1024 && H >= 16 * L->ywarm) {
+            const std::vector<int> b = p1_plan_split(H, L->Ey, L->ywarm, per_chunk, slots);
+            L->nyc = (int)b.size() - 1;
+            L->ych_rows = 0;
+            for (int c = 0; c < L->nyc; ++c) L->ych_rows = std::max(L->ych_rows, b[c + 1] - b[c]);
+            for (int c = 0; c <= L->nyc; ++c) L->ychb[c] = b[c];
+            L->ych_lpt = L->nyc > 1;
+        }
+    }
+    if (!box) {
+        // development override: explicit chunk row counts, e.g. "1280,768"
+        // (multiples of 32, largest first; the last one takes the rest)
+        const char* ev = getenv("TBF_P1_YSPLIT");
+        if (ev && *ev) {
+            int n = 0, r = 0, mx = 0;
+            L->ychb[0] = 0;
+            for (const char* q = ev; *q && n < TBF_MAX_YCH && r < H;) {
+                int v = (int)strtol(q, (char**)&q, 10);
+                if (*q == ',') ++q;
+                v = std::max(TILE, (v + TILE - 1) / TILE * TILE);
+                if (!*q || n == TBF_MAX_YCH - 1) v = H - r;
+                v = std::min(v, H - r);
+                r += v;
+                mx = std::max(mx, v);
+                L->ychb[++n] = r;
+            }
+            if (r < H) {
+                mx = std::max(mx, H - r);
+                L->ychb[n] = H;
+            }
+            L->nyc = n;
+            L->ych_rows = mx;
+            L->ych_lpt = n > 1;
+        }
     }
     L->nseg = (L->ych_rows + std::max(L->ywarm, L->Ey) + TILE - 1) / TILE + 1;
     const size_t px = (size_t)B * H * W;
@@ -2357,7 +2553,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
     if (rc) return rc;
     const int nrange = tend - tbeg;
     Layout L;
-    rc = make_layout(B, H, W, sp, nrange, batch_terms, &L);
+    rc = make_layout(B, H, W, sp, nrange, batch_terms, &L, /*lpt=*/hio == nullptr || (g_lpt_split & 4));
     if (rc) return rc;
     if (!ws || ws_bytes < L.total)
         return fail(TBF_ERR_WORKSPACE, "workspace too small: need %zu have %zu", L.total, ws_bytes);
@@ -2505,6 +2701,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p1.nseg = L.nseg;
         p1.nyc = L.nyc;
         p1.ych_rows = L.ych_rows;
+        std::copy(L.ychb, L.ychb + TBF_MAX_YCH + 1, p1.ychb);
         p1.ywarm = L.ywarm;
         p1.Ex = L.Ex;
         p1.ne = L.ne;
@@ -2524,9 +2721,11 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         // automatic: term groups fastest when many groups share a column
         // tile's f (measured: -2.1% on config 3 with 34 groups, flat with 9,
         // +0.3% with 6)
-        p1.order = box ? 0 : (g_p1_order >= 0 ? g_p1_order : (p1.ngb >= 12 ? 1 : 0));
+        // unequal chunks: chunk index slowest, so the largest chunks go first
+        p1.order = box ? 0 : (g_p1_order >= 0 ? g_p1_order : (p1.ngb >= 12 ? 1 : (L.ych_lpt ? 3 : 0)));
         auto p1grid = [&](int ntx_run) {  // launch shape for the block order
-            return p1.order == 1 ? dim3(ntx_run * L.nyc * p1.ngb, 1, B) : dim3(ntx_run * L.nyc, p1.ngb, B);
+            return (p1.order == 1 || p1.order == 3) ? dim3(ntx_run * L.nyc * p1.ngb, 1, B)
+                                                    : dim3(ntx_run * L.nyc, p1.ngb, B);
         };
         if (!box) g1 = p1grid(L.ntx);
         const int p1smem = g_p1_occ == 2 ? P1_SMEM_OCC2 : P1_SMEM;
@@ -2659,8 +2858,56 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 nchunk *= 2;
             }
         }
+        nchunk = std::min(nchunk, TBF_MAX_XCH);
         p2.tiles_per_chunk = (L.ntx + nchunk - 1) / nchunk;
         nchunk = (L.ntx + p2.tiles_per_chunk - 1) / p2.tiles_per_chunk;
+        p2.nxc = nchunk;
+        for (int c = 0; c <= nchunk; ++c) p2.xcb[c] = std::min(L.ntx, c * p2.tiles_per_chunk);
+        for (int c = 0; c < nchunk; ++c) p2.xord[c] = c;
+        bool p2_lpt = false;
+        if (!box && p2var == 6) {
+            // development override: x-chunk widths in tiles, left to right
+            const char* ev = getenv("TBF_P2_XSPLIT");
+            if (ev && *ev) {
+                int n = 0, t = 0;
+                for (const char* q = ev; *q && n < TBF_MAX_XCH && t < L.ntx;) {
+                    int v = std::max(1, (int)strtol(q, (char**)&q, 10));
+                    if (*q == ',') ++q;
+                    if (!*q || n == TBF_MAX_XCH - 1) v = L.ntx - t;
+                    t += std::min(v, L.ntx - t);
+                    p2.xcb[++n] = t;
+                }
+                if (t < L.ntx) p2.xcb[n] = L.ntx;
+                nchunk = p2.nxc = n;
+                p2_lpt = true;
+            }
+            if (!p2_lpt && g_p2_chunks <= 0 && (g_lpt_split & 2) && (!hpipe || (g_lpt_split & 8))) {
+                // few waves: planned unequal x-chunks, costliest first
+                const int slots = 148 * 3;  // k_pass2_gr blocks resident per SM
+                const long long per_chunk = (long long)nrb * (P2_THREADS / 32) * npart * B;
+                if (per_chunk < 6LL * slots && L.ntx >= 8) {
+                    const std::vector<int> b = p2_plan_split(L.ntx, p2.warm_tiles, nchunk, per_chunk, slots);
+                    if ((int)b.size() - 1 != nchunk || b[1] != p2.xcb[1]) {
+                        nchunk = p2.nxc = (int)b.size() - 1;
+                        for (int c = 0; c <= nchunk; ++c) p2.xcb[c] = b[c];
+                        p2_lpt = true;
+                    }
+                }
+            }
+            if (p2_lpt) {
+                // dispatch the costliest chunks first (tiles incl. warm-up)
+                std::vector<std::pair<int, int>> cs;
+                for (int c = 0; c < nchunk; ++c) {
+                    const bool exact = p2.xcb[c + 1] + p2.warm_tiles >= L.ntx;
+                    const int cost = (exact ? L.ntx : p2.xcb[c + 1] + p2.warm_tiles) - p2.xcb[c];
+                    cs.push_back({-cost, c});
+                }
+                std::stable_sort(cs.begin(), cs.end());
+                for (int c = 0; c < nchunk; ++c) p2.xord[c] = cs[c].second;
+                const char* eo = getenv("TBF_P2_XORDER");
+                p2.order = (eo && *eo) ? atoi(eo) : 4;
+            }
+        }
         ReduceArgs ra;
         ra.part = part;
         ra.ngroups = npart > 0 ? npart : p2.ngroups;
@@ -2693,7 +2940,9 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 if (box)
                     k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, q>>>(p2, sp->radius);
                 else if (p2var == 6)
-                    k_pass2_gr<G2><<<dim3(nrun * (P2_THREADS / 32) * nchunk, npart, B), 32 * P2R_GR, P2R_SMEM, q>>>(p2);
+                    k_pass2_gr<G2><<<p2.order == 4 ? dim3(nrun * (P2_THREADS / 32) * nchunk * npart, 1, B)
+                                                   : dim3(nrun * (P2_THREADS / 32) * nchunk, npart, B),
+                                     32 * P2R_GR, P2R_SMEM, q>>>(p2);
                 else if (p2var == 4)
                     k_pass2_async<4><<<g2, P2_THREADS, p2a_smem_bytes<4>(), q>>>(p2);
                 else if (p2var == 5)
@@ -2801,13 +3050,16 @@ int tbf_set_option(int32_t option, int64_t value) {
             g_host_bands = (int)std::max<int64_t>(0, std::min<int64_t>(64, value));
             return TBF_OK;
         case TBF_OPT_P1_ORDER:
-            g_p1_order = (int)std::max<int64_t>(-1, std::min<int64_t>(2, value));
+            g_p1_order = (int)std::max<int64_t>(-1, std::min<int64_t>(3, value));
             return TBF_OK;
         case TBF_OPT_P2_ORDER:
             g_p2_order = (int)std::max<int64_t>(0, std::min<int64_t>(3, value));
             return TBF_OK;
         case TBF_OPT_P1_FOLD:
             g_pass1_fold = value != 0;
+            return TBF_OK;
+        case TBF_OPT_LPT_SPLIT:
+            g_lpt_split = (int)(value & 15);
             return TBF_OK;
         case TBF_OPT_BATCHES:
             if (value < 1) return fail(TBF_ERR_PARAM, "batches must be >= 1");
@@ -2872,10 +3124,13 @@ const char* tbf_last_error(void) { return g_last_error.c_str(); }
 
 size_t tbf_workspace_bytes(int32_t B, int32_t H, int32_t W, const tbf_spatial* sp,
                            int32_t term_begin, int32_t term_end, int32_t batch_terms) {
-    Layout L;
+    // large enough for both the planned (device entry) and the equal-chunk
+    // (host entry) layouts
+    Layout L, Le;
     if (term_end <= term_begin) return 0;
     if (make_layout(B, H, W, sp, term_end - term_begin, batch_terms, &L)) return 0;
-    return L.total;
+    if (make_layout(B, H, W, sp, term_end - term_begin, batch_terms, &Le, false)) return 0;
+    return std::max(L.total, Le.total);
 }
 
 int tbf_range_check(const float* f, int64_t count, double T, unsigned long long* d_counters,

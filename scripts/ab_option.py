@@ -14,12 +14,17 @@ f = torch.from_numpy(workloads.make_input(cfg, frames=min(cfg.frames, 8))).cuda(
 k = tb.make_trig_kernel(cfg.sigma_r, cfg.T)
 spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
 flush = torch.empty(128 << 20, device="cuda")
-plan = tb.TrigFilter(tuple(f.shape), spec, k)
+# one plan per value: an option may change the layout and so the workspace size
+plans = {}
+for v in (va, vb):
+    lib.tbf_set_option(opt, v)
+    plans[v] = tb.TrigFilter(tuple(f.shape), spec, k)
 out = torch.empty_like(f)
 res = {va: [], vb: []}
 for r in range(rounds):
     for v in (va, vb):
         lib.tbf_set_option(opt, v)
+        plan = plans[v]
         plan(f, out)
         for _ in range(5):
             flush.zero_()

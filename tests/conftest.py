@@ -48,3 +48,19 @@ def reference_pkg():
     import trigbf
 
     return trigbf
+
+
+@pytest.fixture
+def equal_chunks():
+    """Equal pass-1/pass-2 chunks for the device entry too (TBF_OPT_LPT_SPLIT
+    = 0), as the host entry always uses: the two entries then compute the
+    same bits.  The planned unequal chunks of the device entry change results
+    only at the warm-up truncation level (test_planned_chunks_match_equal)."""
+    from paper_1105_4204_b200 import _native
+
+    lib = _native.load()
+    lib.tbf_set_option(_native.TBF_OPT_LPT_SPLIT, 0)
+    try:
+        yield
+    finally:
+        lib.tbf_set_option(_native.TBF_OPT_LPT_SPLIT, _native.TBF_LPT_DEFAULT)

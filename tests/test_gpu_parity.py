@@ -93,9 +93,18 @@ def test_config_goldens(tb, cfg_id):
         f = torch.from_numpy(workloads.frame(cfg, fi)).cuda()
         out = tb.bilateral_trig(f, spec, k)
         if cfg_id in (1, 2) and fi == frames[0]:
-            # the host entry (pinned, strip/band overlapped) gives the same bits
+            # the host entry (pinned, strip/band overlapped) gives the same
+            # bits as the device entry with the same (equal) chunks
+            from paper_1105_4204_b200 import _native
+            lib = _native.load()
             host = tb.bilateral_trig(f.cpu().pin_memory(), spec, k)
-            assert torch.equal(host, out.cpu())
+            lib.tbf_set_option(_native.TBF_OPT_LPT_SPLIT, 0)
+            try:
+                eq = tb.bilateral_trig(f, spec, k)
+            finally:
+                lib.tbf_set_option(_native.TBF_OPT_LPT_SPLIT, _native.TBF_LPT_DEFAULT)
+            assert torch.equal(host, eq.cpu())
+            del eq
         sel = g["frame"] == fi
         got = out[torch.from_numpy(g["y"][sel]).cuda(), torch.from_numpy(g["x"][sel]).cuda()]
         err = float(np.max(np.abs(got.double().cpu().numpy() - g["value"][sel])))
@@ -238,10 +247,11 @@ def test_other_intensity_ranges_match_oracle(tb, orc, T, sigma_r, sigma_s):
     assert np.max(np.abs(got - ref)) <= 1e-3 * T, (T, np.max(np.abs(got - ref)))
 
 
-def test_full_size_runs_bit_identical(tb):
+def test_full_size_runs_bit_identical(tb, equal_chunks):
     """Determinism at the config-2 size, through both entries: repeated device
     calls, a fresh plan, and the pinned host entry give the same bits (fixed
-    term order, fixed-shape block sums, no float atomics)."""
+    term order, fixed-shape block sums, no float atomics; equal chunks in both
+    entries, see test_planned_chunks_match_equal for the planned layout)."""
     from paper_1105_4204_b200 import workloads
 
     cfg = workloads.CONFIGS[2]
@@ -525,7 +535,7 @@ def test_pinned_host_batch_streamed_matches_device(tb):
     ((2, 200, 130), 4, 4),     # two frames, strips of 2 tiles, more bands than row blocks
     ((1, 2048, 2048), 4, 4),   # the config-2 shape
 ])
-def test_host_entry_matches_device(tb, shape, strips, bands):
+def test_host_entry_matches_device(tb, shape, strips, bands, equal_chunks):
     """tbf_bilateral_trig_host (strip-wise copies + pass 1, band-wise pass 2 +
     copies back) computes exactly what the device-resident call computes:
     the same kernels over the same columns / rows, only split across launches."""
@@ -616,7 +626,7 @@ def test_sharded_paths_over_nccl_world1(tb):
     ((1, 70, 45), "box", 9, 40.0),
     ((3, 129, 257), "gauss-recursive", 16.0, 10.0),
 ])
-def test_no_writes_outside_buffers(tb, shape, kind, param, sigma_r):
+def test_no_writes_outside_buffers(tb, shape, kind, param, sigma_r, equal_chunks):
     """Out-of-bounds checks without a sanitizer: every buffer handed to
     the C ABI (workspace, output, counters, the host entry's device buffer)
     sits between canary margins that must survive, and the const input must
@@ -687,7 +697,7 @@ def test_extreme_aspect_ratios(tb, orc, shape, sigma_s):
     assert np.max(np.abs(got - ref)) <= TOL
 
 
-def test_large_batch_of_small_frames(tb, orc):
+def test_large_batch_of_small_frames(tb, orc, equal_chunks):
     """300 frames of 20x30 in one call (grid z = frames; host staging path for
     NumPy input) equal per-frame oracle results."""
     rng = np.random.default_rng(300)
@@ -735,3 +745,30 @@ def test_plan_captured_in_cuda_graph(tb):
     torch.cuda.synchronize()
     assert torch.equal(out, ref_b)
     plan.read_counters()
+
+
+@pytest.mark.parametrize("cfg_id", [2, 3])
+def test_planned_chunks_match_equal(tb, cfg_id):
+    """The device entry's planned unequal y-/x-chunks (list-scheduled,
+    costliest first) start their recursions from epsilon-decayed warm-ups like
+    the equal chunks do: on the config's full image the two layouts agree to
+    the warm-up truncation level (well inside 1e-2), and the planned result is
+    deterministic."""
+    from paper_1105_4204_b200 import _native, workloads
+
+    lib = _native.load()
+    cfg = workloads.CONFIGS[cfg_id]
+    f = torch.from_numpy(workloads.frame(cfg, 0)).cuda()
+    k = tb.make_trig_kernel(cfg.sigma_r, cfg.T)
+    spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
+    planned = tb.bilateral_trig(f, spec, k)
+    again = tb.bilateral_trig(f, spec, k)
+    lib.tbf_set_option(_native.TBF_OPT_LPT_SPLIT, 0)
+    try:
+        equal = tb.bilateral_trig(f, spec, k)
+    finally:
+        lib.tbf_set_option(_native.TBF_OPT_LPT_SPLIT, _native.TBF_LPT_DEFAULT)
+    assert torch.equal(planned, again)
+    d = float((planned - equal).abs().max())
+    print(f"config {cfg_id}: planned vs equal chunks max abs diff {d:.3g}")
+    assert d < 1e-2
