@@ -197,7 +197,7 @@ TBF_API int32_t tbf_profile_timeline(double* start_ms, double* dur_ms, int32_t* 
                                 x-chunks of unequal size, dispatched costliest first, planned by a
                                 list-scheduling model; 0 = equal chunks */
 #define TBF_OPT_P1_ORDER 10 /* block order of pass 1: -1 (default) automatic, 0 column tile fastest,
-                               1 term group fastest, 2 y-chunk fastest, 3 y-chunk slowest */
+                               1 term group fastest, 2 y-chunk fastest */
 #define TBF_OPT_P2_ORDER 9  /* block order of the block-summed pass 2: 0 (default) row fastest, 1 x-chunk fastest, 2/3 reversed */
 #define TBF_OPT_P1_FOLD 6   /* default 1: folds the y-sweep gain into the pass-2 weights
                                (skips 4 multiplies per pixel-term in pass 1 when T/g^4 is safe); 0 scales in pass 1 */

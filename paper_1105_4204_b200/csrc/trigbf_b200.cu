@@ -89,7 +89,6 @@ __host__ __device__ __forceinline__ size_t xm_plane(int B, int W, int H) {
     return (size_t)B * ((H + FL_RB - 1) / FL_RB) * FL_RB * W;
 }
 constexpr int TBF_MAX_YCH = 16;      // most y-chunks per pass-1 column
-constexpr int TBF_MAX_XCH = 64;      // most x-chunks per pass-2 row
 constexpr int P1_BLOCKS_PER_SM = 3;  // smem-limited residency of pass-1 blocks (4 warps, 67.6 KB)
 constexpr int BUF_LD = TILE + 1;  // padded leading dimension of the smem tile
 
@@ -382,7 +381,10 @@ struct Pass1Args {
     int B, H, W;
     int Ey, nseg;  // y mirror extension; checkpoint segments per y-chunk
     int nyc, ych_rows, ywarm;  // y-chunks (at most ych_rows output rows each); warm-up rows (mult. of 32)
-    int ychb[TBF_MAX_YCH + 1];  // chunk c covers output rows [ychb[c], ychb[c+1]) (multiples of 32)
+    // unequal chunks (ylpt, at most 3): rows [0, yb1), [yb1, yb2), [yb2, H);
+    // scalars, not a table: a dynamically indexed parameter array made ptxas
+    // spill in this kernel (9% slower pass 1 on config 5)
+    int ylpt, yb1, yb2;
     int Ex, ne, edge_all, ntx;
     int tile0, ntx_run;  // column tiles [tile0, tile0 + ntx_run) in this launch
     int order, ngb;      // block order (TBF_OPT_P1_ORDER); term-group blocks
@@ -423,9 +425,11 @@ struct Pass2Args {
     float wscale;      // g^2: undoes the two pure x sweeps (1 for box)
     int rb0, nrb_run;     // 128-row blocks [rb0, rb0 + nrb_run) in this launch
     int tiles_per_chunk;  // x-chunking of rows (gauss); == ntx for one chunk
-    int nxc;              // x-chunks (k_pass2_gr: chunk c covers tiles [xcb[c], xcb[c+1]))
-    int xcb[TBF_MAX_XCH + 1];
-    int xord[TBF_MAX_XCH];  // k_pass2_gr order 4: dispatch rank -> chunk (costliest first)
+    // unequal x-chunks (xlpt, at most 3): tiles [0, xb1), [xb1, xb2), [xb2, ntx),
+    // dispatched in the order packed in xord (2 bits per rank, costliest
+    // first); scalars rather than tables (dynamically indexed parameter
+    // arrays cost registers)
+    int xlpt, xb1, xb2, xord;
     int warm_tiles;       // warm-up tiles of a chunk's backward sweep
     const float* floc;
     const float* carry;   // chained carries float4 [n][B][ntx][H][4]
@@ -481,7 +485,9 @@ __device__ __forceinline__ void p1_fwd8(const float (&fv)[8], float nu_hi, float
 // FOLD: the g^2 that undoes the two pure y sweeps is folded into the pass-2
 // weights (g^4 there) instead of one multiply per plane-sample here; used when
 // T/g^4 stays far from the fp32 range limit.
-template <bool FOLD>
+// LPT: unequal y-chunks (ylpt/yb1/yb2); the equal-chunk instantiation keeps
+// the chunk arithmetic rematerialisable (no extra live registers)
+template <bool FOLD, bool LPT>
 __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss(const __grid_constant__ Pass1Args a) {
     extern __shared__ float smem[];
     const int lane = threadIdx.x & 31;
@@ -500,12 +506,6 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
         chunk = blockIdx.x % a.nyc;
         tile_r = blockIdx.x / a.nyc;
         gblk = blockIdx.y;
-    } else if (a.order == 3) {  // column tile fastest, then term group; y-chunk slowest
-        int idx = blockIdx.x;
-        tile_r = idx % a.ntx_run;
-        idx /= a.ntx_run;
-        gblk = idx % a.ngb;
-        chunk = idx / a.ngb;
     } else {
         tile_r = blockIdx.x % a.ntx_run;
         chunk = blockIdx.x / a.ntx_run;
@@ -539,8 +539,14 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     // ywarm from a steady-state guess (exact -Ey start for the top chunk); the
     // backward starts at Bend = R1 + ywarm (exact H+Ey end for the bottom
     // chunk).  ywarm >= the decay length K, so guesses fade below eps.
-    const int R0 = a.ychb[chunk];
-    const int R1 = a.ychb[chunk + 1];
+    int R0, R1;
+    if (LPT) {
+        R0 = chunk == 0 ? 0 : (chunk == 1 ? a.yb1 : a.yb2);
+        R1 = chunk == 0 ? a.yb1 : (chunk == 1 ? a.yb2 : H);
+    } else {
+        R0 = chunk * a.ych_rows;
+        R1 = min(H, R0 + a.ych_rows);
+    }
     const int A0 = R0 - a.ywarm <= 0 ? -Ey : R0 - a.ywarm;
     const int Bend = R1 + a.ywarm >= iend ? iend : R1 + a.ywarm;
     // checkpoints: float4 per plane, [chunk*nseg + local seg][term][b][x][4]
@@ -1498,21 +1504,22 @@ constexpr int P2R_GR = 4;
 
 constexpr int P2R_SMEM = 2 * P2R_GR * TILE * 32 * 8;  // double-buffered float2 [2][warp][x][row]
 
-template <int G>
+// LPT: unequal x-chunks (xlpt/xb1/xb2, dispatch order 4)
+template <int G, bool LPT>
 __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_constant__ Pass2Args a) {
     extern __shared__ float2 sdyn[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nsb = a.nrb_run * (P2_THREADS / 32);  // 32-row sub-blocks in this launch
-    const int nch = a.nxc;
+    const int nch = gridDim.x / nsb;
     int chunk, rsb;
     int gy = blockIdx.y;  // group block
-    if (a.order == 4) {  // 1-D grid, chunk slowest (in xord order), then group block, row sub-block
+    if (LPT) {  // 1-D grid, chunk slowest (in xord order), then group block, row sub-block
         const int npb = (a.ngroups + P2R_GR - 1) / P2R_GR;
         int idx = blockIdx.x;
         rsb = idx % nsb;
         idx /= nsb;
         gy = idx % npb;
-        chunk = a.xord[idx / npb];
+        chunk = (a.xord >> (2 * (idx / npb))) & 3;
     } else if (a.order == 1) {  // x-chunk fastest: both chunks of a row block together
         chunk = blockIdx.x % nch;
         rsb = blockIdx.x / nch;
@@ -1521,9 +1528,6 @@ __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_consta
         rsb = nsb - 1 - blockIdx.x % nsb;
     } else if (a.order == 3) {  // chunks reversed (rightmost, exact-start chunk first)
         chunk = nch - 1 - blockIdx.x / nsb;
-        rsb = blockIdx.x % nsb;
-    } else if (a.order == 5) {  // default grid, chunks in xord order (costliest first)
-        chunk = a.xord[blockIdx.x / nsb];
         rsb = blockIdx.x % nsb;
     } else {
         chunk = blockIdx.x / nsb;
@@ -1561,8 +1565,14 @@ __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_consta
     // buffer written next was last read before the previous barrier)
     auto sbuf = [&](int buf, int q, int m) -> float2& { return sdyn[((buf * P2R_GR + q) * TILE + m) * 32 + lane]; };
 
-    const int t_lo = a.xcb[chunk];
-    const int t_hi = a.xcb[chunk + 1];  // exclusive
+    int t_lo, t_hi;  // exclusive
+    if (LPT) {
+        t_lo = chunk == 0 ? 0 : (chunk == 1 ? a.xb1 : a.xb2);
+        t_hi = chunk == 0 ? a.xb1 : (chunk == 1 ? a.xb2 : a.ntx);
+    } else {
+        t_lo = chunk * a.tiles_per_chunk;
+        t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);
+    }
     float p1[G][4], p2[G][4], q1[G][4], q2[G][4];
     if (active) {
         const bool exact_start = t_hi + a.warm_tiles >= a.ntx;
@@ -2228,10 +2238,11 @@ std::vector<int> p1_plan_split(int H, int Ey, int ywarm, long long per_chunk, in
     return best;
 }
 
-// lpt: allow the planned unequal y-chunks (full-image launches; the host
-// entry's strip-wise pass 1 keeps equal chunks)
+// lpt: 0 equal y-chunks (the host entry's strip-wise pass 1), 1 planned
+// unequal chunks when TBF_OPT_LPT_SPLIT enables them, 2 planned regardless of
+// the option (workspace sizing: a plan must fit whatever the option is later)
 int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, int batch_terms,
-                Layout* L, bool lpt = true) {
+                Layout* L, int lpt = 1) {
     if (B < 1 || H < 1 || W < 1) return fail(TBF_ERR_DIM, "bad shape B=%d H=%d W=%d", B, H, W);
     if (!sp) return fail(TBF_ERR_PARAM, "null spatial");
     L->B = B;
@@ -2291,7 +2302,10 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     }
     for (int c = 0; c <= L->nyc; ++c) L->ychb[c] = std::min(H, c * L->ych_rows);
     L->ych_lpt = false;
-    if (!box && g_p1_ychunks <= 0 && (g_lpt_split & 1) && lpt) {
+    // single-batch runs only: the workspace of batched runs stays affine in
+    // the batch size (the engine's batch picker fits it), and their launches
+    // are many waves anyway (config 5)
+    if (!box && g_p1_ychunks <= 0 && (lpt == 2 || (lpt == 1 && (g_lpt_split & 1))) && L->nb == 1) {
         // few waves: plan unequal chunks, largest first (p1_plan_split)
         const int slots = 148 * P1_BLOCKS_PER_SM;
         const long long per_chunk = (long long)L->ntx * ((tb + P1_WARPS - 1) / P1_WARPS) * B;
@@ -2313,11 +2327,11 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
         if (ev && *ev) {
             int n = 0, r = 0, mx = 0;
             L->ychb[0] = 0;
-            for (const char* q = ev; *q && n < TBF_MAX_YCH && r < H;) {
+            for (const char* q = ev; *q && n < 3 && r < H;) {  // at most 3 chunks
                 int v = (int)strtol(q, (char**)&q, 10);
                 if (*q == ',') ++q;
                 v = std::max(TILE, (v + TILE - 1) / TILE * TILE);
-                if (!*q || n == TBF_MAX_YCH - 1) v = H - r;
+                if (!*q || n == 2) v = H - r;
                 v = std::min(v, H - r);
                 r += v;
                 mx = std::max(mx, v);
@@ -2509,12 +2523,26 @@ void set_p1_smem() {
                          p2t_smem_bytes<G2>());
     cudaFuncSetAttribute(k_pass2_tma<G2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          p2t_smem_bytes<G2>());
-    cudaFuncSetAttribute(k_pass2_gr<G2>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2R_SMEM);
-    cudaFuncSetAttribute(k_pass1_gauss<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
-    cudaFuncSetAttribute(k_pass1_gauss<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
+    cudaFuncSetAttribute(k_pass2_gr<G2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2R_SMEM);
+    cudaFuncSetAttribute(k_pass2_gr<G2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2R_SMEM);
+    cudaFuncSetAttribute(k_pass1_gauss<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
+    cudaFuncSetAttribute(k_pass1_gauss<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
+    cudaFuncSetAttribute(k_pass1_gauss<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
+    cudaFuncSetAttribute(k_pass1_gauss<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
     cudaFuncSetAttribute(k_pass1_box<G1, R_ANCHOR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          P1_SMEM);
     done = true;
+}
+
+void launch_pass1(bool fold, bool lpt, dim3 grid, int smem, cudaStream_t st, const Pass1Args& p1) {
+    if (fold && lpt)
+        k_pass1_gauss<true, true><<<grid, P1_WARPS * 32, smem, st>>>(p1);
+    else if (fold)
+        k_pass1_gauss<true, false><<<grid, P1_WARPS * 32, smem, st>>>(p1);
+    else if (lpt)
+        k_pass1_gauss<false, true><<<grid, P1_WARPS * 32, smem, st>>>(p1);
+    else
+        k_pass1_gauss<false, false><<<grid, P1_WARPS * 32, smem, st>>>(p1);
 }
 
 // Core driver: pairs [tbeg, tend) in batches of L.tb terms.  Either
@@ -2553,7 +2581,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
     if (rc) return rc;
     const int nrange = tend - tbeg;
     Layout L;
-    rc = make_layout(B, H, W, sp, nrange, batch_terms, &L, /*lpt=*/hio == nullptr || (g_lpt_split & 4));
+    rc = make_layout(B, H, W, sp, nrange, batch_terms, &L, (hio == nullptr || (g_lpt_split & 4)) ? 1 : 0);
     if (rc) return rc;
     if (!ws || ws_bytes < L.total)
         return fail(TBF_ERR_WORKSPACE, "workspace too small: need %zu have %zu", L.total, ws_bytes);
@@ -2701,7 +2729,9 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p1.nseg = L.nseg;
         p1.nyc = L.nyc;
         p1.ych_rows = L.ych_rows;
-        std::copy(L.ychb, L.ychb + TBF_MAX_YCH + 1, p1.ychb);
+        p1.ylpt = L.ych_lpt;
+        p1.yb1 = L.nyc > 1 ? L.ychb[1] : H;
+        p1.yb2 = L.nyc > 2 ? L.ychb[2] : H;
         p1.ywarm = L.ywarm;
         p1.Ex = L.Ex;
         p1.ne = L.ne;
@@ -2721,11 +2751,12 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         // automatic: term groups fastest when many groups share a column
         // tile's f (measured: -2.1% on config 3 with 34 groups, flat with 9,
         // +0.3% with 6)
-        // unequal chunks: chunk index slowest, so the largest chunks go first
-        p1.order = box ? 0 : (g_p1_order >= 0 ? g_p1_order : (p1.ngb >= 12 ? 1 : (L.ych_lpt ? 3 : 0)));
+        // unequal chunks: order 1 (y-chunk index slowest), so the largest
+        // chunks go first (measured on config 2: order 1 as fast as tile-fastest
+        // with the chunk slowest, and a separate decode branch cost registers)
+        p1.order = box ? 0 : (g_p1_order >= 0 ? g_p1_order : ((p1.ngb >= 12 || L.ych_lpt) ? 1 : 0));
         auto p1grid = [&](int ntx_run) {  // launch shape for the block order
-            return (p1.order == 1 || p1.order == 3) ? dim3(ntx_run * L.nyc * p1.ngb, 1, B)
-                                                    : dim3(ntx_run * L.nyc, p1.ngb, B);
+            return p1.order == 1 ? dim3(ntx_run * L.nyc * p1.ngb, 1, B) : dim3(ntx_run * L.nyc, p1.ngb, B);
         };
         if (!box) g1 = p1grid(L.ntx);
         const int p1smem = g_p1_occ == 2 ? P1_SMEM_OCC2 : P1_SMEM;
@@ -2746,10 +2777,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 dim3 gs = p1grid(p1.ntx_run);
                 {
                     Prof pr(KK_PASS1, ps);
-                    if (fold)
-                        k_pass1_gauss<true><<<gs, P1_WARPS * 32, p1smem, ps>>>(p1);
-                    else
-                        k_pass1_gauss<false><<<gs, P1_WARPS * 32, p1smem, ps>>>(p1);
+                    launch_pass1(fold, p1.ylpt != 0, gs, p1smem, ps, p1);
                 }
                 cudaEvent_t e = event_get();
                 cudaEventRecord(e, ps);
@@ -2761,10 +2789,8 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             Prof pr(KK_PASS1, st);
             if (box)
                 k_pass1_box<G1, R_ANCHOR><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1, sp->radius);
-            else if (fold)
-                k_pass1_gauss<true><<<g1, P1_WARPS * 32, p1smem, st>>>(p1);
             else
-                k_pass1_gauss<false><<<g1, P1_WARPS * 32, p1smem, st>>>(p1);
+                launch_pass1(fold, p1.ylpt != 0, g1, p1smem, st, p1);
         }
         if ((rc = check_cuda("pass1"))) return rc;
         if (s2 != st) {  // hand the batch to the second stream
@@ -2858,54 +2884,43 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 nchunk *= 2;
             }
         }
-        nchunk = std::min(nchunk, TBF_MAX_XCH);
         p2.tiles_per_chunk = (L.ntx + nchunk - 1) / nchunk;
         nchunk = (L.ntx + p2.tiles_per_chunk - 1) / p2.tiles_per_chunk;
-        p2.nxc = nchunk;
-        for (int c = 0; c <= nchunk; ++c) p2.xcb[c] = std::min(L.ntx, c * p2.tiles_per_chunk);
-        for (int c = 0; c < nchunk; ++c) p2.xord[c] = c;
-        bool p2_lpt = false;
-        if (!box && p2var == 6) {
-            // development override: x-chunk widths in tiles, left to right
+        p2.xlpt = 0;
+        if (!box && p2var == 6 && nb == 1) {
+            // unequal x-chunks (at most 3), costliest first: the development
+            // override TBF_P2_XSPLIT (widths in tiles, left to right), else
+            // the planner for launches of a few waves (device entry only: the
+            // host entry's band launches want short blocks, measured +14%)
+            std::vector<int> b;
             const char* ev = getenv("TBF_P2_XSPLIT");
             if (ev && *ev) {
-                int n = 0, t = 0;
-                for (const char* q = ev; *q && n < TBF_MAX_XCH && t < L.ntx;) {
+                b.push_back(0);
+                for (const char* q = ev; *q && b.size() < 4 && b.back() < L.ntx;) {
                     int v = std::max(1, (int)strtol(q, (char**)&q, 10));
                     if (*q == ',') ++q;
-                    if (!*q || n == TBF_MAX_XCH - 1) v = L.ntx - t;
-                    t += std::min(v, L.ntx - t);
-                    p2.xcb[++n] = t;
+                    b.push_back((!*q || b.size() == 3) ? L.ntx : std::min(L.ntx, b.back() + v));
                 }
-                if (t < L.ntx) p2.xcb[n] = L.ntx;
-                nchunk = p2.nxc = n;
-                p2_lpt = true;
-            }
-            if (!p2_lpt && g_p2_chunks <= 0 && (g_lpt_split & 2) && (!hpipe || (g_lpt_split & 8))) {
-                // few waves: planned unequal x-chunks, costliest first
+                if (b.back() < L.ntx) b.back() = L.ntx;
+            } else if (g_p2_chunks <= 0 && (g_lpt_split & 2) && (!hpipe || (g_lpt_split & 8))) {
                 const int slots = 148 * 3;  // k_pass2_gr blocks resident per SM
                 const long long per_chunk = (long long)nrb * (P2_THREADS / 32) * npart * B;
                 if (per_chunk < 6LL * slots && L.ntx >= 8) {
-                    const std::vector<int> b = p2_plan_split(L.ntx, p2.warm_tiles, nchunk, per_chunk, slots);
-                    if ((int)b.size() - 1 != nchunk || b[1] != p2.xcb[1]) {
-                        nchunk = p2.nxc = (int)b.size() - 1;
-                        for (int c = 0; c <= nchunk; ++c) p2.xcb[c] = b[c];
-                        p2_lpt = true;
-                    }
+                    b = p2_plan_split(L.ntx, p2.warm_tiles, nchunk, per_chunk, slots);
+                    if (b.size() > 4 || (int)b.size() - 1 == nchunk) b.clear();  // equal split kept
                 }
             }
-            if (p2_lpt) {
-                // dispatch the costliest chunks first (tiles incl. warm-up)
-                std::vector<std::pair<int, int>> cs;
-                for (int c = 0; c < nchunk; ++c) {
-                    const bool exact = p2.xcb[c + 1] + p2.warm_tiles >= L.ntx;
-                    const int cost = (exact ? L.ntx : p2.xcb[c + 1] + p2.warm_tiles) - p2.xcb[c];
-                    cs.push_back({-cost, c});
-                }
+            if (b.size() >= 3) {
+                nchunk = (int)b.size() - 1;
+                p2.xlpt = 1;
+                p2.xb1 = b[1];
+                p2.xb2 = nchunk > 2 ? b[2] : L.ntx;
+                std::vector<std::pair<double, int>> cs;
+                for (int c = 0; c < nchunk; ++c) cs.push_back({-p2_chunk_cost(b[c], b[c + 1], L.ntx, p2.warm_tiles), c});
                 std::stable_sort(cs.begin(), cs.end());
-                for (int c = 0; c < nchunk; ++c) p2.xord[c] = cs[c].second;
-                const char* eo = getenv("TBF_P2_XORDER");
-                p2.order = (eo && *eo) ? atoi(eo) : 4;
+                p2.xord = 0;
+                for (int r = 0; r < nchunk; ++r) p2.xord |= cs[r].second << (2 * r);
+                p2.order = 4;
             }
         }
         ReduceArgs ra;
@@ -2940,9 +2955,14 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 if (box)
                     k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, q>>>(p2, sp->radius);
                 else if (p2var == 6)
-                    k_pass2_gr<G2><<<p2.order == 4 ? dim3(nrun * (P2_THREADS / 32) * nchunk * npart, 1, B)
-                                                   : dim3(nrun * (P2_THREADS / 32) * nchunk, npart, B),
-                                     32 * P2R_GR, P2R_SMEM, q>>>(p2);
+                {
+                    if (p2.xlpt)
+                        k_pass2_gr<G2, true><<<dim3(nrun * (P2_THREADS / 32) * nchunk * npart, 1, B), 32 * P2R_GR,
+                                               P2R_SMEM, q>>>(p2);
+                    else
+                        k_pass2_gr<G2, false><<<dim3(nrun * (P2_THREADS / 32) * nchunk, npart, B), 32 * P2R_GR,
+                                                P2R_SMEM, q>>>(p2);
+                }
                 else if (p2var == 4)
                     k_pass2_async<4><<<g2, P2_THREADS, p2a_smem_bytes<4>(), q>>>(p2);
                 else if (p2var == 5)
@@ -3050,7 +3070,7 @@ int tbf_set_option(int32_t option, int64_t value) {
             g_host_bands = (int)std::max<int64_t>(0, std::min<int64_t>(64, value));
             return TBF_OK;
         case TBF_OPT_P1_ORDER:
-            g_p1_order = (int)std::max<int64_t>(-1, std::min<int64_t>(3, value));
+            g_p1_order = (int)std::max<int64_t>(-1, std::min<int64_t>(2, value));
             return TBF_OK;
         case TBF_OPT_P2_ORDER:
             g_p2_order = (int)std::max<int64_t>(0, std::min<int64_t>(3, value));
@@ -3128,8 +3148,8 @@ size_t tbf_workspace_bytes(int32_t B, int32_t H, int32_t W, const tbf_spatial* s
     // (host entry) layouts
     Layout L, Le;
     if (term_end <= term_begin) return 0;
-    if (make_layout(B, H, W, sp, term_end - term_begin, batch_terms, &L)) return 0;
-    if (make_layout(B, H, W, sp, term_end - term_begin, batch_terms, &Le, false)) return 0;
+    if (make_layout(B, H, W, sp, term_end - term_begin, batch_terms, &L, 2)) return 0;
+    if (make_layout(B, H, W, sp, term_end - term_begin, batch_terms, &Le, 0)) return 0;
     return std::max(L.total, Le.total);
 }
 
