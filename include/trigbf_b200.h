@@ -31,7 +31,7 @@
  *   tbf_bilateral_direct engines.py:120-151  bilateral_direct(img, spatial, range_fn)
  *                        (fp64 brute force; Gaussian kernels.py:174-182 or
  *                        raised cosine kernels.py:161-171 range kernel)
- *   tbf_workspace_bytes, tbf_set_option, tbf_profile_*, tbf_last_error,
+ *   tbf_workspace_bytes, tbf_layout_info, tbf_set_option, tbf_profile_*, tbf_last_error,
  *   tbf_abi_version      (new: sizing, tuning, per-kernel timing, errors)
  */
 #ifndef TRIGBF_B200_H
@@ -89,6 +89,19 @@ typedef struct tbf_terms {
     double dnu;           /* 2*omega */
     double T;             /* declared intensity range */
 } tbf_terms;
+
+/* Launch layout a call would use (no GPU needed; for tests and tuning).
+ * host_entry != 0: the layout of tbf_bilateral_trig_host.  Fills
+ * info[TBF_LAYOUT_INFO_N]: term batches, terms per batch, pass-1 y-chunks,
+ * planned unequal y-chunks (0/1), first two y-chunk ends (rows; H when absent),
+ * largest y-chunk (rows), pass-2 x-chunks of the first batch, planned unequal
+ * x-chunks (0/1), first two x-chunk ends (column tiles), equal-chunk width
+ * (tiles), dispatch order of planned x-chunks (2 bits per rank), column tiles.
+ * Returns TBF_OK or an error code. */
+#define TBF_LAYOUT_INFO_N 14
+TBF_API int tbf_layout_info(int32_t B, int32_t H, int32_t W, const tbf_spatial* sp, int32_t term_begin,
+                            int32_t term_end, int32_t batch_terms, int32_t host_entry, int32_t* info,
+                            int32_t n_info);
 
 /* Device workspace needed by tbf_bilateral_trig / tbf_trig_partial for the
  * given shape and term range.  batch_terms <= 0 selects all terms at once. */

@@ -16,6 +16,7 @@ from .engines import (
     bilateral_trig_color,
     clear_plans,
     get_plan,
+    layout_info,
 )
 from .errors import DimensionError, NativeUnavailableError, ParameterError, PnmParseError, TrigbfError
 from .image import ErrorStats, Image, error_stats, image_from_planes
@@ -50,6 +51,6 @@ __all__ = [
     "ErrorStats", "GaussianRange", "Image", "NativeUnavailableError", "ParameterError", "PnmParseError", "SpatialKind",
     "SpatialSpec", "TermPairs", "TrigFilter", "TrigKernel", "TrigbfError", "bilateral_color",
     "bilateral_direct", "bilateral_trig", "bilateral_trig_color", "clear_plans", "decay_length", "degree_estimate", "error_stats",
-    "gaussian_eval", "gaussian_taps", "get_plan", "image_from_planes", "make_trig_kernel", "recursive_biquads",
+    "gaussian_eval", "gaussian_taps", "get_plan", "image_from_planes", "layout_info", "make_trig_kernel", "recursive_biquads",
     "read_pnm", "recursive_coeffs", "select_degree", "term_pairs", "trig_eval", "window_taps", "write_pnm",
 ]

@@ -36,6 +36,9 @@ TBF_OPT_P2_ORDER = 9
 TBF_OPT_P1_ORDER = 10
 TBF_OPT_LPT_SPLIT = 11  # bits 1/2: planned y-/x-chunks (device entry); 4/8: also in the host entry
 TBF_LPT_DEFAULT = 3
+TBF_LAYOUT_INFO_N = 14
+LAYOUT_INFO_FIELDS = ("batches", "batch_terms", "y_chunks", "y_planned", "y_end0", "y_end1", "y_rows_max",
+                      "x_chunks", "x_planned", "x_end0", "x_end1", "x_tiles_equal", "x_order", "tiles")
 
 TBF_SPATIAL_RECURSIVE = 0
 TBF_SPATIAL_BOX = 1
@@ -43,6 +46,7 @@ TBF_SPATIAL_BOX = 1
 # Every symbol the header declares (checked by tests/test_abi.py).
 EXPORTS = (
     "tbf_workspace_bytes",
+    "tbf_layout_info",
     "tbf_bilateral_trig",
     "tbf_bilateral_trig_host",
     "tbf_bilateral_direct",
@@ -105,6 +109,9 @@ def _declare(lib):
     lib.tbf_last_error.argtypes = []
     lib.tbf_workspace_bytes.restype = _sz
     lib.tbf_workspace_bytes.argtypes = [_i32, _i32, _i32, ctypes.POINTER(TbfSpatial), _i32, _i32, _i32]
+    lib.tbf_layout_info.restype = ctypes.c_int
+    lib.tbf_layout_info.argtypes = [_i32, _i32, _i32, ctypes.POINTER(TbfSpatial), _i32, _i32, _i32, _i32,
+                                    ctypes.POINTER(_i32), _i32]
     lib.tbf_bilateral_trig.restype = ctypes.c_int
     lib.tbf_bilateral_trig.argtypes = [
         _vp, _vp, _i32, _i32, _i32, ctypes.POINTER(TbfSpatial), ctypes.POINTER(TbfTerms), _i32,

@@ -2534,6 +2534,90 @@ void set_p1_smem() {
     done = true;
 }
 
+
+// Pass-2 x-chunking of one batch's launch: equal chunks when rows x groups
+// cannot fill the GPU (fitted heuristic), or for the device entry's
+// single-batch runs of a few waves the planned unequal split (p2_plan_split,
+// at most 3 chunks, costliest first).  `ngroups` thread groups of g2run terms,
+// `npart` k_pass2_gr group blocks (p2var 6).
+struct P2Plan {
+    int nchunk, tiles_per_chunk, warm_tiles;
+    int xlpt, xb1, xb2, xord;
+};
+P2Plan p2_chunk_plan(const Layout& L, const tbf_spatial* sp, int ngroups, int npart, int g2run, int p2var,
+                     bool hpipe) {
+    const bool box = sp->kind == TBF_SPATIAL_BOX;
+    const int B = L.B, nrb = (L.H + P2_THREADS - 1) / P2_THREADS;
+    P2Plan pp{};
+    int nchunk = 1;
+    pp.warm_tiles = (std::max(sp->ext_x, 1) + TILE - 1) / TILE;
+    if (box) {
+        const long long threads = (long long)nrb * P2_THREADS * ngroups * B;
+        const long long target = 148LL * 12 * 32 * 3 / 2;
+        const int win = 2 * sp->radius + 1;
+        while (threads * nchunk < target && nchunk < 64) {
+            const int cols = (L.ntx + 2 * nchunk - 1) / (2 * nchunk) * TILE;
+            if (cols < 4 * win) break;  // window init <= 25% of a chunk
+            nchunk *= 2;
+        }
+    } else if (g_p2_chunks > 0) {
+        nchunk = std::min(g_p2_chunks, L.ntx);
+    } else {
+        const long long threads = (long long)nrb * P2_THREADS * ngroups * B;
+        const long long target = 148LL * 12 * 32 * 3 / 2;  // ~1.5 waves of 12 warps/SM
+        const long long wave = 148LL * 12 * 32;
+        // measured: G=4 prefers fewer, longer rows unless the GPU is far from full
+        const int max_chunks = (g2run == 4 && threads * 2 >= wave) ? 2 : 64;
+        while (threads * nchunk < target && nchunk < max_chunks) {
+            const int tpc = (L.ntx + 2 * nchunk - 1) / (2 * nchunk);
+            // warm-up <= 25% of a chunk; below one wave (latency-bound small
+            // images) accept warm-up up to the chunk length
+            const bool ok = tpc >= 4 * pp.warm_tiles || (threads * nchunk < wave && tpc >= pp.warm_tiles);
+            if (!ok) break;
+            nchunk *= 2;
+        }
+    }
+    pp.tiles_per_chunk = (L.ntx + nchunk - 1) / nchunk;
+    nchunk = (L.ntx + pp.tiles_per_chunk - 1) / pp.tiles_per_chunk;
+    pp.nchunk = nchunk;
+    if (box || p2var != 6 || L.nb != 1) return pp;
+    // unequal x-chunks (at most 3), costliest first: the development override
+    // TBF_P2_XSPLIT (widths in tiles, left to right), else the planner for
+    // launches of a few waves (device entry only: the host entry's band
+    // launches want short blocks, measured +14%)
+    std::vector<int> b;
+    const char* ev = getenv("TBF_P2_XSPLIT");
+    if (ev && *ev) {
+        b.push_back(0);
+        for (const char* q = ev; *q && b.size() < 4 && b.back() < L.ntx;) {
+            int v = std::max(1, (int)strtol(q, (char**)&q, 10));
+            if (*q == ',') ++q;
+            b.push_back((!*q || b.size() == 3) ? L.ntx : std::min(L.ntx, b.back() + v));
+        }
+        if (b.back() < L.ntx) b.back() = L.ntx;
+    } else if (g_p2_chunks <= 0 && (g_lpt_split & 2) && (!hpipe || (g_lpt_split & 8))) {
+        const int slots = 148 * 3;  // k_pass2_gr blocks resident per SM
+        const long long per_chunk = (long long)nrb * (P2_THREADS / 32) * npart * B;
+        if (per_chunk < 6LL * slots && L.ntx >= 8) {
+            b = p2_plan_split(L.ntx, pp.warm_tiles, nchunk, per_chunk, slots);
+            bool equal = (int)b.size() - 1 == nchunk;  // the planner kept the equal split
+            for (int c = 0; equal && c <= nchunk; ++c) equal = b[c] == std::min(L.ntx, c * pp.tiles_per_chunk);
+            if (equal || b.size() > 4) b.clear();
+        }
+    }
+    if (b.size() >= 3) {
+        pp.nchunk = (int)b.size() - 1;
+        pp.xlpt = 1;
+        pp.xb1 = b[1];
+        pp.xb2 = pp.nchunk > 2 ? b[2] : L.ntx;
+        std::vector<std::pair<double, int>> cs;
+        for (int c = 0; c < pp.nchunk; ++c) cs.push_back({-p2_chunk_cost(b[c], b[c + 1], L.ntx, pp.warm_tiles), c});
+        std::stable_sort(cs.begin(), cs.end());
+        for (int r = 0; r < pp.nchunk; ++r) pp.xord |= cs[r].second << (2 * r);
+    }
+    return pp;
+}
+
 void launch_pass1(bool fold, bool lpt, dim3 grid, int smem, cudaStream_t st, const Pass1Args& p1) {
     if (fold && lpt)
         k_pass1_gauss<true, true><<<grid, P1_WARPS * 32, smem, st>>>(p1);
@@ -2853,76 +2937,17 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.bstate = bst;
         p2.part = part;
         p2.order = g_p2_order;
-        // x-chunking of pass-2 rows when rows x groups cannot fill the GPU
+        // x-chunking of pass-2 rows (p2_chunk_plan)
         const int nrb = (H + P2_THREADS - 1) / P2_THREADS;
-        int nchunk = 1;
-        p2.warm_tiles = (std::max(sp->ext_x, 1) + TILE - 1) / TILE;
-        if (box) {
-            const long long threads = (long long)nrb * P2_THREADS * p2.ngroups * B;
-            const long long target = 148LL * 12 * 32 * 3 / 2;
-            const int win = 2 * sp->radius + 1;
-            while (threads * nchunk < target && nchunk < 64) {
-                const int cols = (L.ntx + 2 * nchunk - 1) / (2 * nchunk) * TILE;
-                if (cols < 4 * win) break;  // window init <= 25% of a chunk
-                nchunk *= 2;
-            }
-        } else if (!box && g_p2_chunks > 0) {
-            nchunk = std::min(g_p2_chunks, L.ntx);
-        } else if (!box) {
-            const long long threads = (long long)nrb * P2_THREADS * p2.ngroups * B;
-            const long long target = 148LL * 12 * 32 * 3 / 2;  // ~1.5 waves of 12 warps/SM
-            const long long wave = 148LL * 12 * 32;
-            // measured: G=4 prefers fewer, longer rows unless the GPU is far from full
-            const int max_chunks = (g2run == 4 && threads * 2 >= wave) ? 2 : 64;
-            while (threads * nchunk < target && nchunk < max_chunks) {
-                const int tpc = (L.ntx + 2 * nchunk - 1) / (2 * nchunk);
-                // warm-up <= 25% of a chunk; below one wave (latency-bound small
-                // images) accept warm-up up to the chunk length
-                const bool ok = tpc >= 4 * p2.warm_tiles ||
-                                (threads * nchunk < wave && tpc >= p2.warm_tiles);
-                if (!ok) break;
-                nchunk *= 2;
-            }
-        }
-        p2.tiles_per_chunk = (L.ntx + nchunk - 1) / nchunk;
-        nchunk = (L.ntx + p2.tiles_per_chunk - 1) / p2.tiles_per_chunk;
-        p2.xlpt = 0;
-        if (!box && p2var == 6 && nb == 1) {
-            // unequal x-chunks (at most 3), costliest first: the development
-            // override TBF_P2_XSPLIT (widths in tiles, left to right), else
-            // the planner for launches of a few waves (device entry only: the
-            // host entry's band launches want short blocks, measured +14%)
-            std::vector<int> b;
-            const char* ev = getenv("TBF_P2_XSPLIT");
-            if (ev && *ev) {
-                b.push_back(0);
-                for (const char* q = ev; *q && b.size() < 4 && b.back() < L.ntx;) {
-                    int v = std::max(1, (int)strtol(q, (char**)&q, 10));
-                    if (*q == ',') ++q;
-                    b.push_back((!*q || b.size() == 3) ? L.ntx : std::min(L.ntx, b.back() + v));
-                }
-                if (b.back() < L.ntx) b.back() = L.ntx;
-            } else if (g_p2_chunks <= 0 && (g_lpt_split & 2) && (!hpipe || (g_lpt_split & 8))) {
-                const int slots = 148 * 3;  // k_pass2_gr blocks resident per SM
-                const long long per_chunk = (long long)nrb * (P2_THREADS / 32) * npart * B;
-                if (per_chunk < 6LL * slots && L.ntx >= 8) {
-                    b = p2_plan_split(L.ntx, p2.warm_tiles, nchunk, per_chunk, slots);
-                    if (b.size() > 4 || (int)b.size() - 1 == nchunk) b.clear();  // equal split kept
-                }
-            }
-            if (b.size() >= 3) {
-                nchunk = (int)b.size() - 1;
-                p2.xlpt = 1;
-                p2.xb1 = b[1];
-                p2.xb2 = nchunk > 2 ? b[2] : L.ntx;
-                std::vector<std::pair<double, int>> cs;
-                for (int c = 0; c < nchunk; ++c) cs.push_back({-p2_chunk_cost(b[c], b[c + 1], L.ntx, p2.warm_tiles), c});
-                std::stable_sort(cs.begin(), cs.end());
-                p2.xord = 0;
-                for (int r = 0; r < nchunk; ++r) p2.xord |= cs[r].second << (2 * r);
-                p2.order = 4;
-            }
-        }
+        const P2Plan pp = p2_chunk_plan(L, sp, p2.ngroups, npart, g2run, p2var, hpipe);
+        int nchunk = pp.nchunk;
+        p2.warm_tiles = pp.warm_tiles;
+        p2.tiles_per_chunk = pp.tiles_per_chunk;
+        p2.xlpt = pp.xlpt;
+        p2.xb1 = pp.xb1;
+        p2.xb2 = pp.xb2;
+        p2.xord = pp.xord;
+        if (pp.xlpt) p2.order = 4;
         ReduceArgs ra;
         ra.part = part;
         ra.ngroups = npart > 0 ? npart : p2.ngroups;
@@ -3141,6 +3166,30 @@ int tbf_profile_collect(double* ms, long long* launches, int32_t n) {
 }
 
 const char* tbf_last_error(void) { return g_last_error.c_str(); }
+
+int tbf_layout_info(int32_t B, int32_t H, int32_t W, const tbf_spatial* sp, int32_t term_begin,
+                    int32_t term_end, int32_t batch_terms, int32_t host_entry, int32_t* info, int32_t n_info) {
+    if (!info || n_info < TBF_LAYOUT_INFO_N) return fail(TBF_ERR_PARAM, "info needs %d entries", TBF_LAYOUT_INFO_N);
+    if (term_end <= term_begin) return fail(TBF_ERR_PARAM, "empty term range");
+    Layout L;
+    int rc = make_layout(B, H, W, sp, term_end - term_begin, batch_terms, &L, host_entry ? 0 : 1);
+    if (rc) return rc;
+    const bool box = sp->kind == TBF_SPATIAL_BOX;
+    const int n = std::min(L.tb, term_end - term_begin);  // first batch
+    int p2var = g_pass2_tma;
+    if (!box && p2var == 3) p2var = 6;
+    const int npart = (!box && p2var == 6) ? (((n + G2 - 1) / G2 + P2R_GR - 1) / P2R_GR) : -1;
+    const int g2run = (!box && p2var == 4) ? 4 : G2;
+    const bool hpipe = host_entry && !box && L.nslot == 1;
+    const P2Plan pp = p2_chunk_plan(L, sp, (n + g2run - 1) / g2run, npart, g2run, p2var, hpipe);
+    const int32_t v[TBF_LAYOUT_INFO_N] = {L.nb, L.tb, L.nyc, L.ych_lpt ? 1 : 0,
+                                          L.nyc > 1 ? L.ychb[1] : H, L.nyc > 2 ? L.ychb[2] : H, L.ych_rows,
+                                          pp.nchunk, pp.xlpt, pp.xlpt ? pp.xb1 : std::min(L.ntx, pp.tiles_per_chunk),
+                                          pp.xlpt ? pp.xb2 : std::min(L.ntx, 2 * pp.tiles_per_chunk),
+                                          pp.tiles_per_chunk, pp.xord, L.ntx};
+    std::copy(v, v + TBF_LAYOUT_INFO_N, info);
+    return TBF_OK;
+}
 
 size_t tbf_workspace_bytes(int32_t B, int32_t H, int32_t W, const tbf_spatial* sp,
                            int32_t term_begin, int32_t term_end, int32_t batch_terms) {

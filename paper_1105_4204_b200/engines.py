@@ -428,6 +428,25 @@ def bilateral_trig(img, spatial, kernel, *, workers: int = 1,
     return res
 
 
+def layout_info(shape, spatial: SpatialSpec, kernel: TrigKernel, *, host_entry: bool = False,
+                batch_terms: int = 0, term_range=None) -> dict:
+    """The launch layout a call would use (``tbf_layout_info``; no GPU
+    needed): term batches, pass-1 y-chunks and pass-2 x-chunks, planned
+    (unequal, costliest first) or equal.  ``shape`` is [H, W] or [B, H, W];
+    ``host_entry`` selects the layout of the host-array entry."""
+    lib = _native.load()
+    if len(shape) == 2:
+        shape = (1, *shape)
+    B, H, W = (int(v) for v in shape)
+    sp = spatial_struct(_check_spatial(spatial))
+    terms = _TermsHolder(kernel)
+    t0, t1 = (0, terms.pairs.count) if term_range is None else (int(term_range[0]), int(term_range[1]))
+    info = (ctypes.c_int32 * _native.TBF_LAYOUT_INFO_N)()
+    _native.check(lib.tbf_layout_info(B, H, W, ctypes.byref(sp), t0, t1, int(batch_terms), int(bool(host_entry)),
+                                      info, _native.TBF_LAYOUT_INFO_N))
+    return dict(zip(_native.LAYOUT_INFO_FIELDS, list(info)))
+
+
 def bilateral_direct(img, spatial, range_fn, *, samples=None,
                      diagnostics: EngineDiagnostics | None = None):
     """Brute-force bilateral filter on the GPU in fp64 (engines.py:120-151).

@@ -1,0 +1,102 @@
+"""Launch-layout planning (host logic in the C-ABI library, no GPU needed):
+the device entry's planned unequal chunks for few-wave launches, equal chunks
+for the host entry, batched runs and many-wave configs."""
+
+import pytest
+
+from conftest import ROOT  # noqa: F401  (puts the repo on sys.path)
+
+
+@pytest.fixture(scope="module")
+def tb():
+    import os
+
+    from paper_1105_4204_b200.build import LIB, build
+
+    if not os.path.exists(LIB):
+        build()
+    import paper_1105_4204_b200 as tb
+
+    return tb
+
+
+def _cfg(tb, cid):
+    from paper_1105_4204_b200 import workloads
+
+    c = workloads.CONFIGS[cid]
+    return (c.frames, c.height, c.width), tb.SpatialSpec.gaussian_recursive(c.sigma_s), tb.make_trig_kernel(c.sigma_r, c.T)
+
+
+def test_config2_planned_device_layout(tb):
+    """Config 2 (1152 pass-1 blocks = 2.59 waves with equal chunks): two
+    unequal y-chunks, largest first, and two unequal x-chunks (13 + 51 tiles)
+    instead of 4 x 16, as measured fastest on B200."""
+    shape, spec, k = _cfg(tb, 2)
+    d = tb.layout_info(shape, spec, k)
+    assert d["batches"] == 1 and d["y_chunks"] == 2 and d["y_planned"] == 1
+    assert d["y_end0"] == 1376 and d["y_end1"] == 2048 and d["y_rows_max"] == 1376
+    assert d["y_end0"] % 32 == 0
+    assert d["x_chunks"] == 2 and d["x_planned"] == 1 and (d["x_end0"], d["x_end1"]) == (13, 64)
+    assert d["x_order"] & 3 == 1  # the 51-tile chunk (index 1) is dispatched first
+
+
+def test_host_entry_keeps_equal_chunks(tb):
+    """The host entry's strip/band launches keep the equal chunks (planned
+    ones measured +3% / +14% there)."""
+    shape, spec, k = _cfg(tb, 2)
+    d = tb.layout_info(shape, spec, k, host_entry=True)
+    assert d["y_planned"] == 0 and d["x_planned"] == 0
+    assert d["x_chunks"] == 4 and d["x_tiles_equal"] == 16
+
+
+@pytest.mark.parametrize("cid", [1, 3, 4, 5])
+def test_no_y_planning_where_it_does_not_pay(tb, cid):
+    """Config 1 (short columns, latency-bound), configs 3/4 (many waves) and
+    config 5 (term batches: the workspace must stay affine in the batch size)
+    keep equal y-chunks."""
+    shape, spec, k = _cfg(tb, cid)
+    d = tb.layout_info(shape, spec, k, batch_terms=16 if cid == 5 else 0)
+    assert d["y_planned"] == 0
+    if cid == 5:
+        assert d["batches"] > 1 and d["x_planned"] == 0
+
+
+def test_option_disables_planning(tb):
+    from paper_1105_4204_b200 import _native
+
+    lib = _native.load()
+    shape, spec, k = _cfg(tb, 2)
+    lib.tbf_set_option(_native.TBF_OPT_LPT_SPLIT, 0)
+    try:
+        d = tb.layout_info(shape, spec, k)
+    finally:
+        lib.tbf_set_option(_native.TBF_OPT_LPT_SPLIT, _native.TBF_LPT_DEFAULT)
+    assert d["y_planned"] == 0 and d["x_planned"] == 0 and d["x_chunks"] == 4
+
+
+def test_workspace_covers_both_layouts(tb):
+    """A plan's workspace (sized once) must fit the planned device layout and
+    the equal host layout whatever the option is when it runs: the size does
+    not depend on the option."""
+    import ctypes
+
+    from paper_1105_4204_b200 import _native
+    from paper_1105_4204_b200.engines import _TermsHolder, spatial_struct
+
+    lib = _native.load()
+    shape, spec, k = _cfg(tb, 2)
+    sp, terms = spatial_struct(spec), _TermsHolder(k)
+    n = terms.struct.n_terms
+    on = lib.tbf_workspace_bytes(*shape, ctypes.byref(sp), 0, n, 0)
+    lib.tbf_set_option(_native.TBF_OPT_LPT_SPLIT, 0)
+    try:
+        off = lib.tbf_workspace_bytes(*shape, ctypes.byref(sp), 0, n, 0)
+    finally:
+        lib.tbf_set_option(_native.TBF_OPT_LPT_SPLIT, _native.TBF_LPT_DEFAULT)
+    assert on == off > 0
+
+
+def test_layout_info_rejects_bad_arguments(tb):
+    shape, spec, k = _cfg(tb, 2)
+    with pytest.raises(tb.ParameterError):
+        tb.layout_info(shape, spec, k, term_range=(3, 3))
