@@ -2309,9 +2309,11 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
         // few waves: plan unequal chunks, largest first (p1_plan_split)
         const int slots = 148 * P1_BLOCKS_PER_SM;
         const long long per_chunk = (long long)L->ntx * ((tb + P1_WARPS - 1) / P1_WARPS) * B;
-        // (not for short columns: config 1, 512 rows, was 6% slower with the
-        // planned 3-way split; its launches are latency-bound)
-        if (per_chunk < 6LL * slots && H >= 1024 && H >= 16 * L->ywarm) {
+        // (not for short columns or launches under a wave per chunk level:
+        // config 1, 512 rows and 64 blocks, was 6% slower with the planned
+        // 3-way split; such launches are latency-bound, which the model does
+        // not describe)
+        if (per_chunk < 6LL * slots && per_chunk >= slots && H >= 1024 && H >= 16 * L->ywarm) {
             const std::vector<int> b = p1_plan_split(H, L->Ey, L->ywarm, per_chunk, slots);
             L->nyc = (int)b.size() - 1;
             L->ych_rows = 0;
@@ -2598,7 +2600,7 @@ P2Plan p2_chunk_plan(const Layout& L, const tbf_spatial* sp, int ngroups, int np
     } else if (g_p2_chunks <= 0 && (g_lpt_split & 2) && (!hpipe || (g_lpt_split & 8))) {
         const int slots = 148 * 3;  // k_pass2_gr blocks resident per SM
         const long long per_chunk = (long long)nrb * (P2_THREADS / 32) * npart * B;
-        if (per_chunk < 6LL * slots && L.ntx >= 8) {
+        if (per_chunk < 6LL * slots && 2 * per_chunk >= slots && L.ntx >= 8) {
             b = p2_plan_split(L.ntx, pp.warm_tiles, nchunk, per_chunk, slots);
             bool equal = (int)b.size() - 1 == nchunk;  // the planner kept the equal split
             for (int c = 0; equal && c <= nchunk; ++c) equal = b[c] == std::min(L.ntx, c * pp.tiles_per_chunk);

@@ -772,3 +772,31 @@ def test_planned_chunks_match_equal(tb, cfg_id):
     d = float((planned - equal).abs().max())
     print(f"config {cfg_id}: planned vs equal chunks max abs diff {d:.3g}")
     assert d < 1e-2
+
+
+@pytest.mark.parametrize("shape,sigma_s,sigma_r", [
+    ((1, 2000, 2100), 8.0, 20.0),   # ragged last tile and row block; 3 y-chunks + 2 x-chunks planned
+    ((2, 1500, 1000), 5.0, 20.0),   # two frames; 2 y-chunks + 3 x-chunks planned
+])
+def test_planned_chunks_ragged_shapes(tb, shape, sigma_s, sigma_r):
+    """Planned unequal chunks on shapes with a partial last column tile and
+    row block (checked to be planned through layout_info) agree with the
+    equal-chunk layout to the warm-up truncation level."""
+    from paper_1105_4204_b200 import _native
+    from paper_1105_4204_b200.workloads import smooth_image
+
+    lib = _native.load()
+    B, H, W = shape
+    spec = tb.SpatialSpec.gaussian_recursive(sigma_s)
+    k = tb.make_trig_kernel(sigma_r, 255.0)
+    d = tb.layout_info(shape, spec, k)
+    assert d["y_planned"] == 1 and d["x_planned"] == 1, d
+    f = torch.from_numpy(np.stack([smooth_image(H, W, 20, seed=40 + b) for b in range(B)]).astype(np.float32)).cuda()
+    planned = tb.bilateral_trig(f, spec, k)
+    lib.tbf_set_option(_native.TBF_OPT_LPT_SPLIT, 0)
+    try:
+        equal = tb.bilateral_trig(f, spec, k)
+    finally:
+        lib.tbf_set_option(_native.TBF_OPT_LPT_SPLIT, _native.TBF_LPT_DEFAULT)
+    assert torch.isfinite(planned).all()
+    assert float((planned - equal).abs().max()) < 1e-2
