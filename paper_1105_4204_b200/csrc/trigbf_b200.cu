@@ -1502,11 +1502,17 @@ __global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_gauss(const __grid_cons
 // partial traffic (pass-2 writes + reduce reads) drops 4x.
 constexpr int P2R_GR = 4;
 
-constexpr int P2R_SMEM = 2 * P2R_GR * TILE * 32 * 8;  // double-buffered float2 [2][warp][x][row]
+#ifndef TBF_P2_NBUF
+#define TBF_P2_NBUF 2  // staging buffers of the block-summed pass 2 (1: + a barrier per tile, half the smem)
+#endif
+#ifndef TBF_P2_MINB
+#define TBF_P2_MINB 3  // k_pass2_gr blocks per SM requested from ptxas
+#endif
+constexpr int P2R_SMEM = TBF_P2_NBUF * P2R_GR * TILE * 32 * 8;  // float2 [NBUF][warp][x][row]
 
 // LPT: unequal x-chunks (xlpt/xb1/xb2, dispatch order 4)
 template <int G, bool LPT>
-__global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_constant__ Pass2Args a) {
+__global__ void __launch_bounds__(32 * P2R_GR, TBF_P2_MINB) k_pass2_gr(const __grid_constant__ Pass2Args a) {
     extern __shared__ float2 sdyn[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nsb = a.nrb_run * (P2_THREADS / 32);  // 32-row sub-blocks in this launch
@@ -1615,11 +1621,11 @@ __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_consta
 #pragma unroll
         for (int m = 0; m < TILE; ++m) {
             sbuf(0, w, m) = make_float2(0.f, 0.f);
-            sbuf(1, w, m) = make_float2(0.f, 0.f);
+            if (TBF_P2_NBUF > 1) sbuf(1, w, m) = make_float2(0.f, 0.f);
         }
     }
 #pragma unroll 1
-    for (int t = t_hi - 1, buf = 0; t >= t_lo; --t, buf ^= 1) {
+    for (int t = t_hi - 1, buf = 0; t >= t_lo; --t, buf = (buf + 1) % TBF_P2_NBUF) {
         if (active) p2_tile<G, true, true>(a, c, t, p1, p2, q1, q2, pn, pd, iv, &sbuf(buf, w, 0));
         __syncthreads();
         const int x0 = t * TILE;
@@ -1638,6 +1644,7 @@ __global__ void __launch_bounds__(32 * P2R_GR, 3) k_pass2_gr(const __grid_consta
                 pd[off] = acc.y;
             }
         }
+        if (TBF_P2_NBUF == 1) __syncthreads();  // reads done before the next tile's stores
     }
 }
 
