@@ -191,6 +191,28 @@ __device__ __forceinline__ long long mirror_any(long long i, long long n) {
     return i >= n ? period - i : i;
 }
 
+// F_loc is written once (pass 1) and read once (pass 2), far apart: with
+// TBF_CACHE_HINTS its stores and loads are streaming (evict-first), so the
+// 16 B/pixel-term stream does not evict the L2-resident f tile copy,
+// checkpoints and carries.
+#ifndef TBF_CACHE_HINTS
+#define TBF_CACHE_HINTS 1
+#endif
+__device__ __forceinline__ void st_stream(float4* p, float4 v) {
+#if TBF_CACHE_HINTS
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+#if TBF_CACHE_HINTS
+    return __ldcs(p);
+#else
+    return *p;
+#endif
+}
+
 // Read-only global load kept in program order relative to the surrounding
 // shared-memory stores (volatile + memory clobber): pins prefetches where the
 // source puts them instead of letting them sink next to their use.
@@ -740,7 +762,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                         float o[4];
 #pragma unroll
                         for (int p = 0; p < 4; ++p) o[p] = cstep(yv[q][p], lv1[p], lv2[p], ly1[p], ly2[p], k);
-                        fl[(size_t)(xb + q) * FL_RB] = f4(o[0], o[1], o[2], o[3]);
+                        st_stream(fl + (size_t)(xb + q) * FL_RB, f4(o[0], o[1], o[2], o[3]));
                     }
                 }
             } else {
@@ -753,7 +775,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                     float o[4];
 #pragma unroll
                     for (int p = 0; p < 4; ++p) o[p] = cstep(yv[p], lv1[p], lv2[p], ly1[p], ly2[p], k);
-                    fl[(size_t)xx * FL_RB] = f4(o[0], o[1], o[2], o[3]);
+                    st_stream(fl + (size_t)xx * FL_RB, f4(o[0], o[1], o[2], o[3]));
                     if (a.edge_all || gx <= a.Ex || gx >= W - 1 - a.Ex) {
                         const int e = a.edge_all ? gx : (gx <= a.Ex ? gx : gx - (W - 1 - a.Ex) + a.Ex + 1);
                         ed0[(size_t)e * H + i] = f4(yv[0], yv[1], yv[2], yv[3]);
@@ -908,7 +930,7 @@ __device__ __forceinline__ void p2_load4(const P2Ctx<G>& c, int x0, int mb, floa
     for (int q = 0; q < 4; ++q) {
         const size_t off = (size_t)(x0 + max(mb - q, 0)) * FL_RB;
 #pragma unroll
-        for (int g = 0; g < G; ++g) fo[q][g] = c.fl[g][off];
+        for (int g = 0; g < G; ++g) fo[q][g] = ld_stream(c.fl[g] + off);
         if (OUT) fv[q] = c.fT[off];
     }
 }
