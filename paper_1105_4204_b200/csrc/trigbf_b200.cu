@@ -2688,6 +2688,15 @@ P2Plan p2_chunk_plan(const Layout& L, const tbf_spatial* sp, int ngroups, int np
     return pp;
 }
 
+// Pass-1 instantiation for a layout: 2 planned chunks; 1 equal chunks whose
+// interior warm-up rows are at least a tenth of the column (config 1: 62%,
+// 2.8% faster); else 0, the original code (config 5's batches, 2 chunks of
+// 8192 rows with 2% warm-up rows, lost 7% in mode 1 to its spills)
+int p1_mode(const Layout& L, const Pass1Args& p1) {
+    if (p1.ylpt) return 2;
+    return (L.nyc > 1 && 10LL * L.ywarm * (L.nyc - 1) >= L.H) ? 1 : 0;
+}
+
 void launch_pass1(bool fold, int mode, dim3 grid, int smem, cudaStream_t st, const Pass1Args& p1) {
     const dim3 blk(P1_WARPS * 32);
     switch (mode * 2 + (fold ? 1 : 0)) {
@@ -2932,7 +2941,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 dim3 gs = p1grid(p1.ntx_run);
                 {
                     Prof pr(KK_PASS1, ps);
-                    launch_pass1(fold, p1.ylpt ? 2 : (L.nyc > 1 ? 1 : 0), gs, p1smem, ps, p1);
+                    launch_pass1(fold, p1_mode(L, p1), gs, p1smem, ps, p1);
                 }
                 cudaEvent_t e = event_get();
                 cudaEventRecord(e, ps);
@@ -2945,7 +2954,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             if (box)
                 k_pass1_box<G1, R_ANCHOR><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1, sp->radius);
             else
-                launch_pass1(fold, p1.ylpt ? 2 : (L.nyc > 1 ? 1 : 0), g1, p1smem, st, p1);
+                launch_pass1(fold, p1_mode(L, p1), g1, p1smem, st, p1);
         }
         if ((rc = check_cuda("pass1"))) return rc;
         if (s2 != st) {  // hand the batch to the second stream
