@@ -666,7 +666,6 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     const int nseg = (Bend - R0 + TILE - 1) / TILE;  // local segments of this chunk
     const int nsteps = 2 * nseg;
     float seg_f[TILE];
-    float4 ckn[4];
 #pragma unroll
     for (int q = 0; q < TILE; ++q) seg_f[q] = fload(R0 + q);
 #pragma unroll 1
@@ -675,30 +674,15 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
         const int seg = phaseB ? nsteps - 1 - step : step;
         const int i0 = R0 + seg * TILE;
         const int len = min(TILE, Bend - i0);
-        if (!phaseB) {
-            if (xv) {
-                float4* ck = ck0 + (size_t)seg * cks;
+        if (!phaseB && xv) {
+            float4* ck = ck0 + (size_t)seg * cks;
 #pragma unroll
-                for (int p = 0; p < 4; ++p) ck[p] = f4(v1[p], v2[p], y1[p], y2[p]);
-            }
-        } else {
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                v1[p] = ckn[p].x;
-                v2[p] = ckn[p].y;
-                y1[p] = ckn[p].z;
-                y2[p] = ckn[p].w;
-            }
+            for (int p = 0; p < 4; ++p) ck[p] = f4(v1[p], v2[p], y1[p], y2[p]);
         }
-        // the next step's checkpoint (phase B) and f rows are loaded at the
-        // start of this step, one whole segment ahead of their use
+        // the next step's segment: its f rows are loaded during this step's
+        // forward (in-place refill below), its checkpoint (phase B) after it
         const int ns = step + 1 < nseg ? step + 1 : max(nsteps - 2 - step, 0);
         const int rn = R0 + ns * TILE;
-        if (step + 1 >= nseg && step + 1 < nsteps) {  // checkpoint first (before the f burst)
-            const float4* ck = ck0 + (size_t)ns * cks;  // after this step's store (same thread)
-#pragma unroll
-            for (int p = 0; p < 4; ++p) ckn[p] = ck[p];
-        }
         const bool nfast = rn >= 0 && rn + TILE <= H;  // next segment: one whole fY tile
         const bool full = step != nseg && len == TILE;
         // forward over the segment into the smem tile (own column), 4 x 8
@@ -741,6 +725,21 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
             for (int q = 0; q < TILE; ++q) seg_f[q] = fload(rn + q);
         }
         if (!phaseB) continue;
+        if (step + 1 < nsteps) {
+            // the next step's forward restarts from its segment's checkpoint:
+            // loaded straight into the forward state, which this step no
+            // longer needs, a whole backward + epilogue ahead of its use (no
+            // prefetch registers and restore moves)
+            const float4* ck = ck0 + (size_t)ns * cks;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const float4 c = ck[p];
+                v1[p] = c.x;
+                v2[p] = c.y;
+                y1[p] = c.z;
+                y2[p] = c.w;
+            }
+        }
         if (seg == nseg - 1) {
             // backward start = steady state of the last forward output (_core.pyx:85-87)
             const float4 lastf = bl[(len - 1) * BUF_LD];
