@@ -2364,7 +2364,12 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
             }
         }
         int nyc = best_n;
-        if (g_p1_ychunks > 0) nyc = std::min(g_p1_ychunks, (H + TILE - 1) / TILE);
+        if (g_p1_ychunks > 0) {
+            // forced count: at most TBF_MAX_YCH chunks (ychb[] bound), none
+            // shorter than the warm-up (the automatic search's own limit)
+            const int max_by_warm = std::max(1, H / std::max(L->ywarm, TILE));
+            nyc = std::min(std::min(g_p1_ychunks, TBF_MAX_YCH), std::min((H + TILE - 1) / TILE, max_by_warm));
+        }
         L->ych_rows = ((H + nyc - 1) / nyc + TILE - 1) / TILE * TILE;
         L->nyc = (H + L->ych_rows - 1) / L->ych_rows;
     }
@@ -2582,9 +2587,16 @@ int validate(const tbf_spatial* sp, const tbf_terms* terms, int tbeg, int tend) 
 constexpr int P1_SMEM = P1_WARPS * 4 * G1 * TILE * BUF_LD * 4;
 constexpr int P1_SMEM_OCC2 = 80 * 1024;  // padded request: at most 2 pass-1 blocks per SM
 
+// cudaFuncSetAttribute applies to the current device only: done once per
+// device (a process may drive several GPUs)
 void set_p1_smem() {
-    static bool done = false;
-    if (done) return;
+    static std::mutex mu;
+    static uint64_t done_mask[4] = {0, 0, 0, 0};  // devices 0..255
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dev = std::max(0, std::min(dev, 255));
+    std::lock_guard<std::mutex> g(mu);
+    if (done_mask[dev >> 6] & (1ull << (dev & 63))) return;
     cudaFuncSetAttribute(k_pass2_async<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          p2a_smem_bytes<4>());
     cudaFuncSetAttribute(k_pass2_async<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2603,7 +2615,7 @@ void set_p1_smem() {
     cudaFuncSetAttribute(k_pass1_gauss<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
     cudaFuncSetAttribute(k_pass1_box<G1, R_ANCHOR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          P1_SMEM);
-    done = true;
+    done_mask[dev >> 6] |= 1ull << (dev & 63);
 }
 
 
@@ -2739,6 +2751,58 @@ struct HostIO {
     int bands;   // row bands: D2H of band b overlaps pass 2 of band b+1
 };
 
+// Pinned staging of the per-call term table (see run_terms).
+constexpr size_t TAB_CACHE = 64;
+struct TabEntry {
+    uint64_t hash;
+    std::vector<float> content;
+    float* pinned;
+    cudaEvent_t last_use;
+    uint64_t tick;
+};
+
+uint64_t fnv1a(const std::vector<float>& v) {
+    uint64_t h = 1469598103934665603ull;
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(v.data());
+    for (size_t i = 0; i < v.size() * sizeof(float); ++i) h = (h ^ p[i]) * 1099511628211ull;
+    return h;
+}
+
+int stage_term_table(const std::vector<float>& h_tab, float* d_tab, cudaStream_t st) {
+    static std::mutex mu;
+    static std::vector<TabEntry> cache;
+    static uint64_t clock = 0;
+    std::lock_guard<std::mutex> g(mu);
+    const uint64_t h = fnv1a(h_tab);
+    TabEntry* e = nullptr;
+    for (auto& c : cache)
+        if (c.hash == h && c.content == h_tab) e = &c;
+    if (!e) {
+        if (cache.size() >= TAB_CACHE) {  // evict the least recently used entry
+            auto lru = std::min_element(cache.begin(), cache.end(),
+                                        [](const TabEntry& a, const TabEntry& b) { return a.tick < b.tick; });
+            cudaEventSynchronize(lru->last_use);  // its last copy has read the buffer
+            cudaEventDestroy(lru->last_use);
+            cudaFreeHost(lru->pinned);
+            cache.erase(lru);
+        }
+        float* p = nullptr;
+        if (cudaHostAlloc(&p, h_tab.size() * 4, cudaHostAllocDefault) != cudaSuccess)
+            return fail(TBF_ERR_CUDA, "pinned term table: %s", cudaGetErrorString(cudaGetLastError()));
+        std::copy(h_tab.begin(), h_tab.end(), p);
+        cudaEvent_t ev;
+        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        cache.push_back(TabEntry{h, h_tab, p, ev, 0});
+        e = &cache.back();
+    }
+    e->tick = ++clock;
+    cudaMemcpyAsync(d_tab, e->pinned, h_tab.size() * 4, cudaMemcpyHostToDevice, st);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusNone) cudaEventRecord(e->last_use, st);
+    return check_cuda("term table copy");
+}
+
 int run_terms(const float* f, float* num, float* den, float* out, int B, int H, int W,
               const tbf_spatial* sp, const tbf_terms* terms, int tbeg, int tend, int batch_terms,
               int accumulate, void* ws, size_t ws_bytes, unsigned long long* counters,
@@ -2783,27 +2847,14 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         h_tab[ld + j] = (float)(nu - (double)hi);
         h_tab[2 * ld + j] = (float)terms->weight[tbeg + j];
     }
-    // the table is copied from a persistent pinned buffer per distinct table
-    // content (never modified or freed), so a call captured in a CUDA graph
-    // replays the copy of exactly the table it was captured with
+    // the table is copied from a pinned buffer per distinct table content, so
+    // a call captured in a CUDA graph replays the copy of exactly the table it
+    // was captured with.  The cache is bounded (LRU, TAB_CACHE entries): an
+    // evicted buffer is freed only after the event recorded behind its last
+    // copy has completed (a graph capture is the caller's to keep within the
+    // bound: more distinct live tables than TAB_CACHE would recycle buffers)
     {
-        static std::mutex mu;
-        static std::vector<std::pair<std::vector<float>, float*>> pinned;
-        const float* src = nullptr;
-        {
-            std::lock_guard<std::mutex> g(mu);
-            for (const auto& e : pinned)
-                if (e.first == h_tab) src = e.second;
-            if (!src) {
-                float* p = nullptr;
-                if (cudaHostAlloc(&p, h_tab.size() * 4, cudaHostAllocDefault) != cudaSuccess)
-                    return fail(TBF_ERR_CUDA, "pinned term table: %s", cudaGetErrorString(cudaGetLastError()));
-                std::copy(h_tab.begin(), h_tab.end(), p);
-                pinned.emplace_back(h_tab, p);
-                src = p;
-            }
-        }
-        cudaMemcpyAsync(tab, src, h_tab.size() * 4, cudaMemcpyHostToDevice, st);
+        if ((rc = stage_term_table(h_tab, tab, st))) return rc;
     }
 
     // host input: column strips copied on an internal stream; pass 1 of the
@@ -3158,7 +3209,9 @@ int tbf_set_option(int32_t option, int64_t value) {
             g_pipeline = value != 0;
             return TBF_OK;
         case TBF_OPT_P1_YCHUNKS:
-            g_p1_ychunks = (int)std::max<int64_t>(0, value);
+            if (value < 0 || value > TBF_MAX_YCH)
+                return fail(TBF_ERR_PARAM, "pass-1 y-chunks must be in [0, %d]", TBF_MAX_YCH);
+            g_p1_ychunks = (int)value;
             return TBF_OK;
         case TBF_OPT_P1_OCC:
             if (value < 2 || value > 3) return fail(TBF_ERR_PARAM, "pass-1 occupancy must be 2 or 3");

@@ -19,6 +19,7 @@ result is a CUDA tensor; CPU tensors / NumPy arrays are copied in and out).
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -124,6 +125,12 @@ class TrigFilter:
         self.counters = torch.zeros(2, dtype=torch.int64, device=self.device)
         self._io = None  # device input/output of run_host, allocated on first use
         self._pin = None  # pinned host staging (in, out) for pageable callers
+        # one call at a time per plan: the workspace, the staging buffers and
+        # the counters are shared by every call through this plan (the
+        # reference's engines are safe to call from several threads, e.g.
+        # bilateral_color(..., workers=3)); reentrant so a caller can hold it
+        # across a call and the counter read that belongs to it
+        self.lock = threading.RLock()
 
     # -- sizing -----------------------------------------------------------
     def workspace_bytes(self, batch_terms: int) -> int:
@@ -161,13 +168,27 @@ class TrigFilter:
         return min(tb, n)
 
     # -- calls ------------------------------------------------------------
-    def _check_input(self, f):
+    def _check_input(self, f, what: str = "input"):
+        """A device buffer handed to the library: contiguous float32 on this
+        plan's device with exactly B*H*W samples (anything else would be read
+        or written out of bounds by the kernels)."""
         torch = _torch()
-        if f.dtype != torch.float32 or not f.is_cuda or not f.is_contiguous():
-            raise ParameterError("expected a contiguous float32 CUDA tensor")
+        if not isinstance(f, torch.Tensor) or f.dtype != torch.float32 or not f.is_cuda \
+                or not f.is_contiguous():
+            raise ParameterError(f"{what}: expected a contiguous float32 CUDA tensor")
+        if f.device != self.device:
+            raise ParameterError(f"{what}: on {f.device}, plan is on {self.device}")
         if f.numel() != self.B * self.H * self.W:
-            raise DimensionError(f"input has {f.numel()} samples, plan expects "
+            raise DimensionError(f"{what} has {f.numel()} samples, plan expects "
                                  f"{self.B}x{self.H}x{self.W}")
+
+    def _ctx(self):
+        """Library calls run with the plan's device current (the C ABI works
+        on the current device) on that device's current torch stream."""
+        return _torch().cuda.device(self.device)
+
+    def _stream(self):
+        return _torch().cuda.current_stream(self.device).cuda_stream
 
     def __call__(self, f, out=None):
         """out[b] = bilateral_trig(f[b]); async on the current stream."""
@@ -177,11 +198,12 @@ class TrigFilter:
             raise ParameterError("plan covers a term shard; use partial() + finalize()")
         if out is None:
             out = torch.empty_like(f)
-        stream = torch.cuda.current_stream(f.device).cuda_stream
-        rc = self.lib.tbf_bilateral_trig(
-            f.data_ptr(), out.data_ptr(), self.B, self.H, self.W, ctypes.byref(self.sp),
-            ctypes.byref(self.terms.struct), self.batch_terms, self.workspace.data_ptr(),
-            self.workspace.numel(), self.counters.data_ptr(), stream)
+        self._check_input(out, "out")
+        with self.lock, self._ctx():
+            rc = self.lib.tbf_bilateral_trig(
+                f.data_ptr(), out.data_ptr(), self.B, self.H, self.W, ctypes.byref(self.sp),
+                ctypes.byref(self.terms.struct), self.batch_terms, self.workspace.data_ptr(),
+                self.workspace.numel(), self.counters.data_ptr(), self._stream())
         _native.check(rc)
         return out
 
@@ -197,13 +219,14 @@ class TrigFilter:
             raise ParameterError("plan covers a term shard; use partial() + finalize()")
         n = self.B * self.H * self.W
         p_in, p_out = _host_ptr(h_in, n, "input"), _host_ptr(h_out, n, "output")
-        if self._io is None:
-            self._io = torch.empty(2 * n, dtype=torch.float32, device=self.device)
-        stream = torch.cuda.current_stream(self.device).cuda_stream
-        rc = self.lib.tbf_bilateral_trig_host(
-            p_in, p_out, self.B, self.H, self.W, ctypes.byref(self.sp),
-            ctypes.byref(self.terms.struct), self.batch_terms, self._io.data_ptr(),
-            self.workspace.data_ptr(), self.workspace.numel(), self.counters.data_ptr(), stream)
+        with self.lock, self._ctx():
+            if self._io is None:
+                self._io = torch.empty(2 * n, dtype=torch.float32, device=self.device)
+            rc = self.lib.tbf_bilateral_trig_host(
+                p_in, p_out, self.B, self.H, self.W, ctypes.byref(self.sp),
+                ctypes.byref(self.terms.struct), self.batch_terms, self._io.data_ptr(),
+                self.workspace.data_ptr(), self.workspace.numel(), self.counters.data_ptr(),
+                self._stream())
         _native.check(rc)
         return h_out
 
@@ -219,6 +242,11 @@ class TrigFilter:
         n = self.B * self.H * self.W
         if src.size != n or dst.size != n:
             raise DimensionError(f"host arrays must hold {n} samples")
+        with self.lock:
+            return self._run_staged(src, dst, n)
+
+    def _run_staged(self, src, dst, n):
+        torch = _torch()
         if 4 * n > self.PIN_LIMIT:
             s32 = np.ascontiguousarray(src, dtype=np.float32)
             o32 = dst if (dst.dtype == np.float32 and dst.flags.c_contiguous) else np.empty(s32.shape, np.float32)
@@ -239,35 +267,40 @@ class TrigFilter:
 
     def partial(self, f, num, den, accumulate: bool = False):
         """num/den (+)= contribution of this plan's term range (sharded path)."""
-        torch = _torch()
         self._check_input(f)
-        stream = torch.cuda.current_stream(f.device).cuda_stream
+        self._check_input(num, "num")
+        self._check_input(den, "den")
         t0, t1 = self.term_range
-        rc = self.lib.tbf_trig_partial(
-            f.data_ptr(), num.data_ptr(), den.data_ptr(), self.B, self.H, self.W,
-            ctypes.byref(self.sp), ctypes.byref(self.terms.struct), t0, t1, self.batch_terms,
-            int(bool(accumulate)), self.workspace.data_ptr(), self.workspace.numel(), stream)
+        with self.lock, self._ctx():
+            rc = self.lib.tbf_trig_partial(
+                f.data_ptr(), num.data_ptr(), den.data_ptr(), self.B, self.H, self.W,
+                ctypes.byref(self.sp), ctypes.byref(self.terms.struct), t0, t1, self.batch_terms,
+                int(bool(accumulate)), self.workspace.data_ptr(), self.workspace.numel(),
+                self._stream())
         _native.check(rc)
 
     def range_check(self, f):
-        torch = _torch()
-        stream = torch.cuda.current_stream(f.device).cuda_stream
-        _native.check(self.lib.tbf_range_check(f.data_ptr(), f.numel(), float(self.kernel.T),
-                                               self.counters.data_ptr(), stream))
+        self._check_input(f)
+        with self.lock, self._ctx():
+            rc = self.lib.tbf_range_check(f.data_ptr(), f.numel(), float(self.kernel.T),
+                                          self.counters.data_ptr(), self._stream())
+        _native.check(rc)
 
     def finalize(self, num, den, f, out):
-        torch = _torch()
-        stream = torch.cuda.current_stream(f.device).cuda_stream
-        _native.check(self.lib.tbf_finalize(num.data_ptr(), den.data_ptr(), f.data_ptr(),
-                                            out.data_ptr(), f.numel(), self.counters.data_ptr(),
-                                            stream))
+        for t, what in ((num, "num"), (den, "den"), (f, "input"), (out, "out")):
+            self._check_input(t, what)
+        with self.lock, self._ctx():
+            rc = self.lib.tbf_finalize(num.data_ptr(), den.data_ptr(), f.data_ptr(), out.data_ptr(),
+                                       f.numel(), self.counters.data_ptr(), self._stream())
+        _native.check(rc)
         return out
 
     def read_counters(self, reset: bool = True):
         """(samples outside [0, T], guarded pixels) since the last reset; syncs."""
-        vals = self.counters.tolist()
-        if reset:
-            self.counters.zero_()
+        with self.lock, self._ctx():
+            vals = self.counters.tolist()
+            if reset:
+                self.counters.zero_()
         return int(vals[0]), int(vals[1])
 
     @property
@@ -295,6 +328,7 @@ def _host_ptr(a, n: int, what: str) -> int:
 
 _PLANS: dict = {}
 _MAX_PLANS = 4
+_PLANS_LOCK = threading.RLock()
 
 
 def _require_cuda():
@@ -310,25 +344,28 @@ def get_plan(shape, spatial: SpatialSpec, kernel: TrigKernel, device=None) -> Tr
     _require_cuda()
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     key = (str(dev), tuple(shape), spatial, kernel.N, kernel.omega, kernel.T)
-    plan = _PLANS.get(key)
-    if plan is None:
-        while len(_PLANS) >= _MAX_PLANS:
-            _PLANS.pop(next(iter(_PLANS)))
-        try:
-            plan = TrigFilter(shape, spatial, kernel, device=dev)
-        except torch.cuda.OutOfMemoryError:
-            # cached plans hold large workspaces (up to ~80% of free memory for
-            # a 16k^2 image): drop them and size the new plan from scratch
-            _PLANS.clear()
-            torch.cuda.empty_cache()
-            plan = TrigFilter(shape, spatial, kernel, device=dev)
-        _PLANS[key] = plan
-    return plan
+    with _PLANS_LOCK:
+        plan = _PLANS.get(key)
+        if plan is None:
+            while len(_PLANS) >= _MAX_PLANS:
+                _PLANS.pop(next(iter(_PLANS)))
+            try:
+                plan = TrigFilter(shape, spatial, kernel, device=dev)
+            except torch.cuda.OutOfMemoryError:
+                # cached plans hold large workspaces (up to ~80% of free memory for
+                # a 16k^2 image): drop them and size the new plan from scratch
+                # (a thread still using an evicted plan keeps its own reference)
+                _PLANS.clear()
+                torch.cuda.empty_cache()
+                plan = TrigFilter(shape, spatial, kernel, device=dev)
+            _PLANS[key] = plan
+        return plan
 
 
 def clear_plans() -> None:
     """Release the cached plans and their device workspaces."""
-    _PLANS.clear()
+    with _PLANS_LOCK:
+        _PLANS.clear()
     _torch().cuda.empty_cache()
 
 
@@ -392,7 +429,7 @@ def bilateral_trig(img, spatial, kernel, *, workers: int = 1,
         shape = (1, img.height, img.width)
         plan = get_plan(shape, spatial, kernel)
         res = np.empty((1, img.height, img.width), dtype=np.float64)
-        counts = plan.run_staged(host, res)
+        counts = plan.run_staged(host, res)  # holds the plan's lock through its counter read
         _finish(plan, shape, lambda: (float(host.min()), float(host.max())), counts)
         return Image(img.width, img.height, 1, res)
     if isinstance(img, np.ndarray):
@@ -413,8 +450,10 @@ def bilateral_trig(img, spatial, kernel, *, workers: int = 1,
     if img.is_cuda:  # device in, device out, no copies
         f = img.to(dtype=torch.float32).contiguous()
         plan = get_plan(shape, spatial, kernel, device=f.device)
-        out = plan(f)
-        _finish(plan, shape, lambda: (float(f.min()), float(f.max())))
+        with plan.lock:  # the call and the counter read that belongs to it
+            out = plan(f)
+            counts = plan.read_counters()
+        _finish(plan, shape, lambda: (float(f.min()), float(f.max())), counts)
         return out.reshape(img.shape)
     pinned = img.is_pinned()
     if shape[0] >= 4 and pinned and img.dtype == torch.float32:
@@ -423,8 +462,10 @@ def bilateral_trig(img, spatial, kernel, *, workers: int = 1,
     host = img.to(dtype=torch.float32).contiguous()
     res = torch.empty(tuple(img.shape), dtype=torch.float32, pin_memory=pinned)
     plan = get_plan(shape, spatial, kernel)
-    plan.run_host(host, res)
-    _finish(plan, shape, lambda: (float(host.min()), float(host.max())))
+    with plan.lock:
+        plan.run_host(host, res)
+        counts = plan.read_counters()
+    _finish(plan, shape, lambda: (float(host.min()), float(host.max())), counts)
     return res
 
 
@@ -528,6 +569,14 @@ def _bilateral_trig_streamed(t, spatial, kernel, diagnostics, sub: int | None = 
     sub-batches so host->device copies, filtering and device->host copies of
     different sub-batches overlap (copy engines run beside the SMs).  Same
     result as one call: frames are independent."""
+    with _STREAMED_LOCK:  # sub-batch plans and their counters are shared
+        return _bilateral_trig_streamed_locked(t, spatial, kernel, diagnostics, sub, edges)
+
+
+_STREAMED_LOCK = threading.Lock()
+
+
+def _bilateral_trig_streamed_locked(t, spatial, kernel, diagnostics, sub, edges):
     torch = _torch()
     B, H, W = t.shape
     if sub is None:
