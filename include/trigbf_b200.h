@@ -198,19 +198,14 @@ TBF_API int32_t tbf_profile_timeline(double* start_ms, double* dur_ms, int32_t* 
 #define TBF_OPT_P2_CHUNKS 3 /* default 0 = automatic x-chunks per pass-2 row */
 #define TBF_OPT_P1_OCC 4    /* default 3 pass-1 blocks/SM; 2 leaves room for a pass-2 block */
 #define TBF_OPT_P1_YCHUNKS 5 /* default 0 = automatic row chunks per pass-1 column */
-#define TBF_OPT_PASS2_TMA 2 /* pass-2 variant: 0 register prefetch (2 terms/thread), 1|2 TMA bulk
-                               copies + mbarriers with a producer warp (3|2 blocks/SM, W % 32 == 0),
-                               3 (default) automatic (currently 6),
-                               4 per-thread cp.async staging, 4 terms/thread,
-                               5 per-thread cp.async staging, 2 terms/thread,
-                               6 register prefetch with 4 groups summed per block (4x fewer partials) */
+/* (2 and 10, the round-1 pass-2 variant and pass-1 block-order options, were
+ * removed: pass 2 has one variant and pass 1 one block order; tbf_set_option
+ * rejects them) */
 #define TBF_OPT_HOST_STRIPS 7 /* column strips of tbf_bilateral_trig_host's input copy (0 = auto) */
 #define TBF_OPT_HOST_BANDS 8  /* row bands of tbf_bilateral_trig_host's output copy (0 = auto) */
 #define TBF_OPT_LPT_SPLIT 11 /* default 1: for launches of a few waves, pass-1 y-chunks and pass-2
                                 x-chunks of unequal size, dispatched costliest first, planned by a
                                 list-scheduling model; 0 = equal chunks */
-#define TBF_OPT_P1_ORDER 10 /* block order of pass 1: -1 (default) automatic, 0 column tile fastest,
-                               1 term group fastest, 2 y-chunk fastest */
 #define TBF_OPT_P2_ORDER 9  /* block order of the block-summed pass 2: 0 (default) row fastest, 1 x-chunk fastest, 2/3 reversed */
 #define TBF_OPT_P1_FOLD 6   /* default 1: folds the y-sweep gain into the pass-2 weights
                                (skips 4 multiplies per pixel-term in pass 1 when T/g^4 is safe); 0 scales in pass 1 */

@@ -25,7 +25,6 @@ TBF_ERR_WORKSPACE = 5
 
 TBF_OPT_PIPELINE = 0
 TBF_OPT_BATCHES = 1
-TBF_OPT_PASS2_TMA = 2
 TBF_OPT_P2_CHUNKS = 3
 TBF_OPT_P1_OCC = 4
 TBF_OPT_P1_YCHUNKS = 5
@@ -33,7 +32,6 @@ TBF_OPT_P1_FOLD = 6
 TBF_OPT_HOST_STRIPS = 7
 TBF_OPT_HOST_BANDS = 8
 TBF_OPT_P2_ORDER = 9
-TBF_OPT_P1_ORDER = 10
 TBF_OPT_LPT_SPLIT = 11  # bits 1/2: planned y-/x-chunks (device entry); 4/8: also in the host entry
 TBF_LPT_DEFAULT = 3
 TBF_LAYOUT_INFO_N = 14

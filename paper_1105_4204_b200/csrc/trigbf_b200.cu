@@ -28,7 +28,6 @@
 //                  tile-local + H[m] . carry, then the backward cascade,
 //                  demodulation and num/den accumulation in registers; the
 //                  block sums its 4 groups in shared memory (fixed order).
-//                  (k_pass2_gauss / _async / _tma: per-group variants, options)
 //   k_reduce       folds the per-block partial num/den, transposes back to
 //                  row-major and applies the guarded ratio (engines.py:109-117).
 //
@@ -91,6 +90,7 @@ __host__ __device__ __forceinline__ size_t xm_plane(int B, int W, int H) {
 constexpr int TBF_MAX_YCH = 16;      // most y-chunks per pass-1 column
 constexpr int P1_BLOCKS_PER_SM = 3;  // smem-limited residency of pass-1 blocks (4 warps, 67.6 KB)
 constexpr int BUF_LD = TILE + 1;  // padded leading dimension of the smem tile
+constexpr int STRIPE = P1_WARPS * TILE;  // columns per pass-1 block (x carries are chained per stripe)
 
 thread_local std::string g_last_error;
 
@@ -221,6 +221,39 @@ __device__ __forceinline__ float ldg_pinned(const float* p) {
     asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
     return v;
 }
+
+// Named barriers between pairs of warps (the pass-1 x hand-off inside a
+// block): arrive does not wait; sync waits for `count` threads in total.
+// Barrier ids are immediates (ptxas then reserves ids 0..7 only, not all 16):
+// FULL 1 + w and EMPTY 5 + w for the links w -> w+1, w = 0..2.
+#define TBF_BAR_CASE(op, n) \
+    case n: asm volatile(op " " #n ", 64;" ::: "memory"); break;
+__device__ __forceinline__ void named_bar_sync(int id, int /*count = 64*/) {
+    switch (id) {
+        TBF_BAR_CASE("bar.sync", 1)
+        TBF_BAR_CASE("bar.sync", 2)
+        TBF_BAR_CASE("bar.sync", 3)
+        TBF_BAR_CASE("bar.sync", 4)
+        TBF_BAR_CASE("bar.sync", 5)
+        TBF_BAR_CASE("bar.sync", 6)
+        TBF_BAR_CASE("bar.sync", 7)
+        default: __trap();
+    }
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int /*count = 64*/) {
+    switch (id) {
+        TBF_BAR_CASE("bar.arrive", 1)
+        TBF_BAR_CASE("bar.arrive", 2)
+        TBF_BAR_CASE("bar.arrive", 3)
+        TBF_BAR_CASE("bar.arrive", 4)
+        TBF_BAR_CASE("bar.arrive", 5)
+        TBF_BAR_CASE("bar.arrive", 6)
+        TBF_BAR_CASE("bar.arrive", 7)
+        default: __trap();
+    }
+}
+#undef TBF_BAR_CASE
+static_assert(P1_WARPS == 4, "pass-1 hand-off barrier ids 1..7 assume 4 warps per block");
 
 // One pure cascade step (state v1,v2 | y1,y2); output scaled by 1/g.
 __device__ __forceinline__ float cstep(float u, float& v1, float& v2, float& y1, float& y2,
@@ -408,30 +441,30 @@ struct Pass1Args {
     // spill in this kernel (9% slower pass 1 on config 5)
     int ylpt, yb1, yb2;
     int Ex, ne, edge_all, ntx;
-    int tile0, ntx_run;  // column tiles [tile0, tile0 + ntx_run) in this launch
-    int order, ngb;      // block order (TBF_OPT_P1_ORDER); term-group blocks
+    int nst;           // stripes of P1_WARPS column tiles (one pass-1 block each, per term)
+    int st0, nst_run;  // stripes [st0, st0 + nst_run) in this launch
+    int unit, nun;     // x chain unit in tiles (P1_WARPS: hand-off inside the stripe; 1: none), units
     Casc k;
     TermDev t;
-    int ngroups;    // ceil(t.n / G1)
     // Gaussian layouts (float4 = the 4 planes of one term, or the 4 states
     // (v1,v2,y1,y2) of one plane):
     float* ckpt;    // float4 [nseg][n][B][W][4 planes]
     float* floc;    // float4 [n][B][W][H]  tile-local forward along x (x-major)
                     //   (box: planar [n*4][B][W][H] y-filtered values)
-    float* lcarry;  // float4 [n][B][ntx][H][4 planes]
+    float* lcarry;  // float4 [n][B][nun][H][4 planes] chain-unit end states (zero start)
     float* edge;    // float4 [n][B][ne][H] y-filtered values at x-edge columns
 };
 
 struct ChainArgs {
     int B, H, W;
-    int Ex, ne, edge_all, ntx;
+    int Ex, ne, edge_all, nst;  // nst = chain units
     Casc k;
     int nplanes;          // n*4
-    float M[16];          // full-tile state transfer (column-major: M[k*4+r])
-    float Mlast[16];      // last (possibly partial) tile
+    float M[16];          // full-stripe state transfer (column-major: M[k*4+r])
+    float Mlast[16];      // last (possibly partial) stripe
     int n;                // terms in the batch
     const float* edge;    // float4 [n][B][ne][H]
-    float* lcarry;        // in: local carries, out: chained carries (state at tile start)
+    float* lcarry;        // in: stripe end states (zero start), out: chained carries (state at stripe start)
     float Rx[16];         // right extension: bstate = Rx . s(W) + sum_e bx[e] Y(W-2-e)
     const float4* bx;     // [Ex] (see right_ext_coeffs)
     float* bstate;        // float4 [n][B][H][4 planes] backward start state
@@ -443,7 +476,9 @@ struct Pass2Args {
     Casc k;
     TermDev t;
     int ngroups;       // ceil(t.n / G2)
-    float Hm[TILE][4]; // homogeneous response of the cascade to a unit state
+    int nst;           // chain units (carries per row and term)
+    int unit_cols;     // columns per chain unit (32 or STRIPE)
+    float Hm[STRIPE][4];  // homogeneous response of the cascade to a unit state at the unit start
     float wscale;      // g^2: undoes the two pure x sweeps (1 for box)
     int rb0, nrb_run;     // 128-row blocks [rb0, rb0 + nrb_run) in this launch
     int tiles_per_chunk;  // x-chunking of rows (gauss); == ntx for one chunk
@@ -454,7 +489,7 @@ struct Pass2Args {
     int xlpt, xb1, xb2, xord;
     int warm_tiles;       // warm-up tiles of a chunk's backward sweep
     const float* floc;
-    const float* carry;   // chained carries float4 [n][B][ntx][H][4]
+    const float* carry;   // chained carries float4 [n][B][nst][H][4] (state at each stripe start)
     const float* bstate;  // float4 [n][B][H][4]
     float* part;          // [ngroups*2][B][W][H]
     int order;            // k_pass2_gr block order (TBF_OPT_P2_ORDER)
@@ -520,34 +555,28 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     extern __shared__ float smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    // block order (a.order): 0 column tile fastest, then y-chunk, term group;
-    // 1 term group fastest (the groups sharing a column tile's f run
-    // together), then column tile, y-chunk; 2 y-chunk fastest
-    int gblk, tile_r, chunk;
-    if (a.order == 1) {
+    // one block = one term x one stripe of P1_WARPS column tiles (warp w =
+    // tile w of the stripe).  Block order: term fastest (the blocks sharing a
+    // stripe's f run together), then stripe, y-chunk slowest (planned chunks
+    // are numbered largest first)
+    int term, stripe_r, chunk;
+    {
         int idx = blockIdx.x;
-        gblk = idx % a.ngb;
-        idx /= a.ngb;
-        tile_r = idx % a.ntx_run;
-        chunk = idx / a.ntx_run;
-    } else if (a.order == 2) {
-        chunk = blockIdx.x % a.nyc;
-        tile_r = blockIdx.x / a.nyc;
-        gblk = blockIdx.y;
-    } else {
-        tile_r = blockIdx.x % a.ntx_run;
-        chunk = blockIdx.x / a.ntx_run;
-        gblk = blockIdx.y;
+        term = idx % a.t.n;
+        idx /= a.t.n;
+        stripe_r = idx % a.nst_run;
+        chunk = idx / a.nst_run;
     }
-    const int term = gblk * P1_WARPS + warp;
-    if (term >= a.t.n) return;  // whole warp; no block-level barriers below
     const int b = blockIdx.z;
     const int H = a.H, W = a.W;
-    const int tile_x = a.tile0 + tile_r;
+    const int stripe = a.st0 + stripe_r;
+    const int tile_x = stripe * P1_WARPS + warp;
     const int x0 = tile_x * TILE;
     const int x = x0 + lane;
     const bool xv = x < W;
     const int xc = xv ? x : W - 1;
+    // the last stripe's warps past the image edge (tlen <= 0) run clamped
+    // columns without storing anything: every warp takes part in the hand-off
     const int tlen = min(TILE, W - x0);
     // segment tile [row][col] of float4 (the 4 planes of a pixel adjacent),
     // padded row stride BUF_LD: column access (phases A/B) is contiguous, row
@@ -661,8 +690,14 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     const int nrbk = (H + FL_RB - 1) / FL_RB;
     float4* const fl0 = reinterpret_cast<float4*>(a.floc) + ((size_t)term * a.B + b) * nrbk * W * (size_t)FL_RB;
     float4* const ed0 = reinterpret_cast<float4*>(a.edge) + ((size_t)term * a.B + b) * a.ne * (size_t)H;
+    // the chain unit's end state (written by its last warp): float4 [term][b][unit][H][4 planes]
+    const bool handoff = a.unit > 1;  // block-uniform
     float4* const lc0 = reinterpret_cast<float4*>(a.lcarry) +
-                        (((size_t)term * a.B + b) * a.ntx + tile_x) * (size_t)H * 4;
+                        (((size_t)term * a.B + b) * a.nun + tile_x / a.unit) * (size_t)H * 4;
+    // hand-off slots between the stripe's warps: slot w (warp w -> w+1) holds
+    // one float4 per plane and row, after the P1_WARPS tiles
+    float4* const hand = reinterpret_cast<float4*>(smem) + (size_t)P1_WARPS * TILE * BUF_LD;
+    int nout = 0;  // output segments done (the hand-off barriers pair up per segment)
     const int nseg = (Bend - R0 + TILE - 1) / TILE;  // local segments of this chunk
     const int nsteps = 2 * nseg;
     float seg_f[TILE];
@@ -776,11 +811,33 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
         }
         if (i0 >= R1) continue;  // warm-up / extension segment: no output
         __syncwarp();
-        // epilogue: lane <-> row i; tile-local zero-state forward along x
+        // epilogue: lane <-> row i; forward along x over the tile's 32
+        // columns, starting from the state the warp of the tile to the left
+        // hands over (zero at the stripe's first tile: the stripes are
+        // chained by k_chain, the tiles of a stripe here).  Named barriers
+        // per link w -> w+1: FULL (1 + w) when the slot is written, EMPTY
+        // (1 + P1_WARPS + w) when it has been read.
         const int i = i0 + lane;
-        if (lane < min(len, R1 - i0)) {
-            float lv1[4] = {0.f, 0.f, 0.f, 0.f}, lv2[4] = {0.f, 0.f, 0.f, 0.f};
-            float ly1[4] = {0.f, 0.f, 0.f, 0.f}, ly2[4] = {0.f, 0.f, 0.f, 0.f};
+        const bool rowv = lane < min(len, R1 - i0);
+        const bool last_out = i0 == R0;  // segments run bottom to top
+        float lv1[4], lv2[4], ly1[4], ly2[4];
+        if (handoff && warp > 0) {
+            named_bar_sync(1 + (warp - 1), 64);
+            const float4* hs = hand + ((size_t)(warp - 1) * 4) * TILE + lane;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const float4 c = hs[p * TILE];
+                lv1[p] = c.x;
+                lv2[p] = c.y;
+                ly1[p] = c.z;
+                ly2[p] = c.w;
+            }
+            if (!last_out) named_bar_arrive(1 + P1_WARPS + (warp - 1), 64);
+        } else {
+#pragma unroll
+            for (int p = 0; p < 4; ++p) lv1[p] = lv2[p] = ly1[p] = ly2[p] = 0.f;
+        }
+        if (rowv && tlen > 0) {
             float4* fl = fl0 + ((size_t)(i / FL_RB) * W + x0) * FL_RB + (i % FL_RB);
             const bool edge_tile = a.edge_all || x0 <= a.Ex || x0 + tlen - 1 >= W - 1 - a.Ex;
             if (tlen == TILE && !edge_tile) {
@@ -821,10 +878,21 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                     }
                 }
             }
+        }
+        if (handoff && warp < P1_WARPS - 1) {
+            if (nout > 0) named_bar_sync(1 + P1_WARPS + warp, 64);  // the slot's previous state was read
+            float4* hs = hand + ((size_t)warp * 4) * TILE + lane;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) hs[p * TILE] = f4(lv1[p], lv2[p], ly1[p], ly2[p]);
+            named_bar_arrive(1 + warp, 64);
+        } else if (rowv && (handoff || tlen > 0)) {
+            // the unit's end state (clamped warps past the image edge pass
+            // the state of its last column through unchanged)
             float4* lc = lc0 + (size_t)i * 4;
 #pragma unroll
             for (int p = 0; p < 4; ++p) lc[p] = f4(lv1[p], lv2[p], ly1[p], ly2[p]);
         }
+        ++nout;
         __syncwarp();
     }
 }
@@ -871,27 +939,27 @@ __global__ void __launch_bounds__(128) k_chain(const __grid_constant__ ChainArgs
         for (int q = 0; q < 8; ++q)
             if (xb + q < 0) cstep4(u[q], v1, v2, y1, y2, k, o);
     }
-    // chain along x: C_t = state at tile start; s_{t+1} = M s_t + L_t
+    // chain along x over the stripes: C_t = state at stripe start; s_{t+1} = M s_t + L_t
     float M[16], Ml[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
         M[q] = a.M[q];
         Ml[q] = a.Mlast[q];
     }
-    float4* lc = reinterpret_cast<float4*>(a.lcarry) + ((size_t)bt * a.ntx * H + i) * 4;
-    const size_t tstride = (size_t)H * 4;  // float4 stride between tiles
-    for (int tb = 0; tb < a.ntx; tb += 4) {
+    float4* lc = reinterpret_cast<float4*>(a.lcarry) + ((size_t)bt * a.nst * H + i) * 4;
+    const size_t tstride = (size_t)H * 4;  // float4 stride between stripes
+    for (int tb = 0; tb < a.nst; tb += 4) {
         float4 L[4][4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
             for (int p = 0; p < 4; ++p)
-                L[q][p] = tb + q < a.ntx ? lc[(size_t)(tb + q) * tstride + p] : f4(0.f, 0.f, 0.f, 0.f);
+                L[q][p] = tb + q < a.nst ? lc[(size_t)(tb + q) * tstride + p] : f4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int t = tb + q;
-            if (t < a.ntx) {
-                const bool last = t == a.ntx - 1;
+            if (t < a.nst) {
+                const bool last = t == a.nst - 1;
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
                     lc[(size_t)t * tstride + p] = f4(v1[p], v2[p], y1[p], y2[p]);
@@ -956,7 +1024,7 @@ template <int G>
 struct P2Ctx {
     const float4* fl[G];  // this row, x = 0, per term
     const float* fT;
-    const float4* cr[G];  // chained carries, this row, tile 0, per term
+    const float4* cr[G];  // chained carries, this row, stripe 0, per term
     size_t H;             // float4 stride between x
     float nu_hi[G], nu_lo[G], wt[G];
 };
@@ -993,7 +1061,7 @@ __device__ __forceinline__ void p2_step4(const Pass2Args& a, const P2Ctx<G>& c, 
     for (int q = 0; q < 4; ++q) {
         const int m = mb - q;
         if (full || m >= 0) {
-            const float4 h = *reinterpret_cast<const float4*>(&a.Hm[m][0]);
+            const float4 h = *reinterpret_cast<const float4*>(&a.Hm[(x0 & (a.unit_cols - 1)) + m][0]);
             float num = 0.f, den = 0.f;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
@@ -1035,7 +1103,7 @@ __device__ __forceinline__ void p2_tile(const Pass2Args& a, const P2Ctx<G>& c, i
     for (int g = 0; g < G; ++g)
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-            const float4 v = c.cr[g][(size_t)t * c.H * 4 + p];
+            const float4 v = c.cr[g][(size_t)(t * TILE / a.unit_cols) * c.H * 4 + p];
             C[g][p][0] = v.x;
             C[g][p][1] = v.y;
             C[g][p][2] = v.z;
@@ -1061,499 +1129,6 @@ __device__ __forceinline__ void p2_tile(const Pass2Args& a, const P2Ctx<G>& c, i
             p2_step4<G, OUT, SM>(a, c, x0, mb, false, fa, va, C, p1, p2, q1, q2, pn, pd, iv, sb);
         }
     }
-}
-
-// ---------------------------------------------------------------------------
-// Pass 2, TMA-staged variant (W % 32 == 0): per block 128 rows x G terms x one
-// x-chunk.  For every x-step the block's inputs are contiguous rows in HBM
-// (row-block tiled F_loc float4 and fT, see xm_index), so one thread
-// streams them into a P2T_NST-stage shared-memory ring with
-// cp.async.bulk (TMA bulk copies) completing on mbarriers; the 128 threads
-// consume from shared memory.  Deep prefetch without register cost.
-// ---------------------------------------------------------------------------
-
-constexpr int P2T_STEPS = 4;                  // x-steps per stage
-constexpr int P2T_NST = 4;                    // stages in the ring
-constexpr int P2T_THREADS = P2_THREADS + 32;  // 4 consumer warps + 1 producer warp
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_fence_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "LAB_WAIT%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra LAB_WAIT%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-template <int G>
-constexpr int p2t_smem_bytes() {
-    return 256 + P2T_NST * P2T_STEPS * (G * P2_THREADS * 16 + P2_THREADS * 4);
-}
-
-// Requires W % 32 == 0 (whole tiles) and H % 4 == 0 (16-byte aligned rows).
-template <int G, int MINB>
-__global__ void __launch_bounds__(P2T_THREADS, MINB) k_pass2_tma(const __grid_constant__ Pass2Args a) {
-    extern __shared__ __align__(128) unsigned char sm[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm);
-    uint64_t* empty = full + P2T_NST;
-    float4* Fb = reinterpret_cast<float4*>(sm + 256);  // [NST][STEPS][G][128]
-    float* Tb = reinterpret_cast<float*>(Fb + P2T_NST * P2T_STEPS * G * P2_THREADS);  // [NST][STEPS][128]
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int chunk = blockIdx.x / a.nrb_run;
-    const int i0 = (a.rb0 + blockIdx.x % a.nrb_run) * P2_THREADS;
-    const int H = a.H, W = a.W;
-    const int nrow = min(P2_THREADS, H - i0);
-    const int nrow4 = (nrow + 3) & ~3;
-    const int grp = blockIdx.y;
-    const int b = blockIdx.z;
-    const int j0 = grp * G;
-    const int nt = min(G, a.t.n - j0);
-
-    const int t_lo = chunk * a.tiles_per_chunk;
-    const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
-    // a chunk whose warm-up would reach the right edge starts there from the
-    // exact chained backward state instead (a clamped warm-up would be < K)
-    const bool last_chunk = t_hi + a.warm_tiles >= a.ntx;
-    const int t_top = last_chunk ? a.ntx - 1 : t_hi - 1 + a.warm_tiles;
-    const int ntiles = t_top - t_lo + 1;
-    const int nblk = ntiles * (TILE / P2T_STEPS);
-    const int x_top = t_top * TILE + TILE - 1;
-
-    if (tid == 0) {
-        for (int st = 0; st < P2T_NST; ++st) {
-            mbar_init(&full[st], 1);
-            mbar_init(&empty[st], P2_THREADS / 32);
-        }
-        mbar_fence_init();
-    }
-    __syncthreads();
-
-    if (warp == P2_THREADS / 32) {  // ---- producer warp ----
-        if ((tid & 31) == 0) {
-            const float4* flrow[G];
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const int j = min(j0 + g, a.t.n - 1);
-                flrow[g] = reinterpret_cast<const float4*>(a.floc) +
-                           (((size_t)j * a.B + b) * ((H + FL_RB - 1) / FL_RB) + i0 / FL_RB) * W * (size_t)FL_RB;
-            }
-            const float* fTrow = a.fT + xm_index(b, 0, i0, W, H);
-            const uint32_t bytes = (uint32_t)(P2T_STEPS * (G * nrow * 16 + nrow4 * 4));
-            const size_t sbs = (size_t)W * FL_RB;  // stride between 32-row blocks
-            for (int blk = 0; blk < nblk; ++blk) {
-                const int st = blk % P2T_NST;
-                if (blk >= P2T_NST) mbar_wait(&empty[st], ((blk / P2T_NST) - 1) & 1);
-                mbar_expect_tx(&full[st], bytes);
-                const int xs = x_top - blk * P2T_STEPS;
-#pragma unroll
-                for (int q = 0; q < P2T_STEPS; ++q) {
-                    const int x = xs - q;
-                    // one bulk copy per 32-row block of the block's rows
-                    for (int r0 = 0; r0 < nrow; r0 += FL_RB) {
-                        const int rows = min(FL_RB, nrow - r0);
-                        const size_t src = (size_t)(r0 / FL_RB) * sbs + (size_t)x * FL_RB;
-#pragma unroll
-                        for (int g = 0; g < G; ++g)
-                            bulk_g2s(Fb + ((st * P2T_STEPS + q) * G + g) * P2_THREADS + r0, flrow[g] + src,
-                                     (uint32_t)rows * 16, &full[st]);
-                        bulk_g2s(Tb + (st * P2T_STEPS + q) * P2_THREADS + r0, fTrow + src,
-                                 (uint32_t)((rows + 3) / 4 * 4) * 4, &full[st]);
-                    }
-                }
-            }
-        }
-        return;
-    }
-
-    // ---- consumers: one row per thread ----
-    const int i_raw = i0 + tid;
-    const bool iv = i_raw < H;
-    const int i = iv ? i_raw : H - 1;
-    const Casc k = a.k;
-    float nu_hi[G], nu_lo[G], wt[G];
-    const float4* crp[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        const int j = min(j0 + g, a.t.n - 1);
-        nu_hi[g] = a.t.nu_hi[j];
-        nu_lo[g] = a.t.nu_lo[j];
-        wt[g] = g < nt ? a.t.w[j] * a.wscale : 0.f;
-        crp[g] = reinterpret_cast<const float4*>(a.carry) + (((size_t)j * a.B + b) * a.ntx * H + i) * 4;
-    }
-    const size_t xpl = xm_plane(a.B, W, H);
-    float* pn = a.part + (size_t)(grp * 2 + 0) * xpl + xm_index(b, 0, i_raw, W, H);
-    float* pd = a.part + (size_t)(grp * 2 + 1) * xpl + xm_index(b, 0, i_raw, W, H);
-
-    float p1[G][4], p2[G][4], q1[G][4], q2[G][4], C[G][4][4];
-    float4 Cn[G][4];
-    auto load_Cn = [&](int t) {
-        t = max(t, 0);
-#pragma unroll
-        for (int g = 0; g < G; ++g)
-#pragma unroll
-            for (int p = 0; p < 4; ++p) Cn[g][p] = crp[g][(size_t)t * H * 4 + p];
-    };
-    auto take_Cn = [&]() {
-#pragma unroll
-        for (int g = 0; g < G; ++g)
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                C[g][p][0] = Cn[g][p].x;
-                C[g][p][1] = Cn[g][p].y;
-                C[g][p][2] = Cn[g][p].z;
-                C[g][p][3] = Cn[g][p].w;
-            }
-    };
-    load_Cn(t_top);
-    take_Cn();
-    load_Cn(t_top - 1);
-    if (last_chunk) {  // exact start state from the chain
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const int j = min(j0 + g, a.t.n - 1);
-            const float4* bs = reinterpret_cast<const float4*>(a.bstate) + (((size_t)j * a.B + b) * H + i) * 4;
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                const float4 v = bs[p];
-                p1[g][p] = v.x;
-                p2[g][p] = v.y;
-                q1[g][p] = v.z;
-                q2[g][p] = v.w;
-            }
-        }
-    } else {  // warm-up: steady state of the exact forward output at x_top
-        mbar_wait(&full[0], 0);
-        const float4 h = *reinterpret_cast<const float4*>(&a.Hm[TILE - 1][0]);
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const float4 fo = Fb[(0 * G + g) * P2_THREADS + tid];
-            const float fin[4] = {fo.x, fo.y, fo.z, fo.w};
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                const float F = fmaf(h.x, C[g][p][0], fmaf(h.y, C[g][p][1],
-                                     fmaf(h.z, C[g][p][2], fmaf(h.w, C[g][p][3], fin[p]))));
-                csteady(F, p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
-            }
-        }
-    }
-
-    int blk = 0;
-#pragma unroll 1
-    for (int t = t_top; t >= t_lo; --t) {
-        if (t != t_top) {
-            take_Cn();
-            load_Cn(t - 1);
-        }
-        const bool out = t < t_hi;
-        const size_t xrow = (size_t)(t * TILE) * FL_RB;
-#pragma unroll 1
-        for (int mb = TILE - 1; mb >= 0; mb -= P2T_STEPS, ++blk) {
-            const int st = blk % P2T_NST;
-            mbar_wait(&full[st], (blk / P2T_NST) & 1);
-#pragma unroll
-            for (int q = 0; q < P2T_STEPS; ++q) {
-                const int m = mb - q;
-                const float4 h = *reinterpret_cast<const float4*>(&a.Hm[m][0]);
-                float num = 0.f, den = 0.f;
-                const float fv = out ? Tb[(st * P2T_STEPS + q) * P2_THREADS + tid] : 0.f;
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const float4 fo = Fb[((st * P2T_STEPS + q) * G + g) * P2_THREADS + tid];
-                    const float fin[4] = {fo.x, fo.y, fo.z, fo.w};
-                    float y[4];
-#pragma unroll
-                    for (int p = 0; p < 4; ++p) {
-                        float F = fmaf(h.x, C[g][p][0], fin[p]);
-                        F = fmaf(h.y, C[g][p][1], F);
-                        F = fmaf(h.z, C[g][p][2], F);
-                        F = fmaf(h.w, C[g][p][3], F);
-                        y[p] = cstep(F, p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
-                    }
-                    if (out) {
-                        float sn, cs;
-                        sincos_fma(phase(nu_hi[g], nu_lo[g], fv), &sn, &cs);
-                        num = fmaf(wt[g], fmaf(cs, y[2], sn * y[3]), num);
-                        den = fmaf(wt[g], fmaf(cs, y[0], sn * y[1]), den);
-                    }
-                }
-                if (out && iv) {
-                    const size_t off = xrow + (size_t)m * FL_RB;
-                    pn[off] = num;
-                    pd[off] = den;
-                }
-            }
-            __syncwarp();
-            if ((tid & 31) == 0) mbar_arrive(&empty[st]);
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Pass 2, cp.async-staged variant with G terms per thread (G = 4 halves the
-// partial num/den and fT traffic of G = 2).  Each thread streams its own
-// 16-byte F_loc slices (and its fT sample) P2A_DEPTH steps ahead into private
-// shared-memory slots with cp.async; no producer warp, no block barriers, no
-// register prefetch buffers (so G = 4 fits the 3-blocks/SM register budget).
-// ---------------------------------------------------------------------------
-
-constexpr int P2A_DEPTH = 8;
-
-template <int G>
-constexpr int p2a_smem_bytes() {
-    return P2A_DEPTH * P2_THREADS * (G * 16 + 4);
-}
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int G>
-__global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_async(const __grid_constant__ Pass2Args a) {
-    extern __shared__ __align__(128) unsigned char sm[];  // same declaration as the TMA variant
-    float4* Fs = reinterpret_cast<float4*>(sm);                                  // [DEPTH][G][128]
-    float* Ts = reinterpret_cast<float*>(Fs + P2A_DEPTH * G * P2_THREADS);       // [DEPTH][128]
-    const int tid = threadIdx.x;
-    const int chunk = blockIdx.x / a.nrb_run;
-    const int i_raw = (a.rb0 + blockIdx.x % a.nrb_run) * P2_THREADS + tid;
-    const int H = a.H, W = a.W;
-    const bool iv = i_raw < H;
-    const int i = iv ? i_raw : H - 1;
-    const int grp = blockIdx.y;
-    const int b = blockIdx.z;
-    const int j0 = grp * G;
-    const int nt = min(G, a.t.n - j0);
-    const Casc k = a.k;
-    float nu_hi[G], nu_lo[G], wt[G];
-    const float4* fl[G];
-    const float4* crp[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        const int j = min(j0 + g, a.t.n - 1);
-        nu_hi[g] = a.t.nu_hi[j];
-        nu_lo[g] = a.t.nu_lo[j];
-        wt[g] = g < nt ? a.t.w[j] * a.wscale : 0.f;
-        fl[g] = reinterpret_cast<const float4*>(a.floc) +
-                (((size_t)j * a.B + b) * ((H + FL_RB - 1) / FL_RB) + i / FL_RB) * W * (size_t)FL_RB + (i % FL_RB);
-        crp[g] = reinterpret_cast<const float4*>(a.carry) + (((size_t)j * a.B + b) * a.ntx * H + i) * 4;
-    }
-    const float* fT = a.fT + xm_index(b, 0, i, W, H);
-    const size_t xpl = xm_plane(a.B, W, H);
-    float* pn = a.part + (size_t)(grp * 2 + 0) * xpl + xm_index(b, 0, i_raw, W, H);
-    float* pd = a.part + (size_t)(grp * 2 + 1) * xpl + xm_index(b, 0, i_raw, W, H);
-
-    const int t_lo = chunk * a.tiles_per_chunk;
-    const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
-    // a chunk whose warm-up would reach the right edge starts there from the
-    // exact chained backward state instead (a clamped warm-up would be < K)
-    const bool last_chunk = t_hi + a.warm_tiles >= a.ntx;
-    const int x_hi = last_chunk ? W - 1 : (t_hi + a.warm_tiles) * TILE - 1;
-    const int x_lo = t_lo * TILE;
-    const int x_out = min(W, t_hi * TILE);  // outputs for x < x_out
-    const int nx = x_hi - x_lo + 1;
-
-    auto issue = [&](int s) {  // stage slot s % DEPTH <- step s (x = x_hi - s), clamped
-        const int x = max(x_hi - s, x_lo);
-        const int slot = s % P2A_DEPTH;
-#pragma unroll
-        for (int g = 0; g < G; ++g)
-            cp_async16(&Fs[(slot * G + g) * P2_THREADS + tid], fl[g] + (size_t)x * FL_RB);
-        cp_async4(&Ts[slot * P2_THREADS + tid], fT + (size_t)x * FL_RB);
-        cp_async_commit();
-    };
-#pragma unroll
-    for (int s = 0; s < P2A_DEPTH - 1; ++s) issue(s);
-
-    float C[G][4][4];
-    auto load_C = [&](int t) {
-#pragma unroll
-        for (int g = 0; g < G; ++g)
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                const float4 v = crp[g][(size_t)t * H * 4 + p];
-                C[g][p][0] = v.x;
-                C[g][p][1] = v.y;
-                C[g][p][2] = v.z;
-                C[g][p][3] = v.w;
-            }
-    };
-    float p1[G][4], p2[G][4], q1[G][4], q2[G][4];
-    load_C(x_hi >> 5);
-    if (last_chunk) {  // exact start state from the chain
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const int j = min(j0 + g, a.t.n - 1);
-            const float4* bs = reinterpret_cast<const float4*>(a.bstate) + (((size_t)j * a.B + b) * H + i) * 4;
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                const float4 v = bs[p];
-                p1[g][p] = v.x;
-                p2[g][p] = v.y;
-                q1[g][p] = v.z;
-                q2[g][p] = v.w;
-            }
-        }
-    } else {  // warm-up: steady state of the exact forward output at x_hi
-        const float4 h = *reinterpret_cast<const float4*>(&a.Hm[x_hi & 31][0]);
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const float4 fo = fl[g][(size_t)x_hi * FL_RB];
-            const float fin[4] = {fo.x, fo.y, fo.z, fo.w};
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                const float F = fmaf(h.x, C[g][p][0], fmaf(h.y, C[g][p][1],
-                                     fmaf(h.z, C[g][p][2], fmaf(h.w, C[g][p][3], fin[p]))));
-                csteady(F, p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
-            }
-        }
-    }
-
-#pragma unroll 1
-    for (int s = 0; s < nx; ++s) {
-        issue(s + P2A_DEPTH - 1);
-        cp_async_wait<P2A_DEPTH - 1>();  // step s has landed (own slots only)
-        const int x = x_hi - s;
-        const int m = x & 31;
-        if (m == 31 && s > 0) load_C(x >> 5);
-        const int slot = s % P2A_DEPTH;
-        const float4 h = *reinterpret_cast<const float4*>(&a.Hm[m][0]);
-        const bool out = x < x_out;
-        const float fv = Ts[slot * P2_THREADS + tid];
-        float num = 0.f, den = 0.f;
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const float4 fo = Fs[(slot * G + g) * P2_THREADS + tid];
-            const float fin[4] = {fo.x, fo.y, fo.z, fo.w};
-            float y[4];
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                float F = fmaf(h.x, C[g][p][0], fin[p]);
-                F = fmaf(h.y, C[g][p][1], F);
-                F = fmaf(h.z, C[g][p][2], F);
-                F = fmaf(h.w, C[g][p][3], F);
-                y[p] = cstep(F, p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
-            }
-            if (out) {
-                float sn, cs;
-                sincos_fma(phase(nu_hi[g], nu_lo[g], fv), &sn, &cs);
-                num = fmaf(wt[g], fmaf(cs, y[2], sn * y[3]), num);
-                den = fmaf(wt[g], fmaf(cs, y[0], sn * y[1]), den);
-            }
-        }
-        if (out && iv) {
-            pn[(size_t)x * FL_RB] = num;
-            pd[(size_t)x * FL_RB] = den;
-        }
-    }
-    cp_async_wait<0>();
-}
-
-template <int G>
-__global__ void __launch_bounds__(P2_THREADS, 3) k_pass2_gauss(const __grid_constant__ Pass2Args a) {
-    const int chunk = blockIdx.x / a.nrb_run;
-    const int i_raw = (a.rb0 + blockIdx.x % a.nrb_run) * P2_THREADS + threadIdx.x;
-    const int H = a.H, W = a.W;
-    const bool iv = i_raw < H;
-    const int i = iv ? i_raw : H - 1;
-    const int grp = blockIdx.y;
-    const int b = blockIdx.z;
-    const int j0 = grp * G;
-    const int nt = min(G, a.t.n - j0);
-    P2Ctx<G> c;
-    c.H = (size_t)H;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        const int j = min(j0 + g, a.t.n - 1);  // padded terms alias the last one (weight 0)
-        c.nu_hi[g] = a.t.nu_hi[j];
-        c.nu_lo[g] = a.t.nu_lo[j];
-        c.wt[g] = g < nt ? a.t.w[j] * a.wscale : 0.f;
-        c.fl[g] = reinterpret_cast<const float4*>(a.floc) +
-                  (((size_t)j * a.B + b) * ((H + FL_RB - 1) / FL_RB) + i / FL_RB) * W * (size_t)FL_RB + (i % FL_RB);
-        c.cr[g] = reinterpret_cast<const float4*>(a.carry) + (((size_t)j * a.B + b) * a.ntx * H + i) * 4;
-    }
-    c.fT = a.fT + xm_index(b, 0, i, W, H);
-    const size_t xpl = xm_plane(a.B, W, H);
-    float* pn = a.part + (size_t)(grp * 2 + 0) * xpl + xm_index(b, 0, i_raw, W, H);
-    float* pd = a.part + (size_t)(grp * 2 + 1) * xpl + xm_index(b, 0, i_raw, W, H);
-
-    const int t_lo = chunk * a.tiles_per_chunk;
-    const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);  // exclusive
-    float p1[G][4], p2[G][4], q1[G][4], q2[G][4];
-    const bool exact_start = t_hi + a.warm_tiles >= a.ntx;  // warm-up would reach the edge
-    if (exact_start) {  // start at the right edge from the exact chained state
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const int j = min(j0 + g, a.t.n - 1);
-            const float4* bs = reinterpret_cast<const float4*>(a.bstate) + (((size_t)j * a.B + b) * H + i) * 4;
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                const float4 v = bs[p];
-                p1[g][p] = v.x;
-                p2[g][p] = v.y;
-                q1[g][p] = v.z;
-                q2[g][p] = v.w;
-            }
-        }
-#pragma unroll 1
-        for (int t = a.ntx - 1; t >= t_hi; --t) p2_tile<G, false>(a, c, t, p1, p2, q1, q2, pn, pd, iv);
-    } else {
-        // warm-up: start from the steady state of the exact forward output at
-        // the warm-up start, then run backward (no output) down to t_hi
-        const int tw = min(a.ntx - 1, t_hi - 1 + a.warm_tiles);
-        const int xs = min(W - 1, tw * TILE + TILE - 1);
-        const int ms = xs - tw * TILE;
-        const float4 h = *reinterpret_cast<const float4*>(&a.Hm[ms][0]);
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const float4 F = c.fl[g][(size_t)xs * FL_RB];
-            const float fin[4] = {F.x, F.y, F.z, F.w};
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                const float4 cv = c.cr[g][(size_t)tw * c.H * 4 + p];
-                const float v = fmaf(h.x, cv.x, fmaf(h.y, cv.y, fmaf(h.z, cv.z, fmaf(h.w, cv.w, fin[p]))));
-                csteady(v, p1[g][p], p2[g][p], q1[g][p], q2[g][p], a.k);
-            }
-        }
-#pragma unroll 1
-        for (int t = tw; t >= t_hi; --t) p2_tile<G, false>(a, c, t, p1, p2, q1, q2, pn, pd, iv);
-    }
-#pragma unroll 1
-    for (int t = t_hi - 1; t >= t_lo; --t) p2_tile<G, true>(a, c, t, p1, p2, q1, q2, pn, pd, iv);
 }
 
 // Pass 2 with the term groups of a block summed on chip: 4 warps = 32 rows x
@@ -1622,7 +1197,7 @@ __global__ void __launch_bounds__(32 * P2R_GR, TBF_P2_MINB) k_pass2_gr(const __g
         c.wt[g] = g < nt ? a.t.w[j] * a.wscale : 0.f;
         c.fl[g] = reinterpret_cast<const float4*>(a.floc) +
                   (((size_t)j * a.B + b) * ((H + FL_RB - 1) / FL_RB) + i / FL_RB) * W * (size_t)FL_RB + (i % FL_RB);
-        c.cr[g] = reinterpret_cast<const float4*>(a.carry) + (((size_t)j * a.B + b) * a.ntx * H + i) * 4;
+        c.cr[g] = reinterpret_cast<const float4*>(a.carry) + (((size_t)j * a.B + b) * a.nst * H + i) * 4;
     }
     c.fT = a.fT + xm_index(b, 0, i, W, H);
     const size_t xpl = xm_plane(a.B, W, H);
@@ -1662,15 +1237,14 @@ __global__ void __launch_bounds__(32 * P2R_GR, TBF_P2_MINB) k_pass2_gr(const __g
         } else {
             const int tw = min(a.ntx - 1, t_hi - 1 + a.warm_tiles);
             const int xs = min(W - 1, tw * TILE + TILE - 1);
-            const int ms = xs - tw * TILE;
-            const float4 h = *reinterpret_cast<const float4*>(&a.Hm[ms][0]);
+            const float4 h = *reinterpret_cast<const float4*>(&a.Hm[xs & (a.unit_cols - 1)][0]);
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 const float4 F = c.fl[g][(size_t)xs * FL_RB];
                 const float fin[4] = {F.x, F.y, F.z, F.w};
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
-                    const float4 cv = c.cr[g][(size_t)tw * c.H * 4 + p];
+                    const float4 cv = c.cr[g][(size_t)(xs / a.unit_cols) * c.H * 4 + p];
                     const float v = fmaf(h.x, cv.x, fmaf(h.y, cv.y, fmaf(h.z, cv.z, fmaf(h.w, cv.w, fin[p]))));
                     csteady(v, p1[g][p], p2[g][p], q1[g][p], q2[g][p], a.k);
                 }
@@ -2157,6 +1731,8 @@ size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
     int B, H, W, Ey, Ex, nseg, ntx, ne, edge_all;
+    int nst;  // stripes of P1_WARPS column tiles (pass-1 blocks per term and y-chunk)
+    int unit, nun;  // x chain unit in column tiles (P1_WARPS or 1) and units per row
     int nyc, ych_rows, ywarm;  // pass-1 y-chunking (nseg = checkpoint segments per chunk)
     int ychb[TBF_MAX_YCH + 1];  // chunk boundaries (ych_rows = the largest chunk)
     bool ych_lpt;               // chunks of unequal size, dispatched largest first
@@ -2178,10 +1754,8 @@ int g_lpt_split = 3;    // tbf_set_option(TBF_OPT_LPT_SPLIT): bits 1/2 = planned
                         // 4/8 = also in the host entry's strip/band launches
 int g_p1_occ = 3;       // tbf_set_option(TBF_OPT_P1_OCC): pass-1 blocks per SM (2 leaves room for a pass-2 block)
 int g_p2_chunks = 0;    // tbf_set_option(TBF_OPT_P2_CHUNKS): 0 = automatic
-int g_pass2_tma = 3;    // tbf_set_option(TBF_OPT_PASS2_TMA): 0 register prefetch (G=2), 1/2 TMA producer warp, 3 auto (default), 4 cp.async G=4
 int g_pipeline = 0;     // tbf_set_option(TBF_OPT_PIPELINE) (measured: no gain on B200, SMs time-slice)
 int g_auto_batches = 2; // tbf_set_option(TBF_OPT_BATCHES): batches when batch_terms <= 0
-int g_p1_order = -1;    // tbf_set_option(TBF_OPT_P1_ORDER): block order of pass 1 (-1 auto)
 int g_p2_order = 0;     // tbf_set_option(TBF_OPT_P2_ORDER): block order of the block-summed pass 2 (same-box A/B: orders 0 and 1 equal)
 int g_host_strips = 0;  // tbf_set_option(TBF_OPT_HOST_STRIPS): column strips of the host input (0 auto)
 int g_host_bands = 0;   // tbf_set_option(TBF_OPT_HOST_BANDS): row bands of the host output (0 auto)
@@ -2320,6 +1894,13 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     L->Ey = box ? 0 : std::max(0, std::min(sp->ext_y, H - 1));
     L->Ex = box ? 0 : std::max(0, std::min(sp->ext_x, W - 1));
     L->ntx = (W + TILE - 1) / TILE;
+    L->nst = (W + STRIPE - 1) / STRIPE;
+    // x carries per stripe, except for very long decays (sigma_s >~ 130):
+    // there the correction by the unit-state response over 128 columns
+    // loses fp32 digits to cancellation (measured: 0.27 vs 0.18 max error at
+    // sigma_s = 300), and 32-column units keep the round-1 accuracy
+    L->unit = (!box && sp->ext_x > 1536) ? 1 : P1_WARPS;
+    L->nun = (L->ntx + L->unit - 1) / L->unit;
     L->edge_all = 2 * (L->Ex + 1) >= W;
     L->ne = L->edge_all ? W : 2 * (L->Ex + 1);
     int tb;
@@ -2347,7 +1928,7 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     L->ych_rows = H;
     if (!box) {
         const double slots = 148.0 * P1_BLOCKS_PER_SM;
-        const double blocks1 = (double)L->ntx * ((tb + P1_WARPS - 1) / P1_WARPS) * B;
+        const double blocks1 = (double)L->nst * tb * B;
         double best = -1.0;
         int best_n = 1;
         for (int nyc = 1; nyc <= 16; ++nyc) {
@@ -2381,7 +1962,7 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     if (!box && g_p1_ychunks <= 0 && (lpt == 2 || (lpt == 1 && (g_lpt_split & 1))) && L->nb == 1) {
         // few waves: plan unequal chunks, largest first (p1_plan_split)
         const int slots = 148 * P1_BLOCKS_PER_SM;
-        const long long per_chunk = (long long)L->ntx * ((tb + P1_WARPS - 1) / P1_WARPS) * B;
+        const long long per_chunk = (long long)L->nst * tb * B;
         // (not for short columns or launches under a wave per chunk level:
         // config 1, 512 rows and 64 blocks, was 6% slower with the planned
         // 3-way split; such launches are latency-bound, which the model does
@@ -2442,7 +2023,7 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     L->s_floc = q;  // row-block tiled like xm_index (padded to whole FL_RB-row blocks)
     q = align_up(q + (size_t)tb * 4 * B * W * ((size_t)(H + FL_RB - 1) / FL_RB * FL_RB) * 4);
     L->s_lc = q;
-    if (!box) q = align_up(q + (size_t)tb * 16 * B * L->ntx * H * 4);
+    if (!box) q = align_up(q + (size_t)tb * 16 * B * L->nun * H * 4);
     L->s_edge = q;
     if (!box) q = align_up(q + (size_t)tb * 4 * B * L->ne * H * 4);
     L->s_ext = q;  // (unused: the right x-extension is in closed form)
@@ -2585,6 +2166,9 @@ int validate(const tbf_spatial* sp, const tbf_terms* terms, int tbeg, int tend) 
 }
 
 constexpr int P1_SMEM = P1_WARPS * 4 * G1 * TILE * BUF_LD * 4;
+// Gaussian pass 1: the segment tiles plus the x hand-off slots between the
+// stripe's warps (73.7 KB: 3 blocks per SM still fit the 228 KB)
+constexpr int P1_SMEM_GAUSS = P1_SMEM + (P1_WARPS - 1) * 4 * TILE * 16;
 constexpr int P1_SMEM_OCC2 = 80 * 1024;  // padded request: at most 2 pass-1 blocks per SM
 
 // cudaFuncSetAttribute applies to the current device only: done once per
@@ -2597,14 +2181,6 @@ void set_p1_smem() {
     dev = std::max(0, std::min(dev, 255));
     std::lock_guard<std::mutex> g(mu);
     if (done_mask[dev >> 6] & (1ull << (dev & 63))) return;
-    cudaFuncSetAttribute(k_pass2_async<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         p2a_smem_bytes<4>());
-    cudaFuncSetAttribute(k_pass2_async<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         p2a_smem_bytes<2>());
-    cudaFuncSetAttribute(k_pass2_tma<G2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         p2t_smem_bytes<G2>());
-    cudaFuncSetAttribute(k_pass2_tma<G2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         p2t_smem_bytes<G2>());
     cudaFuncSetAttribute(k_pass2_gr<G2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2R_SMEM);
     cudaFuncSetAttribute(k_pass2_gr<G2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2R_SMEM);
     cudaFuncSetAttribute(k_pass1_gauss<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
@@ -2622,13 +2198,13 @@ void set_p1_smem() {
 // Pass-2 x-chunking of one batch's launch: equal chunks when rows x groups
 // cannot fill the GPU (fitted heuristic), or for the device entry's
 // single-batch runs of a few waves the planned unequal split (p2_plan_split,
-// at most 3 chunks, costliest first).  `ngroups` thread groups of g2run terms,
-// `npart` k_pass2_gr group blocks (p2var 6).
+// at most 3 chunks, costliest first).  `ngroups` thread groups of G2 terms,
+// `npart` k_pass2_gr group blocks.
 struct P2Plan {
     int nchunk, tiles_per_chunk, warm_tiles;
     int xlpt, xb1, xb2, xord;
 };
-P2Plan p2_chunk_plan(const Layout& L, const tbf_spatial* sp, int ngroups, int npart, int g2run, int p2var,
+P2Plan p2_chunk_plan(const Layout& L, const tbf_spatial* sp, int ngroups, int npart,
                      bool hpipe) {
     const bool box = sp->kind == TBF_SPATIAL_BOX;
     const int B = L.B, nrb = (L.H + P2_THREADS - 1) / P2_THREADS;
@@ -2651,7 +2227,7 @@ P2Plan p2_chunk_plan(const Layout& L, const tbf_spatial* sp, int ngroups, int np
         const long long target = 148LL * 12 * 32 * 3 / 2;  // ~1.5 waves of 12 warps/SM
         const long long wave = 148LL * 12 * 32;
         // measured: G=4 prefers fewer, longer rows unless the GPU is far from full
-        const int max_chunks = (g2run == 4 && threads * 2 >= wave) ? 2 : 64;
+        const int max_chunks = 64;
         while (threads * nchunk < target && nchunk < max_chunks) {
             const int tpc = (L.ntx + 2 * nchunk - 1) / (2 * nchunk);
             // warm-up <= 25% of a chunk; below one wave (latency-bound small
@@ -2664,7 +2240,7 @@ P2Plan p2_chunk_plan(const Layout& L, const tbf_spatial* sp, int ngroups, int np
     pp.tiles_per_chunk = (L.ntx + nchunk - 1) / nchunk;
     nchunk = (L.ntx + pp.tiles_per_chunk - 1) / pp.tiles_per_chunk;
     pp.nchunk = nchunk;
-    if (box || p2var != 6 || L.nb != 1) return pp;
+    if (box || L.nb != 1) return pp;
     // unequal x-chunks (at most 3), costliest first: the development override
     // TBF_P2_XSPLIT (widths in tiles, left to right), else the planner for
     // launches of a few waves (device entry only: the host entry's band
@@ -2862,7 +2438,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
     // in pass 1), the range check and transpose once the whole input is in
     const bool hpipe = hio && !box && L.nslot == 1 && out;
     std::vector<cudaEvent_t> ev_strip;
-    std::vector<int> sb{0, L.ntx};  // strip boundaries in column tiles
+    std::vector<int> sb{0, L.nst};  // strip boundaries in stripes (P1_WARPS column tiles)
     cudaEvent_t e_ready = nullptr;
     if (hio) {
         cudaStream_t sh = aux_stream(1);
@@ -2870,11 +2446,11 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         e_ready = event_get();
         cudaEventRecord(e_ready, st);  // term table queued, earlier users of f done
         cudaStreamWaitEvent(sh, e_ready, 0);
-        if (hpipe) sb = quad_split(L.ntx, hio->strips, true);
+        if (hpipe) sb = quad_split(L.nst, hio->strips, true);
         float* df = const_cast<float*>(f);
         for (size_t s = 0; s + 1 < sb.size(); ++s) {
-            const int x0 = sb[s] * TILE;
-            const int cols = std::min(W, sb[s + 1] * TILE) - x0;
+            const int x0 = sb[s] * STRIPE;
+            const int cols = std::min(W, sb[s + 1] * STRIPE) - x0;
             {
                 Prof pr(KK_H2D, sh);
                 cudaMemcpy2DAsync(df + x0, (size_t)W * 4, hio->h_f + x0, (size_t)W * 4, (size_t)cols * 4,
@@ -2906,10 +2482,11 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
     // (measured: ~1% faster on configs 2-4 now that it no longer spills)
     const bool fold = g_pass1_fold && !box &&
                       std::log10(std::max(terms->T, 1.0)) - 4.0 * std::log10(sp->g1 * sp->g2) < 34.0;
-    double M[16], Mlast[16], Hm[TILE][4];
+    double M[16], Mlast[16], Hm[STRIPE][4];
     if (!box) {
-        cascade_responses(sp, TILE, M, Hm);
-        cascade_responses(sp, W - (L.ntx - 1) * TILE, Mlast, nullptr);
+        const int ucols = L.unit * TILE;
+        cascade_responses(sp, ucols, M, Hm);
+        cascade_responses(sp, W - (L.nun - 1) * ucols, Mlast, nullptr);
     }
 
     if (s2 != st) {
@@ -2954,29 +2531,22 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p1.ne = L.ne;
         p1.edge_all = L.edge_all;
         p1.ntx = L.ntx;
-        p1.tile0 = 0;
-        p1.ntx_run = L.ntx;
+        p1.nst = L.nst;
+        p1.st0 = 0;
+        p1.nst_run = L.nst;
+        p1.unit = L.unit;
+        p1.nun = L.nun;
         p1.k = kc;
         p1.t = td;
-        p1.ngroups = (n + G1 - 1) / G1;
         p1.ckpt = ckpt;
         p1.floc = floc;
         p1.lcarry = lc;
         p1.edge = edge;
-        dim3 g1(L.ntx * (box ? 1 : L.nyc), (p1.ngroups + P1_WARPS - 1) / P1_WARPS, B);
-        p1.ngb = (int)g1.y;
-        // automatic: term groups fastest when many groups share a column
-        // tile's f (measured: -2.1% on config 3 with 34 groups, flat with 9,
-        // +0.3% with 6)
-        // unequal chunks: order 1 (y-chunk index slowest), so the largest
-        // chunks go first (measured on config 2: order 1 as fast as tile-fastest
-        // with the chunk slowest, and a separate decode branch cost registers)
-        p1.order = box ? 0 : (g_p1_order >= 0 ? g_p1_order : ((p1.ngb >= 12 || L.ych_lpt) ? 1 : 0));
-        auto p1grid = [&](int ntx_run) {  // launch shape for the block order
-            return p1.order == 1 ? dim3(ntx_run * L.nyc * p1.ngb, 1, B) : dim3(ntx_run * L.nyc, p1.ngb, B);
-        };
-        if (!box) g1 = p1grid(L.ntx);
-        const int p1smem = g_p1_occ == 2 ? P1_SMEM_OCC2 : P1_SMEM;
+        // box: blocks of P1_WARPS terms x one column tile; Gaussian: blocks
+        // of one term x one stripe (term fastest, then stripe, y-chunk)
+        const dim3 gbox(L.ntx, (n + P1_WARPS - 1) / P1_WARPS, B);
+        auto p1grid = [&](int nst_run) { return dim3(nst_run * L.nyc * n, 1, B); };
+        const int p1smem = g_p1_occ == 2 ? P1_SMEM_OCC2 : P1_SMEM_GAUSS;
         if (strip_p1 && bi == 0) {
             // strip s on alternating streams, after its copy: transpose (+
             // range check), then pass 1; joined before the chain
@@ -2984,30 +2554,30 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 cudaStream_t ps = aux_stream(2 + (int)(s & 1));
                 cudaStreamWaitEvent(ps, e_ready, 0);
                 cudaStreamWaitEvent(ps, ev_strip[s], 0);
-                p1.tile0 = sb[s];
-                p1.ntx_run = sb[s + 1] - sb[s];
+                p1.st0 = sb[s];
+                p1.nst_run = sb[s + 1] - sb[s];
                 {
-                    dim3 tg(p1.ntx_run, (H + TILE - 1) / TILE, B);
+                    const int t0 = sb[s] * P1_WARPS, t1 = std::min(L.ntx, sb[s + 1] * P1_WARPS);
+                    dim3 tg(t1 - t0, (H + TILE - 1) / TILE, B);
                     Prof pr(KK_TRANSPOSE, ps);
-                    k_transpose<<<tg, 256, 0, ps>>>(f, fT, fY, H, W, -1e-9, terms->T + 1e-9, rc_counters, p1.tile0);
+                    k_transpose<<<tg, 256, 0, ps>>>(f, fT, fY, H, W, -1e-9, terms->T + 1e-9, rc_counters, t0);
                 }
-                dim3 gs = p1grid(p1.ntx_run);
                 {
                     Prof pr(KK_PASS1, ps);
-                    launch_pass1(fold, p1_mode(L, p1), gs, p1smem, ps, p1);
+                    launch_pass1(fold, p1_mode(L, p1), p1grid(p1.nst_run), p1smem, ps, p1);
                 }
                 cudaEvent_t e = event_get();
                 cudaEventRecord(e, ps);
                 cudaStreamWaitEvent(st, e, 0);
             }
-            p1.tile0 = 0;
-            p1.ntx_run = L.ntx;
+            p1.st0 = 0;
+            p1.nst_run = L.nst;
         } else {
             Prof pr(KK_PASS1, st);
             if (box)
-                k_pass1_box<G1, R_ANCHOR><<<g1, P1_WARPS * 32, P1_SMEM, st>>>(p1, sp->radius);
+                k_pass1_box<G1, R_ANCHOR><<<gbox, P1_WARPS * 32, P1_SMEM, st>>>(p1, sp->radius);
             else
-                launch_pass1(fold, p1_mode(L, p1), g1, p1smem, st, p1);
+                launch_pass1(fold, p1_mode(L, p1), p1grid(L.nst), p1smem, st, p1);
         }
         if ((rc = check_cuda("pass1"))) return rc;
         if (s2 != st) {  // hand the batch to the second stream
@@ -3024,7 +2594,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             ca.Ex = L.Ex;
             ca.ne = L.ne;
             ca.edge_all = L.edge_all;
-            ca.ntx = L.ntx;
+            ca.nst = L.nun;
             ca.k = kc;
             ca.nplanes = n * 4;
             ca.n = n;
@@ -3048,19 +2618,15 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.H = H;
         p2.W = W;
         p2.ntx = L.ntx;
+        p2.nst = L.nun;
+        p2.unit_cols = L.unit * TILE;
         p2.k = kc;
         p2.t = td;
-        // pass-2 variant: automatic = the block-summed register variant (6),
-        // measured fastest on configs 1-4 against the per-group register (0)
-        // and cp.async G=4 (4) variants
-        int p2var = g_pass2_tma;
-        if (!box && p2var == 3) p2var = 6;
-        const int npart = (!box && p2var == 6) ? (((n + G2 - 1) / G2 + P2R_GR - 1) / P2R_GR) : -1;
-        const int g2run = (!box && p2var == 4) ? 4 : G2;  // terms per pass-2 thread this launch
-        // (p2var 5: cp.async staging with 2 terms/thread)
-        p2.ngroups = (n + g2run - 1) / g2run;
-        for (int m = 0; m < TILE; ++m)
-            for (int q = 0; q < 4; ++q) p2.Hm[m][q] = box ? 0.f : (float)Hm[m][q];
+        // pass 2: the block-summed variant (k_pass2_gr) for the Gaussian
+        const int npart = box ? -1 : (((n + G2 - 1) / G2 + P2R_GR - 1) / P2R_GR);
+        p2.ngroups = (n + G2 - 1) / G2;
+        for (int m = 0; m < STRIPE; ++m)
+            for (int q = 0; q < 4; ++q) p2.Hm[m][q] = (box || m >= L.unit * TILE) ? 0.f : (float)Hm[m][q];
         {
             const double g = sp->g1 * sp->g2;
             p2.wscale = box ? 1.f : (float)(fold ? g * g * g * g : g * g);
@@ -3072,7 +2638,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.order = g_p2_order;
         // x-chunking of pass-2 rows (p2_chunk_plan)
         const int nrb = (H + P2_THREADS - 1) / P2_THREADS;
-        const P2Plan pp = p2_chunk_plan(L, sp, p2.ngroups, npart, g2run, p2var, hpipe);
+        const P2Plan pp = p2_chunk_plan(L, sp, p2.ngroups, npart, hpipe);
         int nchunk = pp.nchunk;
         p2.warm_tiles = pp.warm_tiles;
         p2.tiles_per_chunk = pp.tiles_per_chunk;
@@ -3112,25 +2678,12 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 Prof pr(KK_PASS2, q);
                 if (box)
                     k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, q>>>(p2, sp->radius);
-                else if (p2var == 6)
-                {
-                    if (p2.xlpt)
-                        k_pass2_gr<G2, true><<<dim3(nrun * (P2_THREADS / 32) * nchunk * npart, 1, B), 32 * P2R_GR,
-                                               P2R_SMEM, q>>>(p2);
-                    else
-                        k_pass2_gr<G2, false><<<dim3(nrun * (P2_THREADS / 32) * nchunk, npart, B), 32 * P2R_GR,
-                                                P2R_SMEM, q>>>(p2);
-                }
-                else if (p2var == 4)
-                    k_pass2_async<4><<<g2, P2_THREADS, p2a_smem_bytes<4>(), q>>>(p2);
-                else if (p2var == 5)
-                    k_pass2_async<2><<<g2, P2_THREADS, p2a_smem_bytes<2>(), q>>>(p2);
-                else if ((W % TILE) == 0 && p2var == 1)
-                    k_pass2_tma<G2, 3><<<g2, P2T_THREADS, p2t_smem_bytes<G2>(), q>>>(p2);
-                else if ((W % TILE) == 0 && p2var == 2)
-                    k_pass2_tma<G2, 2><<<g2, P2T_THREADS, p2t_smem_bytes<G2>(), q>>>(p2);
+                else if (p2.xlpt)
+                    k_pass2_gr<G2, true><<<dim3(nrun * (P2_THREADS / 32) * nchunk * npart, 1, B), 32 * P2R_GR,
+                                           P2R_SMEM, q>>>(p2);
                 else
-                    k_pass2_gauss<G2><<<g2, P2_THREADS, 0, q>>>(p2);
+                    k_pass2_gr<G2, false><<<dim3(nrun * (P2_THREADS / 32) * nchunk, npart, B), 32 * P2R_GR,
+                                            P2R_SMEM, q>>>(p2);
             }
             int e;
             if ((e = check_cuda("pass2"))) return e;
@@ -3220,17 +2773,11 @@ int tbf_set_option(int32_t option, int64_t value) {
         case TBF_OPT_P2_CHUNKS:
             g_p2_chunks = (int)std::max<int64_t>(0, value);
             return TBF_OK;
-        case TBF_OPT_PASS2_TMA:
-            g_pass2_tma = (int)std::max<int64_t>(0, std::min<int64_t>(6, value));
-            return TBF_OK;
         case TBF_OPT_HOST_STRIPS:
             g_host_strips = (int)std::max<int64_t>(0, std::min<int64_t>(64, value));
             return TBF_OK;
         case TBF_OPT_HOST_BANDS:
             g_host_bands = (int)std::max<int64_t>(0, std::min<int64_t>(64, value));
-            return TBF_OK;
-        case TBF_OPT_P1_ORDER:
-            g_p1_order = (int)std::max<int64_t>(-1, std::min<int64_t>(2, value));
             return TBF_OK;
         case TBF_OPT_P2_ORDER:
             g_p2_order = (int)std::max<int64_t>(0, std::min<int64_t>(3, value));
@@ -3311,12 +2858,9 @@ int tbf_layout_info(int32_t B, int32_t H, int32_t W, const tbf_spatial* sp, int3
     if (rc) return rc;
     const bool box = sp->kind == TBF_SPATIAL_BOX;
     const int n = std::min(L.tb, term_end - term_begin);  // first batch
-    int p2var = g_pass2_tma;
-    if (!box && p2var == 3) p2var = 6;
-    const int npart = (!box && p2var == 6) ? (((n + G2 - 1) / G2 + P2R_GR - 1) / P2R_GR) : -1;
-    const int g2run = (!box && p2var == 4) ? 4 : G2;
+    const int npart = box ? -1 : (((n + G2 - 1) / G2 + P2R_GR - 1) / P2R_GR);
     const bool hpipe = host_entry && !box && L.nslot == 1;
-    const P2Plan pp = p2_chunk_plan(L, sp, (n + g2run - 1) / g2run, npart, g2run, p2var, hpipe);
+    const P2Plan pp = p2_chunk_plan(L, sp, (n + G2 - 1) / G2, npart, hpipe);
     const int32_t v[TBF_LAYOUT_INFO_N] = {L.nb, L.tb, L.nyc, L.ych_lpt ? 1 : 0,
                                           L.nyc > 1 ? L.ychb[1] : H, L.nyc > 2 ? L.ychb[2] : H, L.ych_rows,
                                           pp.nchunk, pp.xlpt, pp.xlpt ? pp.xb1 : std::min(L.ntx, pp.tiles_per_chunk),

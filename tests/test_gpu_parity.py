@@ -469,23 +469,23 @@ def test_gauss_large_sigma_s(tb, orc, h, w, s, sr):
 
 
 def test_options_match_default(tb):
-    """The optional pass-2 TMA variants and the two-stream pipeline compute the
-    same filter (up to fp32 reassociation)."""
+    """The two-stream pipeline, forced pass-2 x-chunks and pass-1 y-chunks,
+    the unfolded y gain and the pass-2 block orders compute the same filter
+    (up to fp32 reassociation and warm-up truncation)."""
     from paper_1105_4204_b200 import _native, workloads
 
     lib = _native.load()
-    DEFAULTS = {_native.TBF_OPT_PASS2_TMA: 3, _native.TBF_OPT_PIPELINE: 0, _native.TBF_OPT_P2_CHUNKS: 0,
-                _native.TBF_OPT_P1_FOLD: 1, _native.TBF_OPT_P1_ORDER: -1, _native.TBF_OPT_P2_ORDER: 0}
+    DEFAULTS = {_native.TBF_OPT_PIPELINE: 0, _native.TBF_OPT_P2_CHUNKS: 0, _native.TBF_OPT_P1_YCHUNKS: 0,
+                _native.TBF_OPT_P1_FOLD: 1, _native.TBF_OPT_P2_ORDER: 0}
     cfg = workloads.CONFIGS[2]
     f = torch.from_numpy(workloads.frame(cfg, 0)[:512, :768].copy()).cuda()
     k = tb.make_trig_kernel(cfg.sigma_r)
     spec = tb.SpatialSpec.gaussian_recursive(cfg.sigma_s)
     base = tb.TrigFilter(tuple(f.shape), spec, k)(f)
     try:
-        for opts in ({_native.TBF_OPT_PASS2_TMA: 1}, {_native.TBF_OPT_PASS2_TMA: 2}, {_native.TBF_OPT_PASS2_TMA: 0}, {_native.TBF_OPT_PASS2_TMA: 4},
-                     {_native.TBF_OPT_PIPELINE: 1}, {_native.TBF_OPT_P2_CHUNKS: 1},
-                     {_native.TBF_OPT_PASS2_TMA: 5}, {_native.TBF_OPT_P1_FOLD: 0},
-                     {_native.TBF_OPT_P1_ORDER: 1}, {_native.TBF_OPT_P1_ORDER: 2},
+        for opts in ({_native.TBF_OPT_PIPELINE: 1}, {_native.TBF_OPT_P2_CHUNKS: 1},
+                     {_native.TBF_OPT_P2_CHUNKS: 5}, {_native.TBF_OPT_P1_YCHUNKS: 3},
+                     {_native.TBF_OPT_P1_FOLD: 0},
                      {_native.TBF_OPT_P2_ORDER: 1}, {_native.TBF_OPT_P2_ORDER: 3}):
             for o, v in opts.items():
                 lib.tbf_set_option(o, v)
