@@ -323,21 +323,19 @@ def main():
     if mode == "terms":
         plan = tb.TrigFilter(tuple(f.shape), spec, kernel, term_range=(t0, t1)) if t1 > t0 else None
         fin = plan if plan is not None else tb.TrigFilter(tuple(f.shape), spec, kernel)
-        num = torch.zeros_like(f)
-        den = torch.zeros_like(f)
+        numden = torch.zeros((2, *f.shape), dtype=torch.float32, device=dev)
+        num, den = numden[0], numden[1]
         out = torch.empty_like(f)
 
-        def step():
-            fin.range_check(f)
+        def step(src=f):
+            fin.range_check(src)
             if plan is not None:
-                plan.partial(f, num, den, accumulate=False)
+                plan.partial(src, num, den, accumulate=False)
             else:
-                num.zero_()
-                den.zero_()
-            dist.reduce(num, dst=0)
-            dist.reduce(den, dst=0)
+                numden.zero_()
+            dist.reduce(numden, dst=0)  # one NCCL reduce of both planes
             if rank == 0:
-                fin.finalize(num, den, f, out)
+                fin.finalize(num, den, src, out)
         counters_plan = fin
     else:
         plan = tb.TrigFilter(tuple(f.shape), spec, kernel)
@@ -461,25 +459,34 @@ def main():
                 "achieved": round(ach_t, 2), "unit": "TFLOP/s"}
     # ---- e2e through the public API with pinned host buffers ----
     e2e = None
-    if not args.no_e2e and mode != "terms":
+    if not args.no_e2e and mode == "terms":
+        # term-sharded end to end: every rank copies the input from pinned host
+        # memory, filters its terms, the planes are reduced onto rank 0, which
+        # finalizes and copies the output back (timed per step, max over ranks)
         pin_in = torch.from_numpy(host).pin_memory()
+        pin_out = torch.empty(out.shape, dtype=torch.float32, pin_memory=True)
+        d_in = torch.empty_like(f)
         e2e_times = []
-        res = None
         for i in range(args.warmup + args.steps):
+            barrier()
             torch.cuda.synchronize(dev)
             t = time.perf_counter()
-            res = tb.bilateral_trig(pin_in, spec, kernel)  # H2D, filter, D2H (+ range check)
+            d_in.copy_(pin_in, non_blocking=True)
+            step(d_in)
+            if rank == 0:
+                pin_out.copy_(out, non_blocking=True)
+            torch.cuda.synchronize(dev)
             e2e_times.append(time.perf_counter() - t)
-        tt = sum(e2e_times[args.warmup:])
-        if world > 1:
-            x = torch.tensor([tt], dtype=torch.float64, device=dev)
-            dist.all_reduce(x, op=dist.ReduceOp.MAX)
-            tt = float(x.item())
-        e2e = {"value": px_job * args.steps / tt / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": int(host.nbytes), "d2h_bytes_per_step": int(res.numel() * 4)}
-        del pin_in
-
-    cpu = None
+        tt = torch.tensor([sum(e2e_times[args.warmup:])], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": px_job * args.steps / float(tt.item()) / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": int(host.nbytes), "d2h_bytes_per_step": int(out.numel() * 4),
+               "path": "pinned H2D on every rank, partial, NCCL reduce, finalize and D2H on rank 0"}
+        bad_e, _ = counters_plan.read_counters()
+        if bad_e:
+            raise SystemExit(f"range violations in benchmark input: {bad_e}")
+        del pin_in, pin_out, d_in
+    elif not args.no_e2e:    cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             v, desc, kind, cores = reference_sample(args.config, args.cpu_budget, os.cpu_count() or 1,
@@ -508,6 +515,7 @@ def main():
                        "sigma_s": cfg.sigma_s, "sigma_r": cfg.sigma_r, "T": cfg.T,
                        "N": kernel.N, "terms": pairs.count, "spatial_passes": pairs.spatial_passes,
                        "spatial": "gauss-recursive", "parallelism": f"{mode}x{world}",
+                       "terms_per_batch": int(getattr(counters_plan, "batch_terms", 0)) or (t1 - t0),
                        "l2": f"flushed before each timed step ({args.flush_mb} MiB write, outside the step events)"},
             "roofline": roofline,
             "pipeline_roofline": pipeline,

@@ -68,13 +68,14 @@ class ShardInfo:
     stop: int
 
 
-def reduce_numden(num, den, dst: int = 0, group=None) -> None:
-    """Sum the partial num/den planes onto `dst` (NCCL reduce over NVLink when
-    the process group is NCCL; gloo on CPU tensors in the tests)."""
+def reduce_numden(numden, dst: int = 0, group=None) -> None:
+    """Sum the stacked partial [num, den] planes onto `dst` in one collective
+    (NCCL reduce over NVLink/NVSwitch when the process group is NCCL; gloo on
+    CPU tensors in the tests).  One call moves both planes: half the launches
+    and protocol rounds of two separate reduces."""
     import torch.distributed as dist
 
-    dist.reduce(num, dst=dst, op=dist.ReduceOp.SUM, group=group)
-    dist.reduce(den, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    dist.reduce(numden, dst=dst, op=dist.ReduceOp.SUM, group=group)
 
 
 def bilateral_trig_term_sharded(f, spatial, kernel, *, partial_fn=None, finalize_fn=None,
@@ -95,8 +96,8 @@ def bilateral_trig_term_sharded(f, spatial, kernel, *, partial_fn=None, finalize
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     pairs = term_pairs(kernel)
     t0, t1 = term_range(pairs.count, pairs.has_zero, world, rank)
-    num = torch.zeros_like(f)
-    den = torch.zeros_like(f)
+    numden = torch.zeros((2, *f.shape), dtype=f.dtype, device=f.device)
+    num, den = numden[0], numden[1]
     plan_for_checks = None
     if partial_fn is None or finalize_fn is None:
         from .engines import TrigFilter
@@ -116,7 +117,7 @@ def bilateral_trig_term_sharded(f, spatial, kernel, *, partial_fn=None, finalize
 
     if t1 > t0:
         partial_fn(f, num, den, t0, t1)
-    reduce_numden(num, den, dst=0, group=group)
+    reduce_numden(numden, dst=0, group=group)
     if rank != 0:
         return None
     out = torch.empty_like(f)
@@ -134,12 +135,15 @@ def bilateral_trig_term_sharded(f, spatial, kernel, *, partial_fn=None, finalize
     return out
 
 
-def bilateral_trig_frame_sharded(frames, spatial, kernel, *, gather: bool = False, group=None):
+def bilateral_trig_frame_sharded(frames, spatial, kernel, *, gather: bool = False, group=None,
+                                 filter_fn=None):
     """Frame batches split across ranks with no collective (SURVEY 8(e),
     config 4): rank r filters frames frame_range(B, world, r) of ``frames``
     ([B, H, W], host or device; every rank passes the same batch).  Returns
     this rank's filtered frames, or with ``gather=True`` the whole batch on
-    every rank (all_gather of equal-size shards, padded)."""
+    every rank (all_gather of equal-size shards, padded).  ``filter_fn(frames)``
+    defaults to the device ``bilateral_trig``; the gloo tests inject a CPU
+    implementation (the gather then runs on CPU tensors)."""
     import torch
     import torch.distributed as dist
 
@@ -148,10 +152,14 @@ def bilateral_trig_frame_sharded(frames, spatial, kernel, *, gather: bool = Fals
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     B = int(frames.shape[0])
     f0, f1 = frame_range(B, world, rank)
-    mine = bilateral_trig(frames[f0:f1].contiguous(), spatial, kernel) if f1 > f0 else frames[0:0]
+    if filter_fn is None:
+        def filter_fn(x):
+            return bilateral_trig(x, spatial, kernel)
+    mine = filter_fn(frames[f0:f1].contiguous()) if f1 > f0 else frames[0:0]
     if not gather:
         return mine
-    dev = torch.device("cuda", torch.cuda.current_device())
+    dev = (torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl"
+           else torch.device("cpu"))
     per = max(frame_range(B, world, r)[1] - frame_range(B, world, r)[0] for r in range(world))
     buf = torch.zeros((per, *frames.shape[1:]), dtype=torch.float32, device=dev)
     if f1 > f0:

@@ -151,20 +151,25 @@ class TrigFilter:
         budget = WORKSPACE_FRACTION * free
         if self.workspace_bytes(0) <= budget:
             return 0  # library default: a few pipelined batches
-        # workspace is affine in the batch size (the library rounds batches to
-        # whole pass-2 groups of 4 terms): fit the slope on multiples of 8
+        # workspace is affine in the batch size: fit the slope on multiples of
+        # 8, then take the largest multiple of 2 (whole pass-2 thread groups)
+        # that fits, and spread the terms evenly over that many batches (each
+        # batch re-reads the input and folds its partials: fewer is cheaper)
         w8, w16 = self.workspace_bytes(8), self.workspace_bytes(16)
         per = max(1, (w16 - w8) // 8)
         base = w8 - 8 * per
-        tb = int((budget - base) // per) // 8 * 8
-        if tb < 8:
-            tb = 4 if self.workspace_bytes(4) <= budget else 0
+        tb = int((budget - base) // per) // 2 * 2
+        if tb < 2:
+            tb = 2 if self.workspace_bytes(2) <= budget else 0
         if tb < 1:
             raise ParameterError(
                 f"image too large for device memory: needs {w8 / 2**30:.1f} GiB for 8 terms"
             )
-        while tb > 4 and self.workspace_bytes(tb) > budget:
-            tb -= 4
+        while tb > 2 and self.workspace_bytes(tb) > budget:
+            tb -= 2
+        if tb < n:
+            nb = -(-n // tb)
+            tb = min(tb, -(-n // nb) + (-(-n // nb)) % 2)  # even split, rounded up to even
         return min(tb, n)
 
     # -- calls ------------------------------------------------------------
@@ -643,10 +648,20 @@ def _bilateral_trig_streamed_locked(t, spatial, kernel, diagnostics, sub, edges)
 
 
 def bilateral_color(img: Image, engine, workers: int = 1) -> Image:
-    """Apply a single-channel engine to each channel (engines.py:354-369)."""
+    """Apply a single-channel engine to each channel (engines.py:354-369):
+    channels independently, on a thread pool when workers > 1 (the device
+    engine is thread-safe: each plan serialises its calls), reassembled in
+    channel order."""
     if img.channels != 3:
         raise DimensionError(f"expected a 3-channel image, got {img.channels}")
-    results = [engine(img.channel(c)) for c in range(3)]
+    chans = [img.channel(c) for c in range(3)]
+    if workers > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=workers) as pool:
+            results = list(pool.map(engine, chans))
+    else:
+        results = [engine(ch) for ch in chans]
     stacked = np.stack([r.plane(0) for r in results])
     return Image(img.width, img.height, 3, stacked)
 

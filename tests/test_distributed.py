@@ -103,3 +103,57 @@ def test_term_sharded_reduce_gloo_world2():
     errs = [r for r in res if isinstance(r, float)]
     assert len(errs) == 1 and errs[0] < 1e-9, res
     assert all(r is None or isinstance(r, float) for r in res), res
+
+
+def _frame_worker(rank, world, port, q, gather):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import trigbf_oracle as orc
+        from paper_1105_4204_b200 import SpatialSpec, make_trig_kernel
+        from paper_1105_4204_b200.distributed import bilateral_trig_frame_sharded, frame_range
+
+        B = 5  # odd: ranks get 3 and 2 frames, the gather pads the short shard
+        frames = torch.from_numpy(np.random.default_rng(11).uniform(0, 255, (B, 12, 10)).astype(np.float32))
+        k = make_trig_kernel(40.0)
+        okern = orc.make_trig_kernel(40.0)
+        calls = []
+
+        def filter_fn(x):
+            calls.append(int(x.shape[0]))
+            out = [orc.bilateral_trig(x[i].double().numpy(), "gauss-recursive", 2.0, okern)[0] for i in range(x.shape[0])]
+            return torch.from_numpy(np.stack(out).astype(np.float32))
+
+        got = bilateral_trig_frame_sharded(frames, SpatialSpec.gaussian_recursive(2.0), k, gather=gather,
+                                           filter_fn=filter_fn)
+        ref = np.stack([orc.bilateral_trig(frames[i].double().numpy(), "gauss-recursive", 2.0, okern)[0]
+                        for i in range(B)])
+        f0, f1 = frame_range(B, world, rank)
+        want = ref if gather else ref[f0:f1]
+        q.put((rank, calls, tuple(got.shape), float(np.max(np.abs(got.double().numpy() - want)))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("gather", [False, True])
+def test_frame_sharded_gloo_world2(gather):
+    """Config 4's frame split on two ranks (gloo, CPU compute injected): each
+    rank filters only its own contiguous frames (no collective on the data
+    path); with gather=True every rank ends with the whole batch in order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_frame_worker, args=(r, 2, port, q, gather)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    (r0, c0, s0, e0), (r1, c1, s1, e1) = res
+    assert c0 == [3] and c1 == [2]  # frame_range(5, 2, r): 3 + 2 frames, one call each
+    if gather:
+        assert s0 == s1 == (5, 12, 10)
+    else:
+        assert s0 == (3, 12, 10) and s1 == (2, 12, 10)
+    assert e0 < 1e-4 and e1 < 1e-4

@@ -155,3 +155,106 @@ def test_criterion_9_guard_silent(tb):
         tb.bilateral_trig(_dev(f), tb.SpatialSpec.box(2), tb.make_trig_kernel(170.0, 255.0, degree=n_deg),
                           diagnostics=diag)
         assert diag.guarded_pixels == 0
+
+
+# ---------------------------------------------------------------------------
+# criterion 9 property suites on the device smoothers (test_acceptance.py:
+# 183-217, same seeds and case counts).  Two device forms of smooth_plane:
+#  * the fp64 plugin twins (tbf_recursive_smooth_f64 / tbf_box_pass_f64)
+#    composed as spatial.py:157-172 does, held to the reference's bounds;
+#  * the fp32 pipeline itself at degree 0: then the only term is the zero
+#    frequency with weight 1, so bilateral_trig returns exactly the device's
+#    fp32 separable smoother of f (num = F[f], den = 1), held to fp32 bounds.
+# The reference's gaussian_fir spec has no O(1) device smoother (FIR is out of
+# scope for bilateral_trig); its draw is kept and run as a recursive sigma.
+# ---------------------------------------------------------------------------
+
+def _smooth_f64(spec_kind, param, plane):
+    """smooth_plane (spatial.py:157-172) from the device fp64 plugin twins."""
+    from paper_1105_4204_b200 import _native
+    from paper_1105_4204_b200.spatial import recursive_coeffs
+
+    lib = _native.load()
+
+    def rec_axis0(a):
+        h, w = a.shape
+        out = torch.empty_like(a)
+        scratch = torch.empty((3 * h + 8) * w, dtype=torch.float64, device="cuda")
+        _native.check(lib.tbf_recursive_smooth_f64(a.data_ptr(), out.data_ptr(), h, w,
+                                                   *[float(v) for v in recursive_coeffs(param)], h - 1,
+                                                   scratch.data_ptr(), None))
+        return out
+
+    def box_last(a):
+        out = torch.empty_like(a)
+        _native.check(lib.tbf_box_pass_f64(a.data_ptr(), out.data_ptr(), a.shape[0], a.shape[1], int(param), None))
+        return out
+
+    a = torch.from_numpy(np.ascontiguousarray(plane, dtype=np.float64)).cuda()
+    if spec_kind == "box":
+        out = box_last(a)
+        out = box_last(out.t().contiguous()).t().contiguous()
+    else:
+        out = rec_axis0(a)
+        out = rec_axis0(out.t().contiguous()).t().contiguous()
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def _smooth_f32(tb, spec_kind, param, plane, T=255.0):
+    """The fp32 pipeline's own smoother: bilateral_trig at degree 0."""
+    spec = tb.SpatialSpec.box(int(param)) if spec_kind == "box" else tb.SpatialSpec.gaussian_recursive(float(param))
+    k = tb.make_trig_kernel(30.0, T, degree=0)
+    out = tb.bilateral_trig(_dev(plane), spec, k)
+    return out.double().cpu().numpy()
+
+
+def test_criterion_9_unit_dc_gain(tb):
+    # test_acceptance.py:183-200: 120 cases, seed 106
+    rng = np.random.default_rng(106)
+    specs = [("box", int(rng.integers(0, 12))) for _ in range(4)]
+    specs += [("gauss-recursive", float(rng.uniform(0.5, 8.0))),   # the reference's gaussian_fir draw
+              ("gauss-recursive", float(rng.uniform(0.5, 30.0)))]
+    cases = 0
+    worst64 = worst32 = 0.0
+    for kind, param in specs:
+        for _ in range(20):
+            w, h = int(rng.integers(2, 24)), int(rng.integers(2, 24))
+            level = float(rng.uniform(0.0, 255.0))
+            plane = np.full((h, w), level)
+            e64 = float(np.max(np.abs(_smooth_f64(kind, param, plane) - level)))
+            e32 = float(np.max(np.abs(_smooth_f32(tb, kind, param, plane) - level)))
+            assert e64 < 1e-6, (kind, param, h, w, e64)
+            assert e32 < 1e-3, (kind, param, h, w, e32)
+            worst64, worst32 = max(worst64, e64), max(worst32, e32)
+            cases += 1
+    assert cases == 120
+    print(f"criterion 9 unit DC gain: 120 cases, worst fp64 {worst64:.2g}, fp32 pipeline {worst32:.2g}")
+
+
+def test_criterion_9_linearity(tb):
+    # test_acceptance.py:202-217: 120 cases, seed 107.  The fp32 pipeline only
+    # takes samples in [0, T]: it checks s(a f + b g) = a s(f) + b s(g) with the
+    # same draws folded to a, b in [0, 1] and T = 1000
+    rng = np.random.default_rng(107)
+    specs = [("box", 2), ("gauss-recursive", 1.5), ("gauss-recursive", 2.5)]  # fir 1.5 -> recursive 1.5
+    worst64 = worst32 = 0.0
+    cases = 0
+    for kind, param in specs:
+        for _ in range(40):
+            f = rng.uniform(0, 255, (10, 11))
+            g = rng.uniform(0, 255, (10, 11))
+            a, b = rng.uniform(-2, 2, 2)
+            lhs = _smooth_f64(kind, param, a * f + b * g)
+            rhs = a * _smooth_f64(kind, param, f) + b * _smooth_f64(kind, param, g)
+            e64 = float(np.max(np.abs(lhs - rhs)))
+            assert e64 < 1e-9, (kind, param, e64)
+            a32, b32 = abs(a) / 2.0, abs(b) / 2.0
+            lhs = _smooth_f32(tb, kind, param, a32 * f + b32 * g, T=1000.0)
+            rhs = a32 * _smooth_f32(tb, kind, param, f, T=1000.0) + b32 * _smooth_f32(tb, kind, param, g, T=1000.0)
+            e32 = float(np.max(np.abs(lhs - rhs)))
+            assert e32 < 2e-3, (kind, param, e32)
+            worst64, worst32 = max(worst64, e64), max(worst32, e32)
+            cases += 1
+    assert cases == 120
+    print(f"criterion 9 linearity: 120 cases, worst fp64 {worst64:.2g}, fp32 pipeline {worst32:.2g}")
