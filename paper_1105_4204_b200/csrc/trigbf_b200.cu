@@ -1935,8 +1935,19 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
             const int rows = ((H + nyc - 1) / nyc + TILE - 1) / TILE * TILE;
             const int n = (H + rows - 1) / rows;
             if (n != nyc) continue;  // same split as a smaller count
-            if (nyc > 1 && rows < L->ywarm) break;
-            const double len = nyc == 1 ? (double)H + 2.0 * L->Ey : (double)rows + 2.0 * L->ywarm;
+            // chunks shorter than the warm-up only while the launch stays
+            // under one wave (long decays on small images: parallelism
+            // matters more than the warm-up rows)
+            if (nyc > 1 && rows < L->ywarm && blocks1 * nyc > slots) break;
+            // rows the longest chunk sweeps: its output rows plus warm-ups,
+            // clamped to the mirror extension [-Ey, H + Ey)
+            double len = 0.0;
+            for (int c = 0; c < n; ++c) {
+                const int R0 = c * rows, R1 = std::min(H, R0 + rows);
+                const int A0 = nyc == 1 ? -L->Ey : std::max(R0 - L->ywarm, -L->Ey);
+                const int A1 = nyc == 1 ? H + L->Ey : std::min(R1 + L->ywarm, H + L->Ey);
+                len = std::max(len, (double)(A1 - A0));
+            }
             const double waves = blocks1 * nyc / slots;
             const double cost = len * (waves <= 1.0 ? 1.0 : waves + 0.9);
             if (best < 0 || cost < best * 0.98) {  // prefer fewer chunks on near ties

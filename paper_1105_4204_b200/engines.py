@@ -109,8 +109,10 @@ class TrigFilter:
         if len(shape) != 3 or min(shape) < 1:
             raise DimensionError(f"expected [B, H, W] with positive sizes, got {tuple(shape)}")
         self.B, self.H, self.W = (int(v) for v in shape)
-        self.device = (torch.device(device) if device is not None
-                       else torch.device("cuda", torch.cuda.current_device()))
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        if dev.type != "cuda":
+            raise ParameterError(f"plans live on a CUDA device, got {dev}")
+        self.device = torch.device("cuda", torch.cuda.current_device() if dev.index is None else dev.index)
         self.spatial = spatial
         self.kernel = kernel
         self.sp = spatial_struct(spatial)
@@ -347,7 +349,9 @@ def get_plan(shape, spatial: SpatialSpec, kernel: TrigKernel, device=None) -> Tr
     """Cached plan (workspace reuse across calls with the same configuration)."""
     torch = _torch()
     _require_cuda()
-    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    dev = torch.device("cuda" if device is None else device)
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
     key = (str(dev), tuple(shape), spatial, kernel.N, kernel.omega, kernel.T)
     with _PLANS_LOCK:
         plan = _PLANS.get(key)

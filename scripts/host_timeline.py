@@ -27,5 +27,12 @@ for rep in range(3):
     print(f"call {rep}: wall {wall:.3f} ms, {n} records")
     if rep == 2:
         for i in range(n):
-            print(f"  {lib.tbf_kernel_name(kd[i]).decode():12s} start {st[i]:7.3f}  dur {du[i]:7.3f}  end {st[i] + du[i]:7.3f}")
+            print(f"  {lib.tbf_kernel_name(kd[i]).decode():12s} start {st[i]:9.3f}  dur {du[i]:8.3f}  end {st[i] + du[i]:9.3f}")
+        span = {}
+        for i in range(n):
+            nm = lib.tbf_kernel_name(kd[i]).decode()
+            a, b, d = span.get(nm, (1e30, -1e30, 0.0))
+            span[nm] = (min(a, st[i]), max(b, st[i] + du[i]), d + du[i])
+        for nm, (a, b, d) in span.items():
+            print(f"  summary {nm:12s} first start {a:9.3f}  last end {b:9.3f}  busy {d:9.3f} ms")
 lib.tbf_profile_enable(0)
