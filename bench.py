@@ -414,7 +414,7 @@ def main():
     round_trip = 16 * nz_shard + 4 * z_shard  # one write (pass1) or one read (pass2) of the planes
     alg_kernel = {"pass1": (4 + round_trip) * px_rank, "pass2": (4 + round_trip) * px_rank,
                   "reduce": 8 * px_rank, "transpose": 12 * px_rank, "range_check": 4 * px_rank,
-                  "finalize": 12 * px_rank, "chain": 0}
+                  "finalize": 12 * px_rank, "edge": 0}
     roofline = None
     issue = None
     if dom is not None:

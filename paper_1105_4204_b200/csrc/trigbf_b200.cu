@@ -88,6 +88,7 @@ __host__ __device__ __forceinline__ size_t xm_plane(int B, int W, int H) {
     return (size_t)B * ((H + FL_RB - 1) / FL_RB) * FL_RB * W;
 }
 constexpr int TBF_MAX_YCH = 16;      // most y-chunks per pass-1 column
+constexpr int P1_MAX_LAUNCHES = 64;  // pass-1 launches per batch (host strips), one dispatch ticket each
 constexpr int P1_BLOCKS_PER_SM = 3;  // smem-limited residency of pass-1 blocks (4 warps, 67.6 KB)
 constexpr int BUF_LD = TILE + 1;  // padded leading dimension of the smem tile
 constexpr int STRIPE = P1_WARPS * TILE;  // columns per pass-1 block (x carries are chained per stripe)
@@ -116,7 +117,7 @@ enum KernelKind {
     KK_TRANSPOSE = 0, KK_RANGE, KK_PASS1, KK_CHAIN, KK_PASS2, KK_REDUCE, KK_FINALIZE, KK_H2D, KK_D2H,
     KK_COUNT
 };
-const char* const kKernelNames[KK_COUNT] = {"transpose", "range_check", "pass1", "chain",
+const char* const kKernelNames[KK_COUNT] = {"transpose", "range_check", "pass1", "edge",
                                             "pass2", "reduce", "finalize", "h2d", "d2h"};
 
 struct ProfRec {
@@ -219,6 +220,31 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) {
 __device__ __forceinline__ float ldg_pinned(const float* p) {
     float v;
     asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Flag hand-off between blocks (the pass-1 x chain): release store by the
+// producer after its data.
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Consumer side without acquire semantics (an acquire costs an L1
+// invalidation, CCTL.IVALL, per hand-off and the block's warps share f rows
+// in L1): the flag is polled with strong relaxed loads and the data read with
+// strong loads that are only issued once the poll loop has seen the flag, so
+// both are served by L2, where the producer's release made the data visible
+// before the flag.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ float4 ld_relaxed4(const float4* p) {
+    float4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p)
+                 : "memory");
     return v;
 }
 
@@ -443,7 +469,6 @@ struct Pass1Args {
     int Ex, ne, edge_all, ntx;
     int nst;           // stripes of P1_WARPS column tiles (one pass-1 block each, per term)
     int st0, nst_run;  // stripes [st0, st0 + nst_run) in this launch
-    int unit, nun;     // x chain unit in tiles (P1_WARPS: hand-off inside the stripe; 1: none), units
     Casc k;
     TermDev t;
     // Gaussian layouts (float4 = the 4 planes of one term, or the 4 states
@@ -451,22 +476,31 @@ struct Pass1Args {
     float* ckpt;    // float4 [nseg][n][B][W][4 planes]
     float* floc;    // float4 [n][B][W][H]  tile-local forward along x (x-major)
                     //   (box: planar [n*4][B][W][H] y-filtered values)
-    float* lcarry;  // float4 [n][B][nun][H][4 planes] chain-unit end states (zero start)
+    // x chain across stripes (decoupled hand-off, serial per (term, frame,
+    // 32-row segment)): warp 0 of stripe s waits for stripe s-1's flag and
+    // starts from mail slot s; warp 3 publishes its end state into slot s+1
+    float* mail;           // float4 [n][B][nst+1][H][4 planes]; slot 0 unused (zero start at x = 0)
+    int* flags;            // [n][B][nst][nsegH]: 1 once stripe s's slot s+1 rows of segment k are out
+    int nsegH;             // ceil(H / 32)
+    unsigned int* ticket;  // block dispatch counter (stripe-major order, see k_pass1_gauss)
     float* edge;    // float4 [n][B][ne][H] y-filtered values at x-edge columns
 };
 
-struct ChainArgs {
+// Mirrored x-extensions (spatial.py:171 with pad = W-1 truncated to ext_x,
+// _core.pyx:56-96) per (row, term), after pass 1: the forward state S0 at
+// x = 0 (the left extension, which the pass-1 chain started from zero) and
+// the backward start state at x = W-1 (the right extension, in closed form).
+struct EdgeArgs {
     int B, H, W;
-    int Ex, ne, edge_all, nst;  // nst = chain units
+    int Ex, ne, edge_all, nst;  // nst = stripes (mail slot nst = chain end state at x = W)
     Casc k;
-    int nplanes;          // n*4
-    float M[16];          // full-stripe state transfer (column-major: M[k*4+r])
-    float Mlast[16];      // last (possibly partial) stripe
     int n;                // terms in the batch
     const float* edge;    // float4 [n][B][ne][H]
-    float* lcarry;        // in: stripe end states (zero start), out: chained carries (state at stripe start)
+    const float* mail;    // chain end states: slot ntx = forward state at x = W of the zero-start chain
+    float MW[16];         // zero-input state transfer over W samples (column-major)
     float Rx[16];         // right extension: bstate = Rx . s(W) + sum_e bx[e] Y(W-2-e)
     const float4* bx;     // [Ex] (see right_ext_coeffs)
+    float* s0;            // float4 [n][B][H][4 planes] left-extension state S0
     float* bstate;        // float4 [n][B][H][4 planes] backward start state
 };
 
@@ -476,9 +510,6 @@ struct Pass2Args {
     Casc k;
     TermDev t;
     int ngroups;       // ceil(t.n / G2)
-    int nst;           // chain units (carries per row and term)
-    int unit_cols;     // columns per chain unit (32 or STRIPE)
-    float Hm[STRIPE][4];  // homogeneous response of the cascade to a unit state at the unit start
     float wscale;      // g^2: undoes the two pure x sweeps (1 for box)
     int rb0, nrb_run;     // 128-row blocks [rb0, rb0 + nrb_run) in this launch
     int tiles_per_chunk;  // x-chunking of rows (gauss); == ntx for one chunk
@@ -488,8 +519,12 @@ struct Pass2Args {
     // arrays cost registers)
     int xlpt, xb1, xb2, xord;
     int warm_tiles;       // warm-up tiles of a chunk's backward sweep
-    const float* floc;
-    const float* carry;   // chained carries float4 [n][B][nst][H][4] (state at each stripe start)
+    const float* floc;    // forward output of the zero-start chain (exact once corrected)
+    // exact forward = floc + Hx[x] . S0 for x < nHx (the response to the
+    // left-extension state decays below 1e-9 relative beyond nHx)
+    int nHx;
+    const float4* Hx;     // [nHx] zero-input cascade output at x from unit states at x = 0
+    const float* s0;      // float4 [n][B][H][4]
     const float* bstate;  // float4 [n][B][H][4]
     float* part;          // [ngroups*2][B][W][H]
     int order;            // k_pass2_gr block order (TBF_OPT_P2_ORDER)
@@ -555,19 +590,27 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     extern __shared__ float smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
+    __shared__ unsigned int s_ticket;
     // one block = one term x one stripe of P1_WARPS column tiles (warp w =
-    // tile w of the stripe).  Block order: term fastest (the blocks sharing a
-    // stripe's f run together), then stripe, y-chunk slowest (planned chunks
-    // are numbered largest first)
-    int term, stripe_r, chunk;
+    // tile w of the stripe).  Dispatch order from a ticket taken at block
+    // start (not blockIdx: the x chain makes stripe s wait for stripe s-1, so
+    // every block a block waits for must have been dispatched before it).
+    // Stripe slowest, then frame, y-chunk, term fastest: the blocks sharing a
+    // stripe's f run together, and a wave spreads over many independent
+    // chains (the hand-off lag of a wave grows with the stripes of one chain
+    // in it).
+    if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1u);
+    __syncthreads();
+    int term, stripe_r, chunk, b;
     {
-        int idx = blockIdx.x;
-        term = idx % a.t.n;
-        idx /= a.t.n;
-        stripe_r = idx % a.nst_run;
-        chunk = idx / a.nst_run;
+        unsigned int idx = s_ticket;
+        term = (int)(idx % (unsigned)a.t.n);
+        idx /= (unsigned)a.t.n;
+        chunk = (int)(idx % (unsigned)a.nyc);
+        idx /= (unsigned)a.nyc;
+        b = (int)(idx % (unsigned)a.B);
+        stripe_r = (int)(idx / (unsigned)a.B);
     }
-    const int b = blockIdx.z;
     const int H = a.H, W = a.W;
     const int stripe = a.st0 + stripe_r;
     const int tile_x = stripe * P1_WARPS + warp;
@@ -690,10 +733,10 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     const int nrbk = (H + FL_RB - 1) / FL_RB;
     float4* const fl0 = reinterpret_cast<float4*>(a.floc) + ((size_t)term * a.B + b) * nrbk * W * (size_t)FL_RB;
     float4* const ed0 = reinterpret_cast<float4*>(a.edge) + ((size_t)term * a.B + b) * a.ne * (size_t)H;
-    // the chain unit's end state (written by its last warp): float4 [term][b][unit][H][4 planes]
-    const bool handoff = a.unit > 1;  // block-uniform
-    float4* const lc0 = reinterpret_cast<float4*>(a.lcarry) +
-                        (((size_t)term * a.B + b) * a.nun + tile_x / a.unit) * (size_t)H * 4;
+    // x chain across stripes: mail slot s = state at stripe s's start
+    float4* const mail0 = reinterpret_cast<float4*>(a.mail) +
+                          (((size_t)term * a.B + b) * (a.nst + 1) + stripe) * (size_t)H * 4;
+    int* const flag0 = a.flags + (((size_t)term * a.B + b) * a.nst + stripe) * a.nsegH;
     // hand-off slots between the stripe's warps: slot w (warp w -> w+1) holds
     // one float4 per plane and row, after the P1_WARPS tiles
     float4* const hand = reinterpret_cast<float4*>(smem) + (size_t)P1_WARPS * TILE * BUF_LD;
@@ -821,7 +864,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
         const bool rowv = lane < min(len, R1 - i0);
         const bool last_out = i0 == R0;  // segments run bottom to top
         float lv1[4], lv2[4], ly1[4], ly2[4];
-        if (handoff && warp > 0) {
+        if (warp > 0) {
             named_bar_sync(1 + (warp - 1), 64);
             const float4* hs = hand + ((size_t)(warp - 1) * 4) * TILE + lane;
 #pragma unroll
@@ -833,6 +876,25 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                 ly2[p] = c.w;
             }
             if (!last_out) named_bar_arrive(1 + P1_WARPS + (warp - 1), 64);
+        } else if (stripe > 0) {
+            // stripe s-1 hands its end state over: wait for its flag for this
+            // segment (a hand-off never arrives only if the dispatch order
+            // were broken: fail the launch after ~10 s instead of hanging)
+            const int* pf = flag0 - a.nsegH + (i0 >> 5);
+            unsigned int spins = 0;
+            while (ld_relaxed(pf) == 0) {
+                __nanosleep(32);
+                if (++spins == (1u << 27)) __trap();
+            }
+            const float4* mb = mail0 + (size_t)i * 4;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const float4 c = rowv ? ld_relaxed4(mb + p) : f4(0.f, 0.f, 0.f, 0.f);
+                lv1[p] = c.x;
+                lv2[p] = c.y;
+                ly1[p] = c.z;
+                ly2[p] = c.w;
+            }
         } else {
 #pragma unroll
             for (int p = 0; p < 4; ++p) lv1[p] = lv2[p] = ly1[p] = ly2[p] = 0.f;
@@ -879,18 +941,22 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                 }
             }
         }
-        if (handoff && warp < P1_WARPS - 1) {
+        if (warp < P1_WARPS - 1) {
             if (nout > 0) named_bar_sync(1 + P1_WARPS + warp, 64);  // the slot's previous state was read
             float4* hs = hand + ((size_t)warp * 4) * TILE + lane;
 #pragma unroll
             for (int p = 0; p < 4; ++p) hs[p * TILE] = f4(lv1[p], lv2[p], ly1[p], ly2[p]);
             named_bar_arrive(1 + warp, 64);
-        } else if (rowv && (handoff || tlen > 0)) {
-            // the unit's end state (clamped warps past the image edge pass
-            // the state of its last column through unchanged)
-            float4* lc = lc0 + (size_t)i * 4;
+        } else {
+            // the stripe's end state (clamped warps past the image edge pass
+            // the state of its last column through unchanged) to mail slot
+            // s+1 (L2), then the flag: every lane releases its own stores
+            if (rowv) {
+                float4* mb = mail0 + ((size_t)H + i) * 4;
 #pragma unroll
-            for (int p = 0; p < 4; ++p) lc[p] = f4(lv1[p], lv2[p], ly1[p], ly2[p]);
+                for (int p = 0; p < 4; ++p) __stcg(mb + p, f4(lv1[p], lv2[p], ly1[p], ly2[p]));
+            }
+            st_release(flag0 + (i0 >> 5), 1);
         }
         ++nout;
         __syncwarp();
@@ -898,9 +964,11 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
 }
 
 // ---------------------------------------------------------------------------
-// Chain: per (row, term) the x-direction carries of the 4 planes and the
-// mirrored x-extension (spatial.py:171 with pad = W-1 truncated to ext_x,
-// _core.pyx:56-96).
+// Edge: per (row, term) the mirrored x-extensions (spatial.py:171 with pad =
+// W-1 truncated to ext_x, _core.pyx:56-96) from the edge columns pass 1
+// wrote: the left extension's forward state S0 at x = 0 (the pass-1 chain
+// started from zero; pass 2 adds the response to S0) and the backward start
+// state at x = W-1 (right extension in closed form).
 // ---------------------------------------------------------------------------
 
 __device__ __forceinline__ void cstep4(const float4& u, float (&v1)[4], float (&v2)[4],
@@ -912,7 +980,7 @@ __device__ __forceinline__ void cstep4(const float4& u, float (&v1)[4], float (&
     o[3] = cstep(u.w, v1[3], v2[3], y1[3], y2[3], k);
 }
 
-__global__ void __launch_bounds__(128) k_chain(const __grid_constant__ ChainArgs a) {
+__global__ void __launch_bounds__(128) k_edge(const __grid_constant__ EdgeArgs a) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.H) return;
     const int bt = blockIdx.y;  // term * B + b
@@ -939,41 +1007,21 @@ __global__ void __launch_bounds__(128) k_chain(const __grid_constant__ ChainArgs
         for (int q = 0; q < 8; ++q)
             if (xb + q < 0) cstep4(u[q], v1, v2, y1, y2, k, o);
     }
-    // chain along x over the stripes: C_t = state at stripe start; s_{t+1} = M s_t + L_t
-    float M[16], Ml[16];
+    float4* s0 = reinterpret_cast<float4*>(a.s0) + ((size_t)bt * H + i) * 4;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        M[q] = a.M[q];
-        Ml[q] = a.Mlast[q];
-    }
-    float4* lc = reinterpret_cast<float4*>(a.lcarry) + ((size_t)bt * a.nst * H + i) * 4;
-    const size_t tstride = (size_t)H * 4;  // float4 stride between stripes
-    for (int tb = 0; tb < a.nst; tb += 4) {
-        float4 L[4][4];
+    for (int p = 0; p < 4; ++p) s0[p] = f4(v1[p], v2[p], y1[p], y2[p]);
+    // forward state at x = W: the zero-start chain's end state plus the
+    // response to S0 carried over the W samples
+    const float4* cw = reinterpret_cast<const float4*>(a.mail) + (((size_t)bt * (a.nst + 1) + a.nst) * H + i) * 4;
+    float s[4][4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+    for (int p = 0; p < 4; ++p) {
+        const float4 c = cw[p];
+        const float z[4] = {v1[p], v2[p], y1[p], y2[p]};
+        const float cc[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-            for (int p = 0; p < 4; ++p)
-                L[q][p] = tb + q < a.nst ? lc[(size_t)(tb + q) * tstride + p] : f4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int t = tb + q;
-            if (t < a.nst) {
-                const bool last = t == a.nst - 1;
-#pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    lc[(size_t)t * tstride + p] = f4(v1[p], v2[p], y1[p], y2[p]);
-                    const float s0 = v1[p], s1 = v2[p], s2 = y1[p], s3 = y2[p];
-                    float m[16];
-#pragma unroll
-                    for (int r = 0; r < 16; ++r) m[r] = last ? Ml[r] : M[r];
-                    v1[p] = fmaf(m[0], s0, fmaf(m[4], s1, fmaf(m[8], s2, fmaf(m[12], s3, L[q][p].x))));
-                    v2[p] = fmaf(m[1], s0, fmaf(m[5], s1, fmaf(m[9], s2, fmaf(m[13], s3, L[q][p].y))));
-                    y1[p] = fmaf(m[2], s0, fmaf(m[6], s1, fmaf(m[10], s2, fmaf(m[14], s3, L[q][p].z))));
-                    y2[p] = fmaf(m[3], s0, fmaf(m[7], s1, fmaf(m[11], s2, fmaf(m[15], s3, L[q][p].w))));
-                }
-            }
-        }
+        for (int r = 0; r < 4; ++r)
+            s[p][r] = fmaf(a.MW[r], z[0], fmaf(a.MW[4 + r], z[1], fmaf(a.MW[8 + r], z[2], fmaf(a.MW[12 + r], z[3], cc[r]))));
     }
     // right extension (forward over x = W .. W-1+Ex on Y(2(W-1)-x), steady
     // start from its last output, backward back to x = W-1) in closed form:
@@ -981,11 +1029,11 @@ __global__ void __launch_bounds__(128) k_chain(const __grid_constant__ ChainArgs
     float p1[4], p2[4], q1[4], q2[4];
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-        const float s0 = v1[p], s1 = v2[p], s2 = y1[p], s3 = y2[p];
-        p1[p] = fmaf(a.Rx[0], s0, fmaf(a.Rx[4], s1, fmaf(a.Rx[8], s2, a.Rx[12] * s3)));
-        p2[p] = fmaf(a.Rx[1], s0, fmaf(a.Rx[5], s1, fmaf(a.Rx[9], s2, a.Rx[13] * s3)));
-        q1[p] = fmaf(a.Rx[2], s0, fmaf(a.Rx[6], s1, fmaf(a.Rx[10], s2, a.Rx[14] * s3)));
-        q2[p] = fmaf(a.Rx[3], s0, fmaf(a.Rx[7], s1, fmaf(a.Rx[11], s2, a.Rx[15] * s3)));
+        const float s0v = s[p][0], s1 = s[p][1], s2 = s[p][2], s3 = s[p][3];
+        p1[p] = fmaf(a.Rx[0], s0v, fmaf(a.Rx[4], s1, fmaf(a.Rx[8], s2, a.Rx[12] * s3)));
+        p2[p] = fmaf(a.Rx[1], s0v, fmaf(a.Rx[5], s1, fmaf(a.Rx[9], s2, a.Rx[13] * s3)));
+        q1[p] = fmaf(a.Rx[2], s0v, fmaf(a.Rx[6], s1, fmaf(a.Rx[10], s2, a.Rx[14] * s3)));
+        q2[p] = fmaf(a.Rx[3], s0v, fmaf(a.Rx[7], s1, fmaf(a.Rx[11], s2, a.Rx[15] * s3)));
     }
     for (int eb = 0; eb < Ex; eb += 8) {
         float4 u[8], c[8];
@@ -1016,16 +1064,17 @@ __global__ void __launch_bounds__(128) k_chain(const __grid_constant__ ChainArgs
 
 // ---------------------------------------------------------------------------
 // Pass 2 (recursive Gaussian): x-direction backward sweep on the exact forward
-// output (tile-local + H . carry), fused with demodulation + accumulation
-// (engines.py:297-298).  One thread = one row x G terms.
+// output, fused with demodulation + accumulation (engines.py:297-298).  One
+// thread = one row x G terms.  Pass 1 wrote the forward output of a chain
+// that started from zero at x = 0; the tiles with x < nHx add the response
+// Hx[x] . S0 to the left-extension state (CORR instantiation).
 // ---------------------------------------------------------------------------
 
 template <int G>
 struct P2Ctx {
     const float4* fl[G];  // this row, x = 0, per term
     const float* fT;
-    const float4* cr[G];  // chained carries, this row, stripe 0, per term
-    size_t H;             // float4 stride between x
+    const float4* s0[G];  // left-extension state S0, this row, per term
     float nu_hi[G], nu_lo[G], wt[G];
 };
 
@@ -1042,10 +1091,20 @@ __device__ __forceinline__ void p2_load4(const P2Ctx<G>& c, int x0, int mb, floa
     }
 }
 
-template <int G, bool OUT, bool SM = false>
+// Exact forward output of plane p at x: floc + Hx[x] . S0 when CORR.
+template <bool CORR>
+__device__ __forceinline__ float p2_fwd(float fin, const float4& h, const float (&S)[4]) {
+    if (!CORR) return fin;
+    float F = fmaf(h.x, S[0], fin);
+    F = fmaf(h.y, S[1], F);
+    F = fmaf(h.z, S[2], F);
+    return fmaf(h.w, S[3], F);
+}
+
+template <int G, bool OUT, bool CORR, bool SM = false>
 __device__ __forceinline__ void p2_step4(const Pass2Args& a, const P2Ctx<G>& c, int x0, int mb,
                                          bool full, const float4 (&fo)[4][G], const float (&fv)[4],
-                                         const float (&C)[G][4][4], float (&p1)[G][4],
+                                         const float (&S)[G][4][4], float (&p1)[G][4],
                                          float (&p2)[G][4], float (&q1)[G][4], float (&q2)[G][4],
                                          float* pn, float* pd, bool iv, float2* sb = nullptr) {
     const Casc k = a.k;
@@ -1061,20 +1120,15 @@ __device__ __forceinline__ void p2_step4(const Pass2Args& a, const P2Ctx<G>& c, 
     for (int q = 0; q < 4; ++q) {
         const int m = mb - q;
         if (full || m >= 0) {
-            const float4 h = *reinterpret_cast<const float4*>(&a.Hm[(x0 & (a.unit_cols - 1)) + m][0]);
+            const float4 h = CORR ? __ldg(a.Hx + x0 + m) : f4(0.f, 0.f, 0.f, 0.f);
             float num = 0.f, den = 0.f;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 const float fin[4] = {fo[q][g].x, fo[q][g].y, fo[q][g].z, fo[q][g].w};
                 float y[4];
 #pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    float F = fmaf(h.x, C[g][p][0], fin[p]);
-                    F = fmaf(h.y, C[g][p][1], F);
-                    F = fmaf(h.z, C[g][p][2], F);
-                    F = fmaf(h.w, C[g][p][3], F);
-                    y[p] = cstep(F, p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
-                }
+                for (int p = 0; p < 4; ++p)
+                    y[p] = cstep(p2_fwd<CORR>(fin[p], h, S[g][p]), p1[g][p], p2[g][p], q1[g][p], q2[g][p], k);
                 if (OUT) {
                     num = fmaf(c.wt[g], fmaf(cs[q][g], y[2], sn[q][g] * y[3]), num);
                     den = fmaf(c.wt[g], fmaf(cs[q][g], y[0], sn[q][g] * y[1]), den);
@@ -1091,24 +1145,29 @@ __device__ __forceinline__ void p2_step4(const Pass2Args& a, const P2Ctx<G>& c, 
     }
 }
 
-template <int G, bool OUT, bool SM = false>
-__device__ __forceinline__ void p2_tile(const Pass2Args& a, const P2Ctx<G>& c, int t,
-                                        float (&p1)[G][4], float (&p2)[G][4], float (&q1)[G][4],
-                                        float (&q2)[G][4], float* pn, float* pd, bool iv,
-                                        float2* sb = nullptr) {
-    const int x0 = t * TILE;
-    const int len = min(TILE, a.W - x0);
-    float C[G][4][4];
+template <int G>
+__device__ __forceinline__ void p2_load_s0(const P2Ctx<G>& c, float (&S)[G][4][4]) {
 #pragma unroll
     for (int g = 0; g < G; ++g)
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-            const float4 v = c.cr[g][(size_t)(t * TILE / a.unit_cols) * c.H * 4 + p];
-            C[g][p][0] = v.x;
-            C[g][p][1] = v.y;
-            C[g][p][2] = v.z;
-            C[g][p][3] = v.w;
+            const float4 v = c.s0[g][p];
+            S[g][p][0] = v.x;
+            S[g][p][1] = v.y;
+            S[g][p][2] = v.z;
+            S[g][p][3] = v.w;
         }
+}
+
+template <int G, bool OUT, bool CORR, bool SM = false>
+__device__ __forceinline__ void p2_tile_impl(const Pass2Args& a, const P2Ctx<G>& c, int t,
+                                             float (&p1)[G][4], float (&p2)[G][4], float (&q1)[G][4],
+                                             float (&q2)[G][4], float* pn, float* pd, bool iv,
+                                             float2* sb) {
+    const int x0 = t * TILE;
+    const int len = min(TILE, a.W - x0);
+    float S[G][4][4];
+    if (CORR) p2_load_s0<G>(c, S);
     float4 fa[4][G], fb[4][G];
     float va[4], vb[4];
     if (len == TILE) {
@@ -1118,19 +1177,51 @@ __device__ __forceinline__ void p2_tile(const Pass2Args& a, const P2Ctx<G>& c, i
 #pragma unroll 1
         for (int mb = TILE - 1; mb >= 7; mb -= 8) {
             p2_load4<G, OUT>(c, x0, mb - 4, fb, vb);
-            p2_step4<G, OUT, SM>(a, c, x0, mb, true, fa, va, C, p1, p2, q1, q2, pn, pd, iv, sb);
+            p2_step4<G, OUT, CORR, SM>(a, c, x0, mb, true, fa, va, S, p1, p2, q1, q2, pn, pd, iv, sb);
             p2_load4<G, OUT>(c, x0, mb - 8, fa, va);  // clamped at x0 on the last iteration
-            p2_step4<G, OUT, SM>(a, c, x0, mb - 4, true, fb, vb, C, p1, p2, q1, q2, pn, pd, iv, sb);
+            p2_step4<G, OUT, CORR, SM>(a, c, x0, mb - 4, true, fb, vb, S, p1, p2, q1, q2, pn, pd, iv, sb);
         }
     } else {
 #pragma unroll 1
         for (int mb = len - 1; mb >= 0; mb -= 4) {
             p2_load4<G, OUT>(c, x0, mb, fa, va);
-            p2_step4<G, OUT, SM>(a, c, x0, mb, false, fa, va, C, p1, p2, q1, q2, pn, pd, iv, sb);
+            p2_step4<G, OUT, CORR, SM>(a, c, x0, mb, false, fa, va, S, p1, p2, q1, q2, pn, pd, iv, sb);
         }
     }
 }
 
+// One tile right to left; the tiles left of nHx take the S0 correction.
+template <int G, bool OUT, bool SM = false>
+__device__ __forceinline__ void p2_tile(const Pass2Args& a, const P2Ctx<G>& c, int t,
+                                        float (&p1)[G][4], float (&p2)[G][4], float (&q1)[G][4],
+                                        float (&q2)[G][4], float* pn, float* pd, bool iv,
+                                        float2* sb = nullptr) {
+    if (t * TILE < a.nHx)
+        p2_tile_impl<G, OUT, true, SM>(a, c, t, p1, p2, q1, q2, pn, pd, iv, sb);
+    else
+        p2_tile_impl<G, OUT, false, SM>(a, c, t, p1, p2, q1, q2, pn, pd, iv, sb);
+}
+
+// Exact forward output of one term at x (warm-up start of an x-chunk).
+template <int G>
+__device__ __forceinline__ void p2_fwd_at(const Pass2Args& a, const P2Ctx<G>& c, int g, int x,
+                                          float (&F)[4]) {
+    const float4 v = c.fl[g][(size_t)x * FL_RB];
+    F[0] = v.x;
+    F[1] = v.y;
+    F[2] = v.z;
+    F[3] = v.w;
+    if (x < a.nHx) {
+        const float4 h = __ldg(a.Hx + x);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const float4 s = c.s0[g][p];
+            F[p] = fmaf(h.x, s.x, fmaf(h.y, s.y, fmaf(h.z, s.z, fmaf(h.w, s.w, F[p]))));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Pass 2 with the term groups of a block summed on chip: 4 warps = 32 rows x
 // 4 groups of G terms (warp w = group 4*blockIdx.y + w).  Each warp stages
 // its tile's (num, den) in shared memory; after a barrier the block adds the
@@ -1188,7 +1279,6 @@ __global__ void __launch_bounds__(32 * P2R_GR, TBF_P2_MINB) k_pass2_gr(const __g
     const int j0 = grp * G;
     const int nt = min(G, a.t.n - j0);
     P2Ctx<G> c;
-    c.H = (size_t)H;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         const int j = min(j0 + g, a.t.n - 1);
@@ -1197,7 +1287,7 @@ __global__ void __launch_bounds__(32 * P2R_GR, TBF_P2_MINB) k_pass2_gr(const __g
         c.wt[g] = g < nt ? a.t.w[j] * a.wscale : 0.f;
         c.fl[g] = reinterpret_cast<const float4*>(a.floc) +
                   (((size_t)j * a.B + b) * ((H + FL_RB - 1) / FL_RB) + i / FL_RB) * W * (size_t)FL_RB + (i % FL_RB);
-        c.cr[g] = reinterpret_cast<const float4*>(a.carry) + (((size_t)j * a.B + b) * a.nst * H + i) * 4;
+        c.s0[g] = reinterpret_cast<const float4*>(a.s0) + (((size_t)j * a.B + b) * H + i) * 4;
     }
     c.fT = a.fT + xm_index(b, 0, i, W, H);
     const size_t xpl = xm_plane(a.B, W, H);
@@ -1235,19 +1325,16 @@ __global__ void __launch_bounds__(32 * P2R_GR, TBF_P2_MINB) k_pass2_gr(const __g
 #pragma unroll 1
             for (int t = a.ntx - 1; t >= t_hi; --t) p2_tile<G, false>(a, c, t, p1, p2, q1, q2, pn, pd, iv);
         } else {
+            // warm-up: steady state of the exact forward output at the
+            // warm-up start, then backward (no output) down to t_hi
             const int tw = min(a.ntx - 1, t_hi - 1 + a.warm_tiles);
             const int xs = min(W - 1, tw * TILE + TILE - 1);
-            const float4 h = *reinterpret_cast<const float4*>(&a.Hm[xs & (a.unit_cols - 1)][0]);
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                const float4 F = c.fl[g][(size_t)xs * FL_RB];
-                const float fin[4] = {F.x, F.y, F.z, F.w};
+                float F[4];
+                p2_fwd_at<G>(a, c, g, xs, F);
 #pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    const float4 cv = c.cr[g][(size_t)(xs / a.unit_cols) * c.H * 4 + p];
-                    const float v = fmaf(h.x, cv.x, fmaf(h.y, cv.y, fmaf(h.z, cv.z, fmaf(h.w, cv.w, fin[p]))));
-                    csteady(v, p1[g][p], p2[g][p], q1[g][p], q2[g][p], a.k);
-                }
+                for (int p = 0; p < 4; ++p) csteady(F[p], p1[g][p], p2[g][p], q1[g][p], q2[g][p], a.k);
             }
 #pragma unroll 1
             for (int t = tw; t >= t_hi; --t) p2_tile<G, false>(a, c, t, p1, p2, q1, q2, pn, pd, iv);
@@ -1732,7 +1819,6 @@ size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 struct Layout {
     int B, H, W, Ey, Ex, nseg, ntx, ne, edge_all;
     int nst;  // stripes of P1_WARPS column tiles (pass-1 blocks per term and y-chunk)
-    int unit, nun;  // x chain unit in column tiles (P1_WARPS or 1) and units per row
     int nyc, ych_rows, ywarm;  // pass-1 y-chunking (nseg = checkpoint segments per chunk)
     int ychb[TBF_MAX_YCH + 1];  // chunk boundaries (ych_rows = the largest chunk)
     bool ych_lpt;               // chunks of unequal size, dispatched largest first
@@ -1744,7 +1830,7 @@ struct Layout {
     size_t off_fT, off_fY, off_num, off_den, off_tab;
     // per-slot buffers (offsets relative to the slot base)
     size_t off_slot, slot_bytes;
-    size_t s_ckpt, s_floc, s_lc, s_edge, s_ext, s_bst, s_part;
+    size_t s_ckpt, s_floc, s_mail, s_flags, s_edge, s_s0, s_bst, s_part;
     size_t total;
 };
 
@@ -1895,12 +1981,6 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     L->Ex = box ? 0 : std::max(0, std::min(sp->ext_x, W - 1));
     L->ntx = (W + TILE - 1) / TILE;
     L->nst = (W + STRIPE - 1) / STRIPE;
-    // x carries per stripe, except for very long decays (sigma_s >~ 130):
-    // there the correction by the unit-state response over 128 columns
-    // loses fp32 digits to cancellation (measured: 0.27 vs 0.18 max error at
-    // sigma_s = 300), and 32-column units keep the round-1 accuracy
-    L->unit = (!box && sp->ext_x > 1536) ? 1 : P1_WARPS;
-    L->nun = (L->ntx + L->unit - 1) / L->unit;
     L->edge_all = 2 * (L->Ex + 1) >= W;
     L->ne = L->edge_all ? W : 2 * (L->Ex + 1);
     int tb;
@@ -2026,18 +2106,21 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     L->off_den = o;
     if (multi) o = align_up(o + px * 4);
     L->off_tab = o;
-    o = align_up(o + (tab_bx_offset(nterms_range) + (size_t)4 * L->Ex) * 4);
+    o = align_up(o + (tab_bx_offset(nterms_range) + (size_t)4 * L->Ex + (size_t)4 * L->ntx * TILE) * 4);
     // one slot
     size_t q = 0;
     L->s_ckpt = q;
     if (!box) q = align_up(q + (size_t)L->nyc * L->nseg * tb * 16 * B * W * 4);
     L->s_floc = q;  // row-block tiled like xm_index (padded to whole FL_RB-row blocks)
     q = align_up(q + (size_t)tb * 4 * B * W * ((size_t)(H + FL_RB - 1) / FL_RB * FL_RB) * 4);
-    L->s_lc = q;
-    if (!box) q = align_up(q + (size_t)tb * 16 * B * L->nun * H * 4);
+    L->s_mail = q;  // pass-1 x chain hand-off: float4 [tb][B][nst+1][H][4]
+    if (!box) q = align_up(q + (size_t)tb * 16 * B * (L->nst + 1) * H * 4);
+    L->s_flags = q;  // [tb][B][nst][ceil(H/32)] hand-off flags + the dispatch tickets
+    if (!box) q = align_up(q + ((size_t)tb * B * L->nst * ((H + TILE - 1) / TILE) + P1_MAX_LAUNCHES) * 4);
     L->s_edge = q;
     if (!box) q = align_up(q + (size_t)tb * 4 * B * L->ne * H * 4);
-    L->s_ext = q;  // (unused: the right x-extension is in closed form)
+    L->s_s0 = q;
+    if (!box) q = align_up(q + (size_t)tb * 16 * B * H * 4);
     L->s_bst = q;
     if (!box) q = align_up(q + (size_t)tb * 16 * B * H * 4);
     L->s_part = q;
@@ -2079,27 +2162,41 @@ cudaEvent_t event_get() {
     return pool[next++ % pool.size()];
 }
 
-// Zero-input evolution of the pure cascade: state s=(v1,v2,y1,y2) after
-// `steps` samples (M, column-major) and the output y at each step (Hm).
-void cascade_responses(const tbf_spatial* sp, int steps, double M[16], double (*Hm)[4]) {
+// Response of the pure cascade to a unit state at x = 0 with zero input:
+// hx[x] = output at sample x for each of the 4 unit states (what pass 2 adds
+// to the zero-start chain, times the left-extension state S0), kept up to
+// nHx = the whole tiles that cover every sample where it exceeds 1e-9 of its
+// peak (at most W); MW = the state after all W samples (column-major, what
+// the edge kernel adds to the chain's end state).  Double precision.
+void left_response(const tbf_spatial* sp, int W, std::vector<float>& hx, int& nHx, double MW[16]) {
+    std::vector<double> h((size_t)W * 4);
+    double peak = 0.0;
     for (int kk = 0; kk < 4; ++kk) {
-        double s[4] = {0, 0, 0, 0};
-        s[kk] = 1.0;
-        double v1 = s[0], v2 = s[1], y1 = s[2], y2 = s[3];
-        for (int m = 0; m < steps; ++m) {
-            double v = sp->a1 * v1 + sp->a2 * v2;
+        double v1 = kk == 0, v2 = kk == 1, y1 = kk == 2, y2 = kk == 3;
+        for (int x = 0; x < W; ++x) {
+            const double v = sp->a1 * v1 + sp->a2 * v2;
             v2 = v1;
             v1 = v;
-            double y = v + sp->b1 * y1 + sp->b2 * y2;
+            const double y = v + sp->b1 * y1 + sp->b2 * y2;
             y2 = y1;
             y1 = y;
-            if (Hm) Hm[m][kk] = y;
+            h[(size_t)x * 4 + kk] = y;
+            peak = std::max(peak, std::fabs(y));
         }
-        M[kk * 4 + 0] = v1;
-        M[kk * 4 + 1] = v2;
-        M[kk * 4 + 2] = y1;
-        M[kk * 4 + 3] = y2;
+        MW[kk * 4 + 0] = v1;
+        MW[kk * 4 + 1] = v2;
+        MW[kk * 4 + 2] = y1;
+        MW[kk * 4 + 3] = y2;
     }
+    int last = 0;
+    for (int x = 0; x < W; ++x)
+        for (int kk = 0; kk < 4; ++kk)
+            if (std::fabs(h[(size_t)x * 4 + kk]) > 1e-9 * peak) last = x + 1;
+    nHx = std::min(W, (last + TILE - 1) / TILE * TILE);
+    const int ntile = (nHx + TILE - 1) / TILE * TILE;
+    hx.assign((size_t)ntile * 4, 0.f);
+    for (int x = 0; x < std::min(ntile, W); ++x)
+        for (int kk = 0; kk < 4; ++kk) hx[(size_t)x * 4 + kk] = (float)h[(size_t)x * 4 + kk];
 }
 
 // Closed form of the chain's right x-extension (spatial.py:171 mirror pad,
@@ -2422,11 +2519,16 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
 
     // term tables: nu split hi/lo, float weights; zero padded past the end
     const int ld = nrange + TAB_PAD;
-    double Rx[16] = {0};
-    std::vector<float> bx;
-    if (!box) right_ext_coeffs(sp, L.Ex, Rx, bx);
-    std::vector<float> h_tab(tab_bx_offset(nrange) + bx.size(), 0.f);
+    double Rx[16] = {0}, MW[16] = {0};
+    std::vector<float> bx, hx;
+    int nHx = 0;
+    if (!box) {
+        right_ext_coeffs(sp, L.Ex, Rx, bx);
+        left_response(sp, W, hx, nHx, MW);
+    }
+    std::vector<float> h_tab(tab_bx_offset(nrange) + bx.size() + hx.size(), 0.f);
     std::copy(bx.begin(), bx.end(), h_tab.begin() + tab_bx_offset(nrange));
+    std::copy(hx.begin(), hx.end(), h_tab.begin() + tab_bx_offset(nrange) + bx.size());
     for (int j = 0; j < nrange; ++j) {
         double nu = terms->nu[tbeg + j];
         float hi = (float)nu;
@@ -2493,13 +2595,6 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
     // (measured: ~1% faster on configs 2-4 now that it no longer spills)
     const bool fold = g_pass1_fold && !box &&
                       std::log10(std::max(terms->T, 1.0)) - 4.0 * std::log10(sp->g1 * sp->g2) < 34.0;
-    double M[16], Mlast[16], Hm[STRIPE][4];
-    if (!box) {
-        const int ucols = L.unit * TILE;
-        cascade_responses(sp, ucols, M, Hm);
-        cascade_responses(sp, W - (L.nun - 1) * ucols, Mlast, nullptr);
-    }
-
     if (s2 != st) {
         cudaEvent_t e0 = event_get();
         cudaEventRecord(e0, st);  // f, fT and the term table are ready
@@ -2510,8 +2605,12 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         const int n = std::min(L.tb, nrange - jb);
         float* ckpt = slot(bi, L.s_ckpt);
         float* floc = slot(bi, L.s_floc);
-        float* lc = slot(bi, L.s_lc);
+        float* mail = slot(bi, L.s_mail);
+        int* flags = reinterpret_cast<int*>(slot(bi, L.s_flags));
+        const size_t nflags = (size_t)L.tb * B * L.nst * ((H + TILE - 1) / TILE);
+        unsigned int* tickets = reinterpret_cast<unsigned int*>(flags + nflags);
         float* edge = slot(bi, L.s_edge);
+        float* s0 = slot(bi, L.s_s0);
         float* bst = slot(bi, L.s_bst);
         float* part = slot(bi, L.s_part);
         // the slot is free once batch bi - nslot has finished on s2
@@ -2545,45 +2644,52 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p1.nst = L.nst;
         p1.st0 = 0;
         p1.nst_run = L.nst;
-        p1.unit = L.unit;
-        p1.nun = L.nun;
         p1.k = kc;
         p1.t = td;
         p1.ckpt = ckpt;
         p1.floc = floc;
-        p1.lcarry = lc;
+        p1.mail = mail;
+        p1.flags = flags;
+        p1.nsegH = (H + TILE - 1) / TILE;
         p1.edge = edge;
         // box: blocks of P1_WARPS terms x one column tile; Gaussian: blocks
         // of one term x one stripe (term fastest, then stripe, y-chunk)
         const dim3 gbox(L.ntx, (n + P1_WARPS - 1) / P1_WARPS, B);
-        auto p1grid = [&](int nst_run) { return dim3(nst_run * L.nyc * n, 1, B); };
+        // Gaussian: 1-D grid, blocks map to (stripe, frame, y-chunk, term) by a
+        // dispatch ticket; one counter per launch after the flags
+        auto p1grid = [&](int nst_run) { return dim3(nst_run * B * L.nyc * n, 1, 1); };
         const int p1smem = g_p1_occ == 2 ? P1_SMEM_OCC2 : P1_SMEM_GAUSS;
+        if (!box) cudaMemsetAsync(flags, 0, (nflags + P1_MAX_LAUNCHES) * sizeof(int), st);
         if (strip_p1 && bi == 0) {
-            // strip s on alternating streams, after its copy: transpose (+
-            // range check), then pass 1; joined before the chain
+            // strip s: transpose (+ range check) on a side stream as soon as
+            // its copy lands, pass 1 in strip order on the caller's stream
+            // (stripe s waits for stripe s-1: a strip's blocks only wait for
+            // strips launched before it on the same stream)
+            cudaStream_t ts = aux_stream(2);
+            cudaStreamWaitEvent(ts, e_ready, 0);
             for (size_t s = 0; s < ev_strip.size(); ++s) {
-                cudaStream_t ps = aux_stream(2 + (int)(s & 1));
-                cudaStreamWaitEvent(ps, e_ready, 0);
-                cudaStreamWaitEvent(ps, ev_strip[s], 0);
+                cudaStreamWaitEvent(ts, ev_strip[s], 0);
                 p1.st0 = sb[s];
                 p1.nst_run = sb[s + 1] - sb[s];
                 {
                     const int t0 = sb[s] * P1_WARPS, t1 = std::min(L.ntx, sb[s + 1] * P1_WARPS);
                     dim3 tg(t1 - t0, (H + TILE - 1) / TILE, B);
-                    Prof pr(KK_TRANSPOSE, ps);
-                    k_transpose<<<tg, 256, 0, ps>>>(f, fT, fY, H, W, -1e-9, terms->T + 1e-9, rc_counters, t0);
-                }
-                {
-                    Prof pr(KK_PASS1, ps);
-                    launch_pass1(fold, p1_mode(L, p1), p1grid(p1.nst_run), p1smem, ps, p1);
+                    Prof pr(KK_TRANSPOSE, ts);
+                    k_transpose<<<tg, 256, 0, ts>>>(f, fT, fY, H, W, -1e-9, terms->T + 1e-9, rc_counters, t0);
                 }
                 cudaEvent_t e = event_get();
-                cudaEventRecord(e, ps);
+                cudaEventRecord(e, ts);
                 cudaStreamWaitEvent(st, e, 0);
+                p1.ticket = tickets + std::min<size_t>(s, P1_MAX_LAUNCHES - 1);
+                {
+                    Prof pr(KK_PASS1, st);
+                    launch_pass1(fold, p1_mode(L, p1), p1grid(p1.nst_run), p1smem, st, p1);
+                }
             }
             p1.st0 = 0;
             p1.nst_run = L.nst;
         } else {
+            p1.ticket = tickets;
             Prof pr(KK_PASS1, st);
             if (box)
                 k_pass1_box<G1, R_ANCHOR><<<gbox, P1_WARPS * 32, P1_SMEM, st>>>(p1, sp->radius);
@@ -2598,29 +2704,28 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         }
 
         if (!box) {
-            ChainArgs ca;
-            ca.B = B;
-            ca.H = H;
-            ca.W = W;
-            ca.Ex = L.Ex;
-            ca.ne = L.ne;
-            ca.edge_all = L.edge_all;
-            ca.nst = L.nun;
-            ca.k = kc;
-            ca.nplanes = n * 4;
-            ca.n = n;
+            EdgeArgs ea;
+            ea.B = B;
+            ea.H = H;
+            ea.W = W;
+            ea.Ex = L.Ex;
+            ea.ne = L.ne;
+            ea.edge_all = L.edge_all;
+            ea.nst = L.nst;
+            ea.k = kc;
+            ea.n = n;
+            ea.edge = edge;
+            ea.mail = mail;
             for (int q = 0; q < 16; ++q) {
-                ca.M[q] = (float)M[q];
-                ca.Mlast[q] = (float)Mlast[q];
+                ea.MW[q] = (float)MW[q];
+                ea.Rx[q] = (float)Rx[q];
             }
-            ca.edge = edge;
-            ca.lcarry = lc;
-            for (int q = 0; q < 16; ++q) ca.Rx[q] = (float)Rx[q];
-            ca.bx = reinterpret_cast<const float4*>(tab + tab_bx_offset(nrange));
-            ca.bstate = bst;
+            ea.bx = reinterpret_cast<const float4*>(tab + tab_bx_offset(nrange));
+            ea.s0 = s0;
+            ea.bstate = bst;
             dim3 gc((H + 127) / 128, n * B);
-            { Prof pr(KK_CHAIN, s2); k_chain<<<gc, 128, 0, s2>>>(ca); }
-            if ((rc = check_cuda("chain"))) return rc;
+            { Prof pr(KK_CHAIN, s2); k_edge<<<gc, 128, 0, s2>>>(ea); }
+            if ((rc = check_cuda("edge"))) return rc;
         }
 
         Pass2Args p2;
@@ -2629,21 +2734,19 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.H = H;
         p2.W = W;
         p2.ntx = L.ntx;
-        p2.nst = L.nun;
-        p2.unit_cols = L.unit * TILE;
         p2.k = kc;
         p2.t = td;
         // pass 2: the block-summed variant (k_pass2_gr) for the Gaussian
         const int npart = box ? -1 : (((n + G2 - 1) / G2 + P2R_GR - 1) / P2R_GR);
         p2.ngroups = (n + G2 - 1) / G2;
-        for (int m = 0; m < STRIPE; ++m)
-            for (int q = 0; q < 4; ++q) p2.Hm[m][q] = (box || m >= L.unit * TILE) ? 0.f : (float)Hm[m][q];
         {
             const double g = sp->g1 * sp->g2;
             p2.wscale = box ? 1.f : (float)(fold ? g * g * g * g : g * g);
         }
         p2.floc = floc;
-        p2.carry = lc;
+        p2.nHx = nHx;
+        p2.Hx = reinterpret_cast<const float4*>(tab + tab_bx_offset(nrange) + bx.size());
+        p2.s0 = s0;
         p2.bstate = bst;
         p2.part = part;
         p2.order = g_p2_order;
