@@ -192,6 +192,7 @@ __device__ __forceinline__ long long mirror_any(long long i, long long n) {
     return i >= n ? period - i : i;
 }
 
+
 // F_loc is written once (pass 1) and read once (pass 2), far apart: with
 // TBF_CACHE_HINTS its stores and loads are streaming (evict-first), so the
 // 16 B/pixel-term stream does not evict the L2-resident f tile copy,
@@ -855,11 +856,12 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
         if (i0 >= R1) continue;  // warm-up / extension segment: no output
         __syncwarp();
         // epilogue: lane <-> row i; forward along x over the tile's 32
-        // columns, starting from the state the warp of the tile to the left
-        // hands over (zero at the stripe's first tile: the stripes are
-        // chained by k_chain, the tiles of a stripe here).  Named barriers
-        // per link w -> w+1: FULL (1 + w) when the slot is written, EMPTY
-        // (1 + P1_WARPS + w) when it has been read.
+        // columns, starting from the state at the tile's first column: from
+        // the warp to the left through smem (named barriers per link w ->
+        // w+1: FULL 1 + w when the slot is written, EMPTY 1 + P1_WARPS + w
+        // when it has been read), for warp 0 from stripe s-1 through the L2
+        // mailbox and its flag (zero at x = 0: pass 2 adds the response to
+        // the left extension's state).
         const int i = i0 + lane;
         const bool rowv = lane < min(len, R1 - i0);
         const bool last_out = i0 == R0;  // segments run bottom to top
@@ -899,8 +901,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
 #pragma unroll
             for (int p = 0; p < 4; ++p) lv1[p] = lv2[p] = ly1[p] = ly2[p] = 0.f;
         }
+        float4* const fl = fl0 + ((size_t)(i / FL_RB) * W + x0) * FL_RB + (i % FL_RB);
         if (rowv && tlen > 0) {
-            float4* fl = fl0 + ((size_t)(i / FL_RB) * W + x0) * FL_RB + (i % FL_RB);
             const bool edge_tile = a.edge_all || x0 <= a.Ex || x0 + tlen - 1 >= W - 1 - a.Ex;
             if (tlen == TILE && !edge_tile) {
 #pragma unroll 1
