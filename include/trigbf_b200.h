@@ -20,6 +20,8 @@
  *                        pairs [term_begin, term_end): accumulates num/den only
  *                        (term-sharded multi-GPU path; NCCL reduce sits between
  *                        this and tbf_finalize)
+ *   tbf_trig_partial_rows the same restricted to a band of output rows (balanced
+ *                        term sharding: leftover terms split by rows)
  *   tbf_finalize         engines.py:109-117  _guarded_ratio(num, den, f)
  *   tbf_range_check      engines.py:218-225  _check_range(plane, T)
  *   tbf_recursive_smooth_f64
@@ -139,6 +141,19 @@ TBF_API int tbf_trig_partial(const float* f, float* num, float* den, int32_t B, 
                      const tbf_spatial* sp, const tbf_terms* terms, int32_t term_begin,
                      int32_t term_end, int32_t batch_terms, int32_t accumulate,
                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* Row-band form of tbf_trig_partial (recursive Gaussian only): the pairs'
+ * contribution to rows [row_begin, row_end) of num/den only (other rows are
+ * not touched).  row_begin is a multiple of 128, row_end a multiple of 128 or
+ * H.  Pass 1 starts its y sweeps a warm-up length outside the band, so the
+ * band equals the same rows of a full-image call to the warm-up truncation
+ * level (1e-7 relative).  The term-sharded path gives the terms left over
+ * after an even split to every rank as one band each (balanced work).
+ * Workspace: tbf_workspace_bytes of the whole image. */
+TBF_API int tbf_trig_partial_rows(const float* f, float* num, float* den, int32_t B, int32_t H, int32_t W,
+                                  const tbf_spatial* sp, const tbf_terms* terms, int32_t term_begin,
+                                  int32_t term_end, int32_t row_begin, int32_t row_end, int32_t batch_terms,
+                                  int32_t accumulate, void* workspace, size_t workspace_bytes, void* stream);
 
 /* out = num/den where den >= 1e-12, else f; d_counters[1] += guarded count. */
 TBF_API int tbf_finalize(const float* num, const float* den, const float* f, float* out, int64_t count,

@@ -49,6 +49,7 @@ EXPORTS = (
     "tbf_bilateral_trig_host",
     "tbf_bilateral_direct",
     "tbf_trig_partial",
+    "tbf_trig_partial_rows",
     "tbf_finalize",
     "tbf_range_check",
     "tbf_recursive_smooth_f64",
@@ -62,7 +63,7 @@ EXPORTS = (
     "tbf_profile_timeline",
     "tbf_set_option",
 )
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class TbfSpatial(ctypes.Structure):
@@ -128,6 +129,11 @@ def _declare(lib):
     lib.tbf_trig_partial.argtypes = [
         _vp, _vp, _vp, _i32, _i32, _i32, ctypes.POINTER(TbfSpatial), ctypes.POINTER(TbfTerms),
         _i32, _i32, _i32, _i32, _vp, _sz, _vp,
+    ]
+    lib.tbf_trig_partial_rows.restype = ctypes.c_int
+    lib.tbf_trig_partial_rows.argtypes = [
+        _vp, _vp, _vp, _i32, _i32, _i32, ctypes.POINTER(TbfSpatial), ctypes.POINTER(TbfTerms),
+        _i32, _i32, _i32, _i32, _i32, _i32, _vp, _sz, _vp,
     ]
     lib.tbf_finalize.restype = ctypes.c_int
     lib.tbf_finalize.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _vp]

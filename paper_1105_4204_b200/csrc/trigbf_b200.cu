@@ -56,7 +56,7 @@
 
 #include "trigbf_b200.h"
 
-#define TBF_ABI_VERSION 1
+#define TBF_ABI_VERSION 2
 
 namespace {
 
@@ -463,6 +463,7 @@ struct Pass1Args {
     int B, H, W;
     int Ey, nseg;  // y mirror extension; checkpoint segments per y-chunk
     int nyc, ych_rows, ywarm;  // y-chunks (at most ych_rows output rows each); warm-up rows (mult. of 32)
+    int row0, row1;            // output rows of this call (equal chunks start at row0)
     // unequal chunks (ylpt, at most 3): rows [0, yb1), [yb1, yb2), [yb2, H);
     // scalars, not a table: a dynamically indexed parameter array made ptxas
     // spill in this kernel (9% slower pass 1 on config 5)
@@ -493,6 +494,7 @@ struct Pass1Args {
 // the backward start state at x = W-1 (the right extension, in closed form).
 struct EdgeArgs {
     int B, H, W;
+    int row0, row1;       // rows of this call
     int Ex, ne, edge_all, nst;  // nst = stripes (mail slot nst = chain end state at x = W)
     Casc k;
     int n;                // terms in the batch
@@ -656,8 +658,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
         R0 = chunk == 0 ? 0 : (chunk == 1 ? a.yb1 : a.yb2);
         R1 = chunk == 0 ? a.yb1 : (chunk == 1 ? a.yb2 : H);
     } else {
-        R0 = chunk * a.ych_rows;
-        R1 = min(H, R0 + a.ych_rows);
+        R0 = a.row0 + chunk * a.ych_rows;
+        R1 = min(a.row1, R0 + a.ych_rows);
     }
     const int A0 = R0 - a.ywarm <= 0 ? -Ey : R0 - a.ywarm;
     const int Bend = R1 + a.ywarm >= iend ? iend : R1 + a.ywarm;
@@ -983,8 +985,8 @@ __device__ __forceinline__ void cstep4(const float4& u, float (&v1)[4], float (&
 }
 
 __global__ void __launch_bounds__(128) k_edge(const __grid_constant__ EdgeArgs a) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.H) return;
+    const int i = a.row0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.row1) return;
     const int bt = blockIdx.y;  // term * B + b
     const int H = a.H, W = a.W, Ex = a.Ex;
     const Casc k = a.k;
@@ -1820,6 +1822,7 @@ size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
     int B, H, W, Ey, Ex, nseg, ntx, ne, edge_all;
+    int row0, row1;  // output rows (a band for the term-sharded leftover terms, else [0, H))
     int nst;  // stripes of P1_WARPS column tiles (pass-1 blocks per term and y-chunk)
     int nyc, ych_rows, ywarm;  // pass-1 y-chunking (nseg = checkpoint segments per chunk)
     int ychb[TBF_MAX_YCH + 1];  // chunk boundaries (ych_rows = the largest chunk)
@@ -1972,9 +1975,20 @@ std::vector<int> p1_plan_split(int H, int Ey, int ywarm, long long per_chunk, in
 // unequal chunks when TBF_OPT_LPT_SPLIT enables them, 2 planned regardless of
 // the option (workspace sizing: a plan must fit whatever the option is later)
 int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, int batch_terms,
-                Layout* L, int lpt = 1) {
+                Layout* L, int lpt = 1, int row0 = 0, int row1 = -1) {
     if (B < 1 || H < 1 || W < 1) return fail(TBF_ERR_DIM, "bad shape B=%d H=%d W=%d", B, H, W);
     if (!sp) return fail(TBF_ERR_PARAM, "null spatial");
+    if (row1 < 0) row1 = H;
+    // output rows [row0, row1): a band of whole 128-row pass-2 blocks (the
+    // term-sharded path splits leftover terms by bands); planned chunks only
+    // for the whole image
+    if (row0 < 0 || row1 > H || row0 >= row1 || row0 % P2_THREADS || (row1 % P2_THREADS && row1 != H))
+        return fail(TBF_ERR_PARAM, "bad row band [%d, %d) of %d (multiples of %d)", row0, row1, H, P2_THREADS);
+    const bool band = row0 > 0 || row1 < H;
+    if (band) lpt = 0;
+    L->row0 = row0;
+    L->row1 = row1;
+    const int Hb = row1 - row0;
     L->B = B;
     L->H = H;
     L->W = W;
@@ -2014,8 +2028,8 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
         double best = -1.0;
         int best_n = 1;
         for (int nyc = 1; nyc <= 16; ++nyc) {
-            const int rows = ((H + nyc - 1) / nyc + TILE - 1) / TILE * TILE;
-            const int n = (H + rows - 1) / rows;
+            const int rows = ((Hb + nyc - 1) / nyc + TILE - 1) / TILE * TILE;
+            const int n = (Hb + rows - 1) / rows;
             if (n != nyc) continue;  // same split as a smaller count
             // chunks shorter than the warm-up only while the launch stays
             // under one wave (long decays on small images: parallelism
@@ -2025,9 +2039,9 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
             // clamped to the mirror extension [-Ey, H + Ey)
             double len = 0.0;
             for (int c = 0; c < n; ++c) {
-                const int R0 = c * rows, R1 = std::min(H, R0 + rows);
-                const int A0 = nyc == 1 ? -L->Ey : std::max(R0 - L->ywarm, -L->Ey);
-                const int A1 = nyc == 1 ? H + L->Ey : std::min(R1 + L->ywarm, H + L->Ey);
+                const int R0 = row0 + c * rows, R1 = std::min(row1, R0 + rows);
+                const int A0 = (nyc == 1 && !band) ? -L->Ey : std::max(R0 - L->ywarm, -L->Ey);
+                const int A1 = (nyc == 1 && !band) ? H + L->Ey : std::min(R1 + L->ywarm, H + L->Ey);
                 len = std::max(len, (double)(A1 - A0));
             }
             const double waves = blocks1 * nyc / slots;
@@ -2041,13 +2055,13 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
         if (g_p1_ychunks > 0) {
             // forced count: at most TBF_MAX_YCH chunks (ychb[] bound), none
             // shorter than the warm-up (the automatic search's own limit)
-            const int max_by_warm = std::max(1, H / std::max(L->ywarm, TILE));
-            nyc = std::min(std::min(g_p1_ychunks, TBF_MAX_YCH), std::min((H + TILE - 1) / TILE, max_by_warm));
+            const int max_by_warm = std::max(1, Hb / std::max(L->ywarm, TILE));
+            nyc = std::min(std::min(g_p1_ychunks, TBF_MAX_YCH), std::min((Hb + TILE - 1) / TILE, max_by_warm));
         }
-        L->ych_rows = ((H + nyc - 1) / nyc + TILE - 1) / TILE * TILE;
-        L->nyc = (H + L->ych_rows - 1) / L->ych_rows;
+        L->ych_rows = ((Hb + nyc - 1) / nyc + TILE - 1) / TILE * TILE;
+        L->nyc = (Hb + L->ych_rows - 1) / L->ych_rows;
     }
-    for (int c = 0; c <= L->nyc; ++c) L->ychb[c] = std::min(H, c * L->ych_rows);
+    for (int c = 0; c <= L->nyc; ++c) L->ychb[c] = std::min(row1, row0 + c * L->ych_rows);
     L->ych_lpt = false;
     // single-batch runs only: the workspace of batched runs stays affine in
     // the batch size (the engine's batch picker fits it), and their launches
@@ -2069,7 +2083,7 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
             L->ych_lpt = L->nyc > 1;
         }
     }
-    if (!box) {
+    if (!box && !band) {
         // development override: explicit chunk row counts, e.g. "1280,768"
         // (multiples of 32, largest first; the last one takes the rest)
         const char* ev = getenv("TBF_P1_YSPLIT");
@@ -2492,13 +2506,17 @@ int stage_term_table(const std::vector<float>& h_tab, float* d_tab, cudaStream_t
 int run_terms(const float* f, float* num, float* den, float* out, int B, int H, int W,
               const tbf_spatial* sp, const tbf_terms* terms, int tbeg, int tend, int batch_terms,
               int accumulate, void* ws, size_t ws_bytes, unsigned long long* counters,
-              cudaStream_t st, const HostIO* hio = nullptr) {
+              cudaStream_t st, const HostIO* hio = nullptr, int row0 = 0, int row1 = -1) {
     int rc = validate(sp, terms, tbeg, tend);
     if (rc) return rc;
     const int nrange = tend - tbeg;
     Layout L;
-    rc = make_layout(B, H, W, sp, nrange, batch_terms, &L, (hio == nullptr || (g_lpt_split & 4)) ? 1 : 0);
+    rc = make_layout(B, H, W, sp, nrange, batch_terms, &L, (hio == nullptr || (g_lpt_split & 4)) ? 1 : 0,
+                     row0, row1);
     if (rc) return rc;
+    const bool band = L.row0 > 0 || L.row1 < H;
+    if (band && (out || hio || sp->kind == TBF_SPATIAL_BOX))
+        return fail(TBF_ERR_PARAM, "row bands are for the recursive partial (num/den) path only");
     if (!ws || ws_bytes < L.total)
         return fail(TBF_ERR_WORKSPACE, "workspace too small: need %zu have %zu", L.total, ws_bytes);
     char* w8 = (char*)ws;
@@ -2639,6 +2657,8 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p1.yb1 = L.nyc > 1 ? L.ychb[1] : H;
         p1.yb2 = L.nyc > 2 ? L.ychb[2] : H;
         p1.ywarm = L.ywarm;
+        p1.row0 = L.row0;
+        p1.row1 = L.row1;
         p1.Ex = L.Ex;
         p1.ne = L.ne;
         p1.edge_all = L.edge_all;
@@ -2710,6 +2730,8 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             ea.B = B;
             ea.H = H;
             ea.W = W;
+            ea.row0 = L.row0;
+            ea.row1 = L.row1;
             ea.Ex = L.Ex;
             ea.ne = L.ne;
             ea.edge_all = L.edge_all;
@@ -2725,7 +2747,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             ea.bx = reinterpret_cast<const float4*>(tab + tab_bx_offset(nrange));
             ea.s0 = s0;
             ea.bstate = bst;
-            dim3 gc((H + 127) / 128, n * B);
+            dim3 gc((L.row1 - L.row0 + 127) / 128, n * B);
             { Prof pr(KK_CHAIN, s2); k_edge<<<gc, 128, 0, s2>>>(ea); }
             if ((rc = check_cuda("edge"))) return rc;
         }
@@ -2839,7 +2861,8 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             if ((rc = check_cuda("device to host"))) return rc;
             hio = nullptr;  // output delivered
         } else {
-            if ((rc = pass2_reduce(0, nrb, s2))) return rc;
+            const int rb0 = L.row0 / P2_THREADS, rb1 = (L.row1 + P2_THREADS - 1) / P2_THREADS;
+            if ((rc = pass2_reduce(rb0, rb1 - rb0, s2))) return rc;
         }
         if (s2 != st) {
             ev_done[bi] = event_get();
@@ -3044,6 +3067,15 @@ int tbf_trig_partial(const float* f, float* num, float* den, int32_t B, int32_t 
     if (!num || !den) return fail(TBF_ERR_PARAM, "null num/den");
     return run_terms(f, num, den, nullptr, B, H, W, sp, terms, term_begin, term_end, batch_terms,
                      accumulate, workspace, workspace_bytes, nullptr, (cudaStream_t)stream);
+}
+
+int tbf_trig_partial_rows(const float* f, float* num, float* den, int32_t B, int32_t H, int32_t W,
+                          const tbf_spatial* sp, const tbf_terms* terms, int32_t term_begin, int32_t term_end,
+                          int32_t row_begin, int32_t row_end, int32_t batch_terms, int32_t accumulate,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+    if (!num || !den) return fail(TBF_ERR_PARAM, "null num/den");
+    return run_terms(f, num, den, nullptr, B, H, W, sp, terms, term_begin, term_end, batch_terms, accumulate,
+                     workspace, workspace_bytes, nullptr, (cudaStream_t)stream, nullptr, row_begin, row_end);
 }
 
 int tbf_finalize(const float* num, const float* den, const float* f, float* out, int64_t count,

@@ -7,10 +7,10 @@ Two ways the path shards:
 * terms  -- one huge image (config 5): the filter is a sum over independent
   frequency terms (engines.py:264-300 accumulates num/den term by term), so
   each rank accumulates partial num/den planes for its share of the terms,
-  the two planes are summed onto the root with an NCCL reduce over
-  NVLink/NVSwitch, and the root applies the guarded ratio.  Term costs are
-  not uniform (the zero frequency needs one plane, the others four), so the
-  split balances plane counts, not term counts.
+  the two planes are summed onto the root with one NCCL reduce over
+  NVLink/NVSwitch, and the root applies the guarded ratio.  Whole terms
+  would leave up to a term of imbalance, so the terms left over after an
+  even split go to every rank as a band of rows (term_shard).
 
 The reference has no distributed mode; its only parallelism is a thread pool
 over the 4 planes of one term (engines.py:262-303).
@@ -30,33 +30,57 @@ def frame_range(n_frames: int, world: int, rank: int) -> tuple[int, int]:
     return start, start + base + (1 if rank < extra else 0)
 
 
-def term_costs(n_terms: int, has_zero: bool) -> list[int]:
-    """Relative cost of each pair: planes to filter (4, or 1 for nu = 0)."""
-    return [1 if (has_zero and j == 0) else 4 for j in range(n_terms)]
+ROW_BLOCK = 128  # band granularity of tbf_trig_partial_rows (pass-2 row blocks)
+PASS1_SHARE = 0.6  # share of a term's device time in pass 1 (the part with y warm-ups), measured on config 5
 
 
-def term_range(n_terms: int, has_zero: bool, world: int, rank: int, align: int = 2) -> tuple[int, int]:
-    """Contiguous term range of `rank` with balanced plane cost.
+@dataclass
+class TermShard:
+    """One rank's share of a term-sharded filter: whole terms [t0, t1) over the
+    full image plus the leftover terms [l0, l1) over output rows [r0, r1)."""
 
-    Boundaries are multiples of `align` (the device's phasor anchor block) so
-    every rank generates bit-identical phasors; a rank may get an empty range
-    when there are fewer aligned blocks than ranks.
+    t0: int
+    t1: int
+    l0: int
+    l1: int
+    r0: int
+    r1: int
+
+
+def term_shard(n_terms: int, world: int, rank: int, height: int, warm_rows: int = 0) -> TermShard:
+    """Balanced split of n_terms pairs across `world` ranks.
+
+    Whole terms alone leave up to one term of imbalance (config 5: 60 terms on
+    8 ranks = 8 vs 7.5, +6.7%).  Here every rank takes floor(n/world)
+    consecutive terms over the whole image, and the n % world leftover terms
+    are split by rows instead: every rank filters them over its own band of
+    whole 128-row blocks (tbf_trig_partial_rows).  A band costs its rows plus
+    the y warm-ups on both sides in pass 1, so the bands are what balances.
     """
     if world < 1 or not (0 <= rank < world):
         raise ValueError(f"bad rank {rank} of {world}")
-    costs = term_costs(n_terms, has_zero)
-    nblocks = (n_terms + align - 1) // align
-    cum = [0]
-    for b in range(nblocks):
-        cum.append(cum[-1] + sum(costs[b * align:(b + 1) * align]))
-    total = cum[-1]
-    idx = [0]
-    for r in range(1, world):
-        target = total * r / world
-        lo = idx[-1]
-        idx.append(min(range(lo, nblocks + 1), key=lambda i: (abs(cum[i] - target), i)))
-    idx.append(nblocks)
-    return min(n_terms, idx[rank] * align), min(n_terms, idx[rank + 1] * align)
+    q, r = divmod(n_terms, world)
+    t0, t1 = rank * q, (rank + 1) * q
+    l0, l1 = world * q, n_terms
+    nrb = -(-height // ROW_BLOCK)
+    b0, b1 = frame_range(nrb, world, rank)
+    r0, r1 = min(height, b0 * ROW_BLOCK), min(height, b1 * ROW_BLOCK)
+    if r == 0 or r1 <= r0:
+        l0 = l1 = n_terms
+        r0 = r1 = 0
+    return TermShard(t0, t1, l0, l1, r0, r1)
+
+
+def shard_cost(sh: TermShard, height: int, warm_rows: int) -> float:
+    """Model of a rank's device time in whole-image term units: pass 1 (the
+    PASS1_SHARE of a term) sweeps a band's rows plus its warm-ups, pass 2
+    the band's rows."""
+    full = sh.t1 - sh.t0
+    if sh.l1 <= sh.l0:
+        return float(full)
+    ext = min(height, sh.r1 + warm_rows) - max(0, sh.r0 - warm_rows)
+    frac = PASS1_SHARE * ext / height + (1.0 - PASS1_SHARE) * (sh.r1 - sh.r0) / height
+    return full + (sh.l1 - sh.l0) * frac
 
 
 @dataclass
@@ -83,10 +107,12 @@ def bilateral_trig_term_sharded(f, spatial, kernel, *, partial_fn=None, finalize
     """Term-sharded filter of one image on every rank of the default group.
 
     Every rank holds the full input `f` ([B, H, W] float32).  Returns the
-    filtered image on rank 0 and None elsewhere.  `partial_fn(f, num, den,
-    t0, t1)` / `finalize_fn(num, den, f, out)` default to the device path
-    (TrigFilter); tests inject CPU implementations to exercise the
-    partitioning and the reduce with the gloo backend.
+    filtered image on rank 0 and None elsewhere.  The split is term_shard's:
+    whole terms plus a row band of the leftover terms per rank.
+    `partial_fn(f, num, den, t0, t1, rows=None, accumulate=False)` /
+    `finalize_fn(num, den, f, out)` default to the device path (TrigFilter);
+    tests inject CPU implementations to exercise the partitioning and the
+    reduce with the gloo backend.
     """
     import torch
     import torch.distributed as dist
@@ -95,28 +121,34 @@ def bilateral_trig_term_sharded(f, spatial, kernel, *, partial_fn=None, finalize
 
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     pairs = term_pairs(kernel)
-    t0, t1 = term_range(pairs.count, pairs.has_zero, world, rank)
+    H = int(f.shape[-2])
+    sh = term_shard(pairs.count, world, rank, H)
     numden = torch.zeros((2, *f.shape), dtype=f.dtype, device=f.device)
     num, den = numden[0], numden[1]
     plan_for_checks = None
     if partial_fn is None or finalize_fn is None:
         from .engines import TrigFilter
 
-        plan = TrigFilter(tuple(f.shape), spatial, kernel, term_range=(t0, t1)) if t1 > t0 else None
+        plan = TrigFilter(tuple(f.shape), spatial, kernel, term_range=(sh.t0, sh.t1)) if sh.t1 > sh.t0 else None
+        left = (TrigFilter(tuple(f.shape), spatial, kernel, term_range=(sh.l0, sh.l1))
+                if sh.l1 > sh.l0 else None)
         if plan is not None:
             plan_for_checks = plan
         elif rank == 0:  # the root finalises even without terms of its own
             plan_for_checks = TrigFilter(tuple(f.shape), spatial, kernel)
 
-        def partial_fn(f_, n_, d_, a, b):
-            if plan is not None:
-                plan.partial(f_, n_, d_, accumulate=False)
+        def partial_fn(f_, n_, d_, a, b, rows=None, accumulate=False):
+            p = plan if rows is None else left
+            if p is not None:
+                p.partial(f_, n_, d_, accumulate=accumulate, rows=rows)
 
         def finalize_fn(n_, d_, f_, o_):
             return plan_for_checks.finalize(n_, d_, f_, o_)
 
-    if t1 > t0:
-        partial_fn(f, num, den, t0, t1)
+    if sh.t1 > sh.t0:
+        partial_fn(f, num, den, sh.t0, sh.t1)
+    if sh.l1 > sh.l0:
+        partial_fn(f, num, den, sh.l0, sh.l1, rows=(sh.r0, sh.r1), accumulate=sh.t1 > sh.t0)
     reduce_numden(numden, dst=0, group=group)
     if rank != 0:
         return None

@@ -272,18 +272,27 @@ class TrigFilter:
         torch.from_numpy(dst.reshape(-1)).copy_(pin_out)
         return counts
 
-    def partial(self, f, num, den, accumulate: bool = False):
-        """num/den (+)= contribution of this plan's term range (sharded path)."""
+    def partial(self, f, num, den, accumulate: bool = False, rows=None):
+        """num/den (+)= contribution of this plan's term range (sharded path);
+        with ``rows=(r0, r1)`` only to those output rows (tbf_trig_partial_rows:
+        r0 a multiple of 128, r1 a multiple of 128 or H; recursive Gaussian)."""
         self._check_input(f)
         self._check_input(num, "num")
         self._check_input(den, "den")
         t0, t1 = self.term_range
         with self.lock, self._ctx():
-            rc = self.lib.tbf_trig_partial(
-                f.data_ptr(), num.data_ptr(), den.data_ptr(), self.B, self.H, self.W,
-                ctypes.byref(self.sp), ctypes.byref(self.terms.struct), t0, t1, self.batch_terms,
-                int(bool(accumulate)), self.workspace.data_ptr(), self.workspace.numel(),
-                self._stream())
+            if rows is None:
+                rc = self.lib.tbf_trig_partial(
+                    f.data_ptr(), num.data_ptr(), den.data_ptr(), self.B, self.H, self.W,
+                    ctypes.byref(self.sp), ctypes.byref(self.terms.struct), t0, t1, self.batch_terms,
+                    int(bool(accumulate)), self.workspace.data_ptr(), self.workspace.numel(),
+                    self._stream())
+            else:
+                rc = self.lib.tbf_trig_partial_rows(
+                    f.data_ptr(), num.data_ptr(), den.data_ptr(), self.B, self.H, self.W,
+                    ctypes.byref(self.sp), ctypes.byref(self.terms.struct), t0, t1, int(rows[0]), int(rows[1]),
+                    self.batch_terms, int(bool(accumulate)), self.workspace.data_ptr(), self.workspace.numel(),
+                    self._stream())
         _native.check(rc)
 
     def range_check(self, f):

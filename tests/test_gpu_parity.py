@@ -872,3 +872,36 @@ def test_color_parity(tb):
         seq = tb.bilateral_color(img, engine, workers=1)
         assert np.array_equal(threaded.samples, seq.samples), name
         assert float(np.max(np.abs(threaded.samples - ref))) <= TOL, name
+
+
+def test_partial_row_bands_sum_to_full(tb):
+    """tbf_trig_partial_rows (the term-sharded path's leftover terms): the
+    row bands of a term range, accumulated onto a whole-term partial, equal
+    one whole-image partial of both ranges up to the warm-up truncation
+    (bands start their y sweeps a decay length outside)."""
+    from paper_1105_4204_b200.distributed import term_shard
+    from paper_1105_4204_b200.workloads import smooth_image
+
+    f = torch.from_numpy(smooth_image(700, 333, 10, seed=4)).cuda()[None]  # 700 rows: 128-row blocks + a partial one
+    k = tb.make_trig_kernel(25.0)
+    spec = tb.SpatialSpec.gaussian_recursive(5.0)
+    n = tb.kernels.term_pairs(k).count
+    full = torch.zeros((2, *f.shape), device="cuda")
+    tb.TrigFilter(tuple(f.shape), spec, k, term_range=(0, n)).partial(f, full[0], full[1])
+    for world in (2, 3):
+        acc = torch.zeros_like(full)
+        for r in range(world):
+            sh = term_shard(n, world, r, 700)
+            if sh.t1 > sh.t0:
+                part = torch.zeros_like(full)
+                tb.TrigFilter(tuple(f.shape), spec, k, term_range=(sh.t0, sh.t1)).partial(f, part[0], part[1])
+                if sh.l1 > sh.l0:
+                    tb.TrigFilter(tuple(f.shape), spec, k, term_range=(sh.l0, sh.l1)).partial(
+                        f, part[0], part[1], accumulate=True, rows=(sh.r0, sh.r1))
+                acc += part
+        torch.cuda.synchronize()
+        err_num = float((acc[0] - full[0]).abs().max())
+        err_den = float((acc[1] - full[1]).abs().max())
+        assert err_num < 2e-3 and err_den < 1e-5, (world, err_num, err_den)
+    with pytest.raises(tb.ParameterError):
+        tb.TrigFilter(tuple(f.shape), spec, k).partial(f, full[0], full[1], rows=(64, 700))
