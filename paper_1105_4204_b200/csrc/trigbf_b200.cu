@@ -193,6 +193,7 @@ __device__ __forceinline__ long long mirror_any(long long i, long long n) {
 }
 
 
+
 // F_loc is written once (pass 1) and read once (pass 2), far apart: with
 // TBF_CACHE_HINTS its stores and loads are streaming (evict-first), so the
 // 16 B/pixel-term stream does not evict the L2-resident f tile copy,
@@ -604,6 +605,9 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     // in it).
     if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1u);
     __syncthreads();
+    // a programmatically dependent next launch (the next host strip) may
+    // start once every block of this one has got here
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     int term, stripe_r, chunk, b;
     {
         unsigned int idx = s_ticket;
@@ -2329,9 +2333,11 @@ struct P2Plan {
     int xlpt, xb1, xb2, xord;
 };
 P2Plan p2_chunk_plan(const Layout& L, const tbf_spatial* sp, int ngroups, int npart,
-                     bool hpipe) {
+                     bool hpipe, int nrb_run = -1) {
     const bool box = sp->kind == TBF_SPATIAL_BOX;
-    const int B = L.B, nrb = (L.H + P2_THREADS - 1) / P2_THREADS;
+    // 128-row blocks in flight: the whole image, or the host entry's output
+    // bands (nrb_run)
+    const int B = L.B, nrb = nrb_run > 0 ? nrb_run : (L.H + P2_THREADS - 1) / P2_THREADS;
     P2Plan pp{};
     int nchunk = 1;
     pp.warm_tiles = (std::max(sp->ext_x, 1) + TILE - 1) / TILE;
@@ -2411,15 +2417,31 @@ int p1_mode(const Layout& L, const Pass1Args& p1) {
     return (L.nyc > 1 && 10LL * L.ywarm * (L.nyc - 1) >= L.H) ? 1 : 0;
 }
 
-void launch_pass1(bool fold, int mode, dim3 grid, int smem, cudaStream_t st, const Pass1Args& p1) {
-    const dim3 blk(P1_WARPS * 32);
+// pdl: programmatic dependent launch on the previous pass-1 launch of the
+// stream (the host entry's column strips): this launch's blocks may start
+// once every block of the previous one is running (each signals at its
+// start), so strip s+1 fills the slots strip s frees instead of waiting for
+// its tail.  Safe with the x chain: strip s+1's blocks wait only for strip
+// s's, which are all resident by then.
+void launch_pass1(bool fold, int mode, dim3 grid, int smem, cudaStream_t st, const Pass1Args& p1,
+                  bool pdl = false) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(P1_WARPS * 32);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
     switch (mode * 2 + (fold ? 1 : 0)) {
-        case 0: k_pass1_gauss<false, 0><<<grid, blk, smem, st>>>(p1); break;
-        case 1: k_pass1_gauss<true, 0><<<grid, blk, smem, st>>>(p1); break;
-        case 2: k_pass1_gauss<false, 1><<<grid, blk, smem, st>>>(p1); break;
-        case 3: k_pass1_gauss<true, 1><<<grid, blk, smem, st>>>(p1); break;
-        case 4: k_pass1_gauss<false, 2><<<grid, blk, smem, st>>>(p1); break;
-        default: k_pass1_gauss<true, 2><<<grid, blk, smem, st>>>(p1); break;
+        case 0: cudaLaunchKernelEx(&cfg, k_pass1_gauss<false, 0>, p1); break;
+        case 1: cudaLaunchKernelEx(&cfg, k_pass1_gauss<true, 0>, p1); break;
+        case 2: cudaLaunchKernelEx(&cfg, k_pass1_gauss<false, 1>, p1); break;
+        case 3: cudaLaunchKernelEx(&cfg, k_pass1_gauss<true, 1>, p1); break;
+        case 4: cudaLaunchKernelEx(&cfg, k_pass1_gauss<false, 2>, p1); break;
+        default: cudaLaunchKernelEx(&cfg, k_pass1_gauss<true, 2>, p1); break;
     }
 }
 
@@ -2592,7 +2614,9 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             ev_strip.push_back(event_get());
             cudaEventRecord(ev_strip.back(), sh);
         }
-        cudaStreamWaitEvent(st, ev_strip.back(), 0);
+        // with strip-wise pass 1 the caller's stream waits for each strip's
+        // transpose instead (below), so pass 1 starts on the first strip
+        if (!(hpipe && ev_strip.size() > 1)) cudaStreamWaitEvent(st, ev_strip.back(), 0);
         if ((rc = check_cuda("host to device"))) return rc;
     }
 
@@ -2705,7 +2729,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 p1.ticket = tickets + std::min<size_t>(s, P1_MAX_LAUNCHES - 1);
                 {
                     Prof pr(KK_PASS1, st);
-                    launch_pass1(fold, p1_mode(L, p1), p1grid(p1.nst_run), p1smem, st, p1);
+                    launch_pass1(fold, p1_mode(L, p1), p1grid(p1.nst_run), p1smem, st, p1, s > 0);
                 }
             }
             p1.st0 = 0;
@@ -2837,14 +2861,27 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         if (hpipe && last && hio->bands > 1 && nrb > 1) {
             // row bands on alternating streams; each band's rows go back to the
             // host while the next band filters
-            const std::vector<int> bb = quad_split(nrb, hio->bands, false);  // in 128-row blocks
+            // equal bands (in 128-row blocks): the copy-back is about as long
+            // as the last pass 2, so it must start early and keep pace; each
+            // band's pass 2 gets x-chunks for its own (two bands') rows
+            std::vector<int> bb{0};
+            const int nbands = std::max(1, std::min(hio->bands, nrb));
+            for (int k = 1; k <= nbands; ++k) bb.push_back((int)((long long)nrb * k / nbands));
             cudaStream_t sd = aux_stream(4);
             cudaEvent_t e_c = event_get();
-            cudaEventRecord(e_c, s2);  // chain and everything before it
+            cudaEventRecord(e_c, s2);  // edge kernel and everything before it
             for (size_t k = 0; k + 1 < bb.size(); ++k) {
                 const int rb0 = bb[k], nrun = bb[k + 1] - bb[k];
                 cudaStream_t q = aux_stream(2 + (int)(k & 1));
                 cudaStreamWaitEvent(q, e_c, 0);
+                if (!box) {
+                    const P2Plan bp = p2_chunk_plan(L, sp, p2.ngroups, npart, true, 2 * nrun);
+                    nchunk = bp.nchunk;
+                    p2.tiles_per_chunk = bp.tiles_per_chunk;
+                    p2.warm_tiles = bp.warm_tiles;
+                    p2.xlpt = 0;
+                    p2.order = g_p2_order;
+                }
                 if ((rc = pass2_reduce(rb0, nrun, q))) return rc;
                 cudaEvent_t e_r = event_get();
                 cudaEventRecord(e_r, q);
@@ -3048,11 +3085,18 @@ int tbf_bilateral_trig_host(const float* h_f, float* h_out, int32_t B, int32_t H
     if (!terms) return fail(TBF_ERR_PARAM, "null terms");
     if (!h_f || !h_out || !d_io) return fail(TBF_ERR_PARAM, "null host or device buffer");
     if (B < 1 || H < 1 || W < 1) return fail(TBF_ERR_DIM, "bad shape B=%d H=%d W=%d", B, H, W);
-    // automatic split (measured on configs 1-2): one strip per 16 column tiles
-    // (2..8); 4 output bands once there are >= 8 row blocks of 128, else one
-    const int ntx = (W + TILE - 1) / TILE, nrb = (H + P2_THREADS - 1) / P2_THREADS;
-    const int strips = g_host_strips > 0 ? g_host_strips : std::max(2, std::min(8, ntx / 16));
-    const int bands = g_host_bands > 0 ? g_host_bands : (nrb >= 8 ? 4 : 1);
+    // automatic split (same-box sweeps, scripts/host_sweep.py): images of
+    // >= 8 MiB copy in column strips (pass 1 of a strip starts as it lands;
+    // more than a few strips leave each launch under-filled while the x chain
+    // serialises them) and return in row bands (the copy-back overlaps the
+    // last pass 2).  Config 2 (16 MiB): 2 strips + 4 bands 1.87 ms per call,
+    // 1 + 1 2.31 ms, 4 + 4 2.17 ms; config 5 (1 GiB): 4-8 strips and 8-24
+    // bands within 0.5%, 2 strips +3%, 12 strips +2%.
+    const int nrb = (H + P2_THREADS - 1) / P2_THREADS;
+    const size_t bytes = (size_t)B * H * W * 4;
+    const int strips = g_host_strips > 0 ? g_host_strips
+                                         : (bytes < ((size_t)8 << 20) ? 1 : (bytes < ((size_t)128 << 20) ? 2 : 4));
+    const int bands = g_host_bands > 0 ? g_host_bands : (nrb < 8 ? 1 : (bytes < ((size_t)128 << 20) ? 4 : 8));
     HostIO hio{h_f, h_out, strips, bands};
     float* d_f = d_io;
     float* d_out = d_io + (size_t)B * H * W;
