@@ -177,6 +177,12 @@ TBF_API int tbf_bilateral_direct(const float* f, int32_t B, int32_t H, int32_t W
                          int64_t n, const double* taps, int32_t radius, int32_t range_kind,
                          double range_param, int32_t degree, double* out, unsigned long long* d_counters,
                          void* stream);
+/* tbf_bilateral_direct on fp64 samples (the reference's Image planes are
+ * float64: no quantisation to fp32 before the fp64 brute force). */
+TBF_API int tbf_bilateral_direct_f64(const double* f, int32_t B, int32_t H, int32_t W, const int32_t* samples,
+                                     int64_t n, const double* taps, int32_t radius, int32_t range_kind,
+                                     double range_param, int32_t degree, double* out,
+                                     unsigned long long* d_counters, void* stream);
 
 /* Plugin-level twins of the reference's compiled core, fp64 like the
  * reference.  recursive_smooth filters along axis 0 of a[h][w] with `pad`

@@ -48,6 +48,7 @@ EXPORTS = (
     "tbf_bilateral_trig",
     "tbf_bilateral_trig_host",
     "tbf_bilateral_direct",
+    "tbf_bilateral_direct_f64",
     "tbf_trig_partial",
     "tbf_trig_partial_rows",
     "tbf_finalize",
@@ -125,6 +126,8 @@ def _declare(lib):
     lib.tbf_bilateral_direct.argtypes = [
         _vp, _i32, _i32, _i32, _vp, _i64, _vp, _i32, _i32, _f64, _i32, _vp, _vp, _vp,
     ]
+    lib.tbf_bilateral_direct_f64.restype = ctypes.c_int
+    lib.tbf_bilateral_direct_f64.argtypes = lib.tbf_bilateral_direct.argtypes
     lib.tbf_trig_partial.restype = ctypes.c_int
     lib.tbf_trig_partial.argtypes = [
         _vp, _vp, _vp, _i32, _i32, _i32, ctypes.POINTER(TbfSpatial), ctypes.POINTER(TbfTerms),

@@ -1720,7 +1720,8 @@ __global__ void k_recursive_smooth_f64(const double* a, double* out, int h, int 
 // (= trig_eval, kernels.py:161-171).
 constexpr int BF_THREADS = 256;
 
-__global__ void __launch_bounds__(BF_THREADS) k_bilateral_direct(const float* f, int B, int H, int W,
+template <typename T>
+__global__ void __launch_bounds__(BF_THREADS) k_bilateral_direct(const T* f, int B, int H, int W,
                                                                 const int32_t* samples, long long n,
                                                                 const double* taps, int r, int kind,
                                                                 double param, int degree, double* out,
@@ -1738,7 +1739,7 @@ __global__ void __launch_bounds__(BF_THREADS) k_bilateral_direct(const float* f,
             y = (int)(rem / W);
             x = (int)(rem - (long long)y * W);
         }
-        const float* F = f + (size_t)b * H * W;
+        const T* F = f + (size_t)b * H * W;
         const double c = (double)F[(size_t)y * W + x];
         const int win = 2 * r + 1;
         const long long taps2 = (long long)win * win;
@@ -2914,6 +2915,24 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
     return TBF_OK;
 }
 
+template <typename T>
+int bilateral_direct_impl(const T* f, int32_t B, int32_t H, int32_t W, const int32_t* samples, int64_t n,
+                          const double* taps, int32_t radius, int32_t range_kind, double range_param,
+                          int32_t degree, double* out, unsigned long long* d_counters, void* stream) {
+    if (B < 1 || H < 1 || W < 1) return fail(TBF_ERR_DIM, "bad shape B=%d H=%d W=%d", B, H, W);
+    if (radius < 0 || !taps) return fail(TBF_ERR_PARAM, "bad window (radius %d)", radius);
+    if (range_kind != 0 && range_kind != 1) return fail(TBF_ERR_PARAM, "unknown range kind %d", range_kind);
+    if (range_kind == 0 && !(range_param > 0.0)) return fail(TBF_ERR_PARAM, "sigma_r must be positive");
+    if (range_kind == 1 && degree < 0) return fail(TBF_ERR_PARAM, "degree must be >= 0");
+    const long long count = samples ? (long long)n : (long long)B * H * W;
+    if (count <= 0) return fail(TBF_ERR_DIM, "no output pixels");
+    const unsigned grid = (unsigned)std::min<long long>(count, 148LL * 16);
+    k_bilateral_direct<T><<<grid, BF_THREADS, 0, (cudaStream_t)stream>>>(
+        f, B, H, W, samples, count, taps, radius, range_kind, range_param, degree, out,
+        d_counters ? d_counters + 1 : nullptr);
+    return check_cuda("bilateral_direct");
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -3144,22 +3163,21 @@ int tbf_recursive_smooth_f64(const double* a, double* out, int32_t h, int32_t w,
     return check_cuda("recursive_smooth_f64");
 }
 
+
 int tbf_bilateral_direct(const float* f, int32_t B, int32_t H, int32_t W, const int32_t* samples,
                          int64_t n, const double* taps, int32_t radius, int32_t range_kind,
                          double range_param, int32_t degree, double* out, unsigned long long* d_counters,
                          void* stream) {
-    if (B < 1 || H < 1 || W < 1) return fail(TBF_ERR_DIM, "bad shape B=%d H=%d W=%d", B, H, W);
-    if (radius < 0 || !taps) return fail(TBF_ERR_PARAM, "bad window (radius %d)", radius);
-    if (range_kind != 0 && range_kind != 1) return fail(TBF_ERR_PARAM, "unknown range kind %d", range_kind);
-    if (range_kind == 0 && !(range_param > 0.0)) return fail(TBF_ERR_PARAM, "sigma_r must be positive");
-    if (range_kind == 1 && degree < 0) return fail(TBF_ERR_PARAM, "degree must be >= 0");
-    const long long count = samples ? (long long)n : (long long)B * H * W;
-    if (count <= 0) return fail(TBF_ERR_DIM, "no output pixels");
-    const unsigned grid = (unsigned)std::min<long long>(count, 148LL * 16);
-    k_bilateral_direct<<<grid, BF_THREADS, 0, (cudaStream_t)stream>>>(
-        f, B, H, W, samples, count, taps, radius, range_kind, range_param, degree, out,
-        d_counters ? d_counters + 1 : nullptr);
-    return check_cuda("bilateral_direct");
+    return bilateral_direct_impl(f, B, H, W, samples, n, taps, radius, range_kind, range_param, degree, out,
+                                 d_counters, stream);
+}
+
+int tbf_bilateral_direct_f64(const double* f, int32_t B, int32_t H, int32_t W, const int32_t* samples,
+                             int64_t n, const double* taps, int32_t radius, int32_t range_kind,
+                             double range_param, int32_t degree, double* out, unsigned long long* d_counters,
+                             void* stream) {
+    return bilateral_direct_impl(f, B, H, W, samples, n, taps, radius, range_kind, range_param, degree, out,
+                                 d_counters, stream);
 }
 
 int tbf_box_pass_f64(const double* a, double* out, int32_t h, int32_t w, int32_t radius,

@@ -533,14 +533,18 @@ def bilateral_direct(img, spatial, range_fn, *, samples=None,
         if not isinstance(sigma, (int, float)) or sigma <= 0:
             raise ParameterError("range_fn must be a TrigKernel, a GaussianRange or a positive sigma")
         kind, param, degree = 0, float(sigma), 0
+    # float64 inputs (an Image's planes, float64 arrays / tensors) stay float64:
+    # the brute force then sees the reference's exact samples
     if isinstance(img, Image):
         if img.channels != 1:
             raise DimensionError(f"engine expects a single-channel image, got {img.channels} channels")
-        f = torch.from_numpy(np.ascontiguousarray(img.samples[0], dtype=np.float32)).cuda()
+        f = torch.from_numpy(np.ascontiguousarray(img.samples[0], dtype=np.float64)).cuda()
     elif isinstance(img, np.ndarray):
-        f = torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32)).cuda()
+        dt = np.float64 if img.dtype == np.float64 else np.float32
+        f = torch.from_numpy(np.ascontiguousarray(img, dtype=dt)).cuda()
     elif isinstance(img, torch.Tensor):
-        f = img.to(device="cuda" if not img.is_cuda else img.device, dtype=torch.float32).contiguous()
+        dt = torch.float64 if img.dtype == torch.float64 else torch.float32
+        f = img.to(device="cuda" if not img.is_cuda else img.device, dtype=dt).contiguous()
     else:
         raise DimensionError(f"unsupported input type {type(img).__name__}")
     if f.dim() not in (2, 3):
@@ -566,7 +570,8 @@ def bilateral_direct(img, spatial, range_fn, *, samples=None,
         out = torch.empty((B, H, W), dtype=torch.float64, device=f.device)
         n = B * H * W
     stream = torch.cuda.current_stream(f.device).cuda_stream
-    _native.check(lib.tbf_bilateral_direct(
+    entry = lib.tbf_bilateral_direct_f64 if f.dtype == torch.float64 else lib.tbf_bilateral_direct
+    _native.check(entry(
         f.data_ptr(), B, H, W, d_s.data_ptr() if d_s is not None else None, n, taps.data_ptr(),
         radius, kind, param, degree, out.data_ptr(), counters.data_ptr(), stream))
     guarded = int(counters[1].item())  # syncs

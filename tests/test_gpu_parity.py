@@ -380,6 +380,13 @@ def test_bilateral_direct_matches_oracle(tb, orc, kind, param, range_kind):
         ys, xs = rng.integers(0, h, 9), rng.integers(0, w, 9)
         smp = tb.bilateral_direct(f, spec, rk, samples=np.stack([ys, xs], 1))
         np.testing.assert_array_equal(smp, got[ys, xs])
+        # float64 input (non-integer samples) is not quantised to fp32 first
+        f64 = rng.uniform(0, 255, (h, w))
+        got64 = tb.bilateral_direct(f64, spec, rk)
+        assert got64.dtype == np.float64
+        assert np.max(np.abs(got64 - orc.bilateral_direct(f64, kind, param, rf))) < 1e-9, (h, w)
+        img = tb.Image(w, h, 1, f64[None])
+        assert np.max(np.abs(tb.bilateral_direct(img, spec, rk).plane(0) - got64)) == 0.0
 
 
 def test_trig_matches_direct_trig(tb):
