@@ -228,6 +228,10 @@ TBF_API int32_t tbf_profile_timeline(double* start_ms, double* dur_ms, int32_t* 
                                 x-chunks of unequal size, dispatched costliest first, planned by a
                                 list-scheduling model; 0 = equal chunks */
 #define TBF_OPT_P2_ORDER 9  /* block order of the block-summed pass 2: 0 (default) row fastest, 1 x-chunk fastest, 2/3 reversed */
+#define TBF_OPT_ZERO_UNIT 12 /* 1: the zero frequency (even N) as one packed unit whose four lanes
+                                are f at four row quarters (a quarter of a term's work and bytes;
+                                engines.py:265-271 filters f alone there), on a side stream;
+                                default 0 (a full term): measured 1-20% slower end to end */
 #define TBF_OPT_P1_FOLD 6   /* default 1: folds the y-sweep gain into the pass-2 weights
                                (skips 4 multiplies per pixel-term in pass 1 when T/g^4 is safe); 0 scales in pass 1 */
 TBF_API int tbf_set_option(int32_t option, int64_t value);

@@ -472,6 +472,9 @@ struct Pass1Args {
     int Ex, ne, edge_all, ntx;
     int nst;           // stripes of P1_WARPS column tiles (one pass-1 block each, per term)
     int st0, nst_run;  // stripes [st0, st0 + nst_run) in this launch
+    int term0, nterm;  // terms [term0, term0 + nterm) of the batch in this launch
+    int hq;            // zero unit (ZU launch): virtual rows = row quarters of 32-row segments
+    int zyc, zrows;    // ... in y-chunks of zrows virtual rows
     Casc k;
     TermDev t;
     // Gaussian layouts (float4 = the 4 planes of one term, or the 4 states
@@ -513,7 +516,8 @@ struct Pass2Args {
     int B, H, W, ntx;
     Casc k;
     TermDev t;
-    int ngroups;       // ceil(t.n / G2)
+    int ngroups;       // ceil((t.n - term0) / G2)
+    int term0;         // first term of the batch in this launch
     float wscale;      // g^2: undoes the two pure x sweeps (1 for box)
     int rb0, nrb_run;     // 128-row blocks [rb0, rb0 + nrb_run) in this launch
     int tiles_per_chunk;  // x-chunking of rows (gauss); == ntx for one chunk
@@ -546,6 +550,24 @@ struct ReduceArgs {
     float* out;           // [B][H][W] guarded ratio when non-null
     unsigned long long* counters;
     int i_base;           // first row of this launch (multiple of RED_I)
+    const float* zpart;   // zero unit's num plane (x-major) added last when non-null
+    float den_add;        // ... with its den, w0 exactly (engines.py:270)
+};
+
+// Pass 2 of the zero unit (k_pass2_zero): the x backward of its four row
+// quarters and num at the image rows; den is w0, added by the reduce.
+struct ZeroArgs {
+    int B, H, W, ntx, hq;
+    int term;             // the unit's term slot in the batch
+    Casc k;
+    int tiles_per_chunk, warm_tiles;
+    float wt;             // w0 * wscale
+    const float* floc;
+    int nHx;
+    const float4* Hx;
+    const float* s0;
+    const float* bstate;
+    float* num;           // x-major plane (xm_index) of image rows
 };
 
 // ---------------------------------------------------------------------------
@@ -588,7 +610,15 @@ __device__ __forceinline__ void p1_fwd8(const float (&fv)[8], float nu_hi, float
 // chunks (LPT bounds + the same warm-up reads).  Separate instantiations keep
 // each one's register allocation: the warm-up fast path cost config 3 (one
 // chunk) 0.8% through register pressure while gaining 2.5% on config 2.
-template <bool FOLD, int MODE>
+// ZU: the zero-frequency term as one packed unit (engines.py:
+// 265-271): nu = 0 needs only F[f] (den += w0 exactly), so the unit's four
+// float4 lanes carry f itself at four row quarters (virtual row v, plane p =
+// image row v + p*hq) instead of (cos, sin, f cos, f sin) of one row: a
+// quarter of a term's sweeps and bytes.  Plane 0 starts at the exact mirror
+// extension, planes 1-3 a decay length Ey >= K above their quarter (rows of
+// the image), plane 3 runs on past the image into a general reflection that
+// the backward start forgets within K.
+template <bool FOLD, int MODE, bool ZU = false>
 __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss(const __grid_constant__ Pass1Args a) {
     constexpr bool LPT = MODE == 2;
     extern __shared__ float smem[];
@@ -611,10 +641,16 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     int term, stripe_r, chunk, b;
     {
         unsigned int idx = s_ticket;
-        term = (int)(idx % (unsigned)a.t.n);
-        idx /= (unsigned)a.t.n;
-        chunk = (int)(idx % (unsigned)a.nyc);
-        idx /= (unsigned)a.nyc;
+        if (ZU) {  // one term; y-chunks of the virtual rows
+            term = a.term0;
+            chunk = (int)(idx % (unsigned)a.zyc);
+            idx /= (unsigned)a.zyc;
+        } else {
+            term = a.term0 + (int)(idx % (unsigned)a.nterm);
+            idx /= (unsigned)a.nterm;
+            chunk = (int)(idx % (unsigned)a.nyc);
+            idx /= (unsigned)a.nyc;
+        }
         b = (int)(idx % (unsigned)a.B);
         stripe_r = (int)(idx / (unsigned)a.B);
     }
@@ -634,7 +670,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     float4* const buf = reinterpret_cast<float4*>(smem) + (size_t)warp * TILE * BUF_LD;
     float4* const bl = buf + lane;           // own column (phases A/B)
     float4* const br = buf + lane * BUF_LD;  // own row (epilogue)
-    const float nu_hi = a.t.nu_hi[term], nu_lo = a.t.nu_lo[term];
+    const float nu_hi = ZU ? 0.f : a.t.nu_hi[term], nu_lo = ZU ? 0.f : a.t.nu_lo[term];
     const Casc k = a.k;
     const int Ey = a.Ey;
     const int iend = H + Ey;  // forward runs over extended rows [-Ey, H+Ey)
@@ -653,12 +689,30 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
         if (MODE == 0) return __ldg(a.fY + ty_index(b, xc, mirror1(i, H), W, H));
         return __ldg(frow(mirror1(i, H)));
     };
+    // the four plane inputs at (extended / virtual) row i
+    auto modrow = [&](int i, float (&u)[4]) {
+        if (ZU) {  // rows i + p*hq of the image, one reflection at either end
+#pragma unroll
+            for (int p = 0; p < 4; ++p) u[p] = __ldg(frow(mirror1(i + p * a.hq, H)));
+        } else {
+            const float fs = fload(i);
+            float s0, c0;
+            sincos_fma(phase(nu_hi, nu_lo, fs), &s0, &c0);
+            u[0] = c0;
+            u[1] = s0;
+            u[2] = fs * c0;
+            u[3] = fs * s0;
+        }
+    };
     // y-chunk: output rows [R0, R1).  The forward sweep starts at A0 = R0 -
     // ywarm from a steady-state guess (exact -Ey start for the top chunk); the
     // backward starts at Bend = R1 + ywarm (exact H+Ey end for the bottom
     // chunk).  ywarm >= the decay length K, so guesses fade below eps.
     int R0, R1;
-    if (LPT) {
+    if (ZU) {
+        R0 = chunk * a.zrows;
+        R1 = min(a.hq, R0 + a.zrows);
+    } else if (LPT) {
         R0 = chunk == 0 ? 0 : (chunk == 1 ? a.yb1 : a.yb2);
         R1 = chunk == 0 ? a.yb1 : (chunk == 1 ? a.yb2 : H);
     } else {
@@ -666,7 +720,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
         R1 = min(a.row1, R0 + a.ych_rows);
     }
     const int A0 = R0 - a.ywarm <= 0 ? -Ey : R0 - a.ywarm;
-    const int Bend = R1 + a.ywarm >= iend ? iend : R1 + a.ywarm;
+    const int Bend = ZU ? (R1 + a.ywarm >= a.hq + Ey ? a.hq + Ey : R1 + a.ywarm)
+                        : (R1 + a.ywarm >= iend ? iend : R1 + a.ywarm);
     // checkpoints: float4 per plane, [chunk*nseg + local seg][term][b][x][4]
     const size_t cks = (size_t)a.t.n * a.B * W * 4;  // float4 stride between segments
     float4* const ck0 = reinterpret_cast<float4*>(a.ckpt) +
@@ -674,24 +729,39 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
 
     float v1[4], v2[4], y1[4], y2[4];
     {
-        const float f0 = fload(A0);
-        float s0, c0;
-        sincos_fma(phase(nu_hi, nu_lo, f0), &s0, &c0);
-        const float u[4] = {c0, s0, f0 * c0, f0 * s0};
+        float u[4];
+        modrow(A0, u);
 #pragma unroll
         for (int p = 0; p < 4; ++p) csteady(u[p], v1[p], v2[p], y1[p], y2[p], k);
     }
 
     // ---- phase A: forward sweep, double-buffered 8-row blocks ----
     auto step1 = [&](int i) {
-        const float fs = fload(i);
-        float s0, c0;
-        sincos_fma(phase(nu_hi, nu_lo, fs), &s0, &c0);
-        const float u[4] = {c0, s0, fs * c0, fs * s0};
+        float u[4];
+        modrow(i, u);
 #pragma unroll
         for (int p = 0; p < 4; ++p) cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
     };
-    if (MODE > 0 && A0 >= 0) {
+    if (ZU) {  // lead-in in 8-row blocks, the next block's loads in flight
+        float cur[8][4], nxt[8][4];
+        int i = A0;
+        for (; i < A0 + ((R0 - A0) & 7); ++i) step1(i);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) modrow(i + q, cur[q]);
+#pragma unroll 1
+        for (; i < R0; i += 8) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) modrow(i + 8 + q, nxt[q]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+#pragma unroll
+                for (int p = 0; p < 4; ++p) cstep(cur[q][p], v1[p], v2[p], y1[p], y2[p], k);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+#pragma unroll
+                for (int p = 0; p < 4; ++p) cur[q][p] = nxt[q][p];
+        }
+    } else if (MODE > 0 && A0 >= 0) {
         // interior chunk: the warm-up rows [A0, R0) are whole 32-row tiles of
         // fY (both multiples of 32): 8-row blocks at immediate offsets, one
         // pointer step per block instead of a mirrored, clamped index per row
@@ -751,8 +821,10 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     const int nseg = (Bend - R0 + TILE - 1) / TILE;  // local segments of this chunk
     const int nsteps = 2 * nseg;
     float seg_f[TILE];
+    if (!ZU) {
 #pragma unroll
-    for (int q = 0; q < TILE; ++q) seg_f[q] = fload(R0 + q);
+        for (int q = 0; q < TILE; ++q) seg_f[q] = fload(R0 + q);
+    }
 #pragma unroll 1
     for (int step = 0; step < nsteps; ++step) {
         const bool phaseB = step >= nseg;
@@ -768,8 +840,8 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
         // forward (in-place refill below), its checkpoint (phase B) after it
         const int ns = step + 1 < nseg ? step + 1 : max(nsteps - 2 - step, 0);
         const int rn = R0 + ns * TILE;
-        const bool nfast = rn >= 0 && rn + TILE <= H;  // next segment: one whole fY tile
-        const bool full = step != nseg && len == TILE;
+        const bool nfast = !ZU && rn >= 0 && rn + TILE <= H;  // next segment: one whole fY tile
+        const bool full = !ZU && step != nseg && len == TILE;
         // forward over the segment into the smem tile (own column), 4 x 8
         // samples; the first phase-B step finds the tile already filled by the
         // last phase-A step.  In-place refill: after each 8-row block has
@@ -787,13 +859,36 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                     for (int q = q0; q < q0 + 8; ++q) seg_f[q] = ldg_pinned(fpn + q * 32);
                 }
             }
+        } else if (ZU) {
+            if (step != nseg) {
+                // 8-row blocks, the next block's 32 loads in flight meanwhile
+                float cur[8][4], nxt[8][4];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) modrow(i0 + q, cur[q]);
+#pragma unroll 1
+                for (int r0 = 0; r0 < len; r0 += 8) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) modrow(min(i0 + r0 + 8 + q, Bend - 1), nxt[q]);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        if (r0 + q < len) {
+                            float o[4];
+#pragma unroll
+                            for (int p = 0; p < 4; ++p) o[p] = cstep(cur[q][p], v1[p], v2[p], y1[p], y2[p], k);
+                            bl[(r0 + q) * BUF_LD] = make_float4(o[0], o[1], o[2], o[3]);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+#pragma unroll
+                        for (int p = 0; p < 4; ++p) cur[q][p] = nxt[q][p];
+                }
+            }
         } else {
             if (step != nseg) {
                 for (int r = 0; r < len; ++r) {
-                    const float fs = fload(i0 + r);
-                    float s0, c0;
-                    sincos_fma(phase(nu_hi, nu_lo, fs), &s0, &c0);
-                    const float u[4] = {c0, s0, fs * c0, fs * s0};
+                    float u[4];
+                    modrow(i0 + r, u);
                     float o[4];
 #pragma unroll
                     for (int p = 0; p < 4; ++p) o[p] = cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
@@ -805,7 +900,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                 for (int q = 0; q < TILE; ++q) seg_f[q] = ldg_pinned(fpn + q * 32);
             }
         }
-        if (!nfast) {  // boundary segments (mirror extension): generic loads
+        if (!ZU && !nfast) {  // boundary segments (mirror extension): generic loads
 #pragma unroll
             for (int q = 0; q < TILE; ++q) seg_f[q] = fload(rn + q);
         }
@@ -1284,7 +1379,9 @@ __global__ void __launch_bounds__(32 * P2R_GR, TBF_P2_MINB) k_pass2_gr(const __g
     const bool active = grp_raw < a.ngroups;
     const int grp = active ? grp_raw : a.ngroups - 1;
     const int b = blockIdx.z;
-    const int j0 = grp * G;
+    // terms [term0, t.n) of the batch (term0 = 1 when the zero unit has its
+    // own pass 2)
+    const int j0 = a.term0 + grp * G;
     const int nt = min(G, a.t.n - j0);
     P2Ctx<G> c;
 #pragma unroll
@@ -1375,6 +1472,97 @@ __global__ void __launch_bounds__(32 * P2R_GR, TBF_P2_MINB) k_pass2_gr(const __g
             }
         }
         if (TBF_P2_NBUF == 1) __syncthreads();  // reads done before the next tile's stores
+    }
+}
+
+// Zero unit, pass 2: thread = virtual row v (planes p = image rows v + p*hq),
+// tiles right to left from the exact backward start (rightmost chunk) or a
+// warm-up; F + Hx . S0 near x = 0 as in k_pass2_gr; no phasors (nu = 0).
+__global__ void __launch_bounds__(128) k_pass2_zero(const __grid_constant__ ZeroArgs a) {
+    const int v = blockIdx.x * 128 + threadIdx.x;
+    if (v >= a.hq) return;
+    const int chunk = blockIdx.y, b = blockIdx.z;
+    const int H = a.H, W = a.W;
+    const Casc k = a.k;
+    const int nrbk = (H + FL_RB - 1) / FL_RB;
+    const float4* fl = reinterpret_cast<const float4*>(a.floc) +
+                       (((size_t)a.term * a.B + b) * nrbk + v / FL_RB) * W * (size_t)FL_RB + (v % FL_RB);
+    const float4* s0 = reinterpret_cast<const float4*>(a.s0) + (((size_t)a.term * a.B + b) * H + v) * 4;
+    auto fwd = [&](int x, float (&F)[4]) {
+        const float4 t = ld_stream(fl + (size_t)x * FL_RB);
+        F[0] = t.x;
+        F[1] = t.y;
+        F[2] = t.z;
+        F[3] = t.w;
+        if (x < a.nHx) {
+            const float4 h = __ldg(a.Hx + x);
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const float4 c = s0[p];
+                F[p] = fmaf(h.x, c.x, fmaf(h.y, c.y, fmaf(h.z, c.z, fmaf(h.w, c.w, F[p]))));
+            }
+        }
+    };
+    const int t_lo = chunk * a.tiles_per_chunk;
+    const int t_hi = min(a.ntx, t_lo + a.tiles_per_chunk);
+    float p1[4], p2[4], q1[4], q2[4];
+    int xs;
+    if (t_hi + a.warm_tiles >= a.ntx) {  // exact start at the right edge
+        const float4* bs = reinterpret_cast<const float4*>(a.bstate) + (((size_t)a.term * a.B + b) * H + v) * 4;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const float4 c = bs[p];
+            p1[p] = c.x;
+            p2[p] = c.y;
+            q1[p] = c.z;
+            q2[p] = c.w;
+        }
+        xs = W - 1;
+    } else {  // warm-up from the steady state of the forward output
+        xs = min(W - 1, (t_hi + a.warm_tiles) * TILE - 1);
+        float F[4];
+        fwd(xs, F);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) csteady(F[p], p1[p], p2[p], q1[p], q2[p], k);
+    }
+    const int xo = min(W, t_hi * TILE);  // outputs for x < xo
+    const int xlo = t_lo * TILE;
+    // 4-step blocks, the next block's loads in flight meanwhile
+    float4 cur[4], nxt[4];
+    auto load4 = [&](int xb, float4 (&d)[4]) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) d[q] = ld_stream(fl + (size_t)max(xb - q, xlo) * FL_RB);
+    };
+    load4(xs, cur);
+#pragma unroll 1
+    for (int xb = xs; xb >= xlo; xb -= 4) {
+        load4(xb - 4, nxt);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int x = xb - q;
+            if (x < xlo) break;
+            float F[4] = {cur[q].x, cur[q].y, cur[q].z, cur[q].w};
+            if (x < a.nHx) {
+                const float4 h = __ldg(a.Hx + x);
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const float4 c = s0[p];
+                    F[p] = fmaf(h.x, c.x, fmaf(h.y, c.y, fmaf(h.z, c.z, fmaf(h.w, c.w, F[p]))));
+                }
+            }
+            float y[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) y[p] = cstep(F[p], p1[p], p2[p], q1[p], q2[p], k);
+            if (x < xo) {
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const int r = v + p * a.hq;
+                    if (r < H) a.num[xm_index(b, x, r, W, H)] = a.wt * y[p];
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
     }
 }
 
@@ -1575,6 +1763,11 @@ __global__ void __launch_bounds__(256) k_reduce(const __grid_constant__ ReduceAr
                     n[0] += vn.x; n[1] += vn.y; n[2] += vn.z; n[3] += vn.w;
                     d[0] += vd.x; d[1] += vd.y; d[2] += vd.z; d[3] += vd.w;
                 }
+                if (a.zpart) {  // the zero unit last (fixed order)
+                    const float4 vn = *reinterpret_cast<const float4*>(a.zpart + xm_index(b, gx, gi, a.W, a.H));
+                    n[0] += vn.x; n[1] += vn.y; n[2] += vn.z; n[3] += vn.w;
+                    d[0] += a.den_add; d[1] += a.den_add; d[2] += a.den_add; d[3] += a.den_add;
+                }
             } else {
                 const int cnt = min(4, a.H - gi);
                 for (int g = 0; g < a.ngroups; ++g)
@@ -1582,6 +1775,10 @@ __global__ void __launch_bounds__(256) k_reduce(const __grid_constant__ ReduceAr
                         n[q] += pp[(size_t)(2 * g) * plane + q];
                         d[q] += pp[(size_t)(2 * g + 1) * plane + q];
                     }
+                for (int q = 0; a.zpart && q < cnt; ++q) {
+                    n[q] += a.zpart[xm_index(b, gx, gi, a.W, a.H) + q];
+                    d[q] += a.den_add;
+                }
             }
         }
 #pragma unroll
@@ -1828,6 +2025,7 @@ size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 struct Layout {
     int B, H, W, Ey, Ex, nseg, ntx, ne, edge_all;
     int row0, row1;  // output rows (a band for the term-sharded leftover terms, else [0, H))
+    int zhq;         // zero unit: virtual rows (a quarter of H in whole 32-row segments)
     int nst;  // stripes of P1_WARPS column tiles (pass-1 blocks per term and y-chunk)
     int nyc, ych_rows, ywarm;  // pass-1 y-chunking (nseg = checkpoint segments per chunk)
     int ychb[TBF_MAX_YCH + 1];  // chunk boundaries (ych_rows = the largest chunk)
@@ -1855,6 +2053,8 @@ int g_auto_batches = 2; // tbf_set_option(TBF_OPT_BATCHES): batches when batch_t
 int g_p2_order = 0;     // tbf_set_option(TBF_OPT_P2_ORDER): block order of the block-summed pass 2 (same-box A/B: orders 0 and 1 equal)
 int g_host_strips = 0;  // tbf_set_option(TBF_OPT_HOST_STRIPS): column strips of the host input (0 auto)
 int g_host_bands = 0;   // tbf_set_option(TBF_OPT_HOST_BANDS): row bands of the host output (0 auto)
+int g_zero_unit = 0;    // tbf_set_option(TBF_OPT_ZERO_UNIT): the zero frequency as a packed 1-plane unit
+                        // (measured slower end to end: off by default)
 
 // Pass-1 y-chunk planner for launches of a few waves.  Blocks of one chunk
 // level all cost the same; the levels are dispatched largest first (block
@@ -2115,6 +2315,9 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
         }
     }
     L->nseg = (L->ych_rows + std::max(L->ywarm, L->Ey) + TILE - 1) / TILE + 1;
+    // the zero unit's chunk: the virtual rows (row quarters) plus Ey both ways
+    L->zhq = ((H + 3) / 4 + TILE - 1) / TILE * TILE;
+    if (!box) L->nseg = std::max(L->nseg, (L->zhq + 2 * L->Ey + TILE - 1) / TILE + 1);
     const size_t px = (size_t)B * H * W;
     size_t o = 0;
     L->off_fT = o;
@@ -2144,8 +2347,8 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     if (!box) q = align_up(q + (size_t)tb * 16 * B * H * 4);
     L->s_bst = q;
     if (!box) q = align_up(q + (size_t)tb * 16 * B * H * 4);
-    L->s_part = q;
-    q = align_up(q + (size_t)L->ng2 * 2 * xm_plane(B, W, H) * 4);
+    L->s_part = q;  // the group blocks' (num, den) pairs, then the zero unit's num plane
+    q = align_up(q + ((size_t)L->ng2 + 1) * 2 * xm_plane(B, W, H) * 4);
     L->slot_bytes = q;
     L->off_slot = o;
     o += (size_t)L->nslot * q;
@@ -2155,8 +2358,8 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
 
 // Internal streams per device: 0 = pipelined batches, 1 = host->device
 // copies, 2/3 = pass-1 strips and pass-2 bands of the host pipeline, 4 =
-// device->host copies.
-constexpr int N_AUX = 5;
+// device->host copies, 5 = the zero unit's passes.
+constexpr int N_AUX = 6;
 cudaStream_t aux_stream(int idx = 0) {
     static std::mutex mu;
     static cudaStream_t streams[64][N_AUX] = {};
@@ -2318,6 +2521,8 @@ void set_p1_smem() {
     cudaFuncSetAttribute(k_pass1_gauss<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
     cudaFuncSetAttribute(k_pass1_gauss<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
     cudaFuncSetAttribute(k_pass1_gauss<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
+    cudaFuncSetAttribute(k_pass1_gauss<false, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
+    cudaFuncSetAttribute(k_pass1_gauss<true, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P1_SMEM_OCC2);
     cudaFuncSetAttribute(k_pass1_box<G1, R_ANCHOR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          P1_SMEM);
     done_mask[dev >> 6] |= 1ull << (dev & 63);
@@ -2444,6 +2649,13 @@ void launch_pass1(bool fold, int mode, dim3 grid, int smem, cudaStream_t st, con
         case 4: cudaLaunchKernelEx(&cfg, k_pass1_gauss<false, 2>, p1); break;
         default: cudaLaunchKernelEx(&cfg, k_pass1_gauss<true, 2>, p1); break;
     }
+}
+
+void launch_pass1_zero(bool fold, dim3 grid, int smem, cudaStream_t st, const Pass1Args& p1) {
+    if (fold)
+        k_pass1_gauss<true, 0, true><<<grid, P1_WARPS * 32, smem, st>>>(p1);
+    else
+        k_pass1_gauss<false, 0, true><<<grid, P1_WARPS * 32, smem, st>>>(p1);
 }
 
 // Core driver: pairs [tbeg, tend) in batches of L.tb terms.  Either
@@ -2667,6 +2879,15 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         td.dnu = (float)terms->dnu;
         td.n = n;
         td.anchor = R_ANCHOR;
+        // the zero frequency (first pair of an even N) as the packed 1-plane
+        // unit: its own pass 1 (k_pass1_gauss<.., ZU>) and pass 2
+        // (k_pass2_zero) on a side stream; the main launches take the rest.
+        // Needs every row quarter's warm-up inside the image (Ey = K <= hq)
+        const bool zu = !box && !band && g_zero_unit && jb == 0 && terms->nu[tbeg] == 0.0 && H >= 4 * TILE &&
+                        L.Ey == sp->ext_y && L.Ey <= L.zhq && H >= L.Ey + 4 * TILE;
+        const int term0 = zu ? 1 : 0;
+        const int nmain = n - term0;
+        cudaStream_t zs = zu ? aux_stream(5) : nullptr;
 
         Pass1Args p1;
         p1.f = f;
@@ -2691,6 +2912,15 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p1.nst = L.nst;
         p1.st0 = 0;
         p1.nst_run = L.nst;
+        p1.term0 = term0;
+        p1.nterm = nmain;
+        p1.hq = L.zhq;
+        // the zero unit's virtual rows in chunks about as long as the main
+        // ones (its blocks then run beside the main pass 1), at most nyc
+        // (checkpoint slots)
+        p1.zyc = std::max(1, std::min(L.nyc, (L.zhq + std::max(L.ych_rows, L.ywarm) - 1) / std::max(L.ych_rows, L.ywarm)));
+        p1.zrows = ((L.zhq + p1.zyc - 1) / p1.zyc + TILE - 1) / TILE * TILE;
+        p1.zyc = (L.zhq + p1.zrows - 1) / p1.zrows;
         p1.k = kc;
         p1.t = td;
         p1.ckpt = ckpt;
@@ -2704,10 +2934,26 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         const dim3 gbox(L.ntx, (n + P1_WARPS - 1) / P1_WARPS, B);
         // Gaussian: 1-D grid, blocks map to (stripe, frame, y-chunk, term) by a
         // dispatch ticket; one counter per launch after the flags
-        auto p1grid = [&](int nst_run) { return dim3(nst_run * B * L.nyc * n, 1, 1); };
+        auto p1grid = [&](int nst_run) { return dim3(nst_run * B * L.nyc * nmain, 1, 1); };
         const int p1smem = g_p1_occ == 2 ? P1_SMEM_OCC2 : P1_SMEM_GAUSS;
         if (!box) cudaMemsetAsync(flags, 0, (nflags + P1_MAX_LAUNCHES) * sizeof(int), st);
-        if (strip_p1 && bi == 0) {
+        cudaEvent_t e_zu_ready = nullptr;
+        if (zu) {  // flags cleared (and, without host strips, f transposed)
+            e_zu_ready = event_get();
+            cudaEventRecord(e_zu_ready, st);
+        }
+        if (strip_p1 && bi == 0 && nmain == 0) {
+            // only the zero unit: the whole input must be in before it starts
+            for (size_t s = 0; s < ev_strip.size(); ++s) {
+                const int t0 = sb[s] * P1_WARPS, t1 = std::min(L.ntx, sb[s + 1] * P1_WARPS);
+                dim3 tg(t1 - t0, (H + TILE - 1) / TILE, B);
+                cudaStreamWaitEvent(st, ev_strip[s], 0);
+                Prof pr(KK_TRANSPOSE, st);
+                k_transpose<<<tg, 256, 0, st>>>(f, fT, fY, H, W, -1e-9, terms->T + 1e-9, rc_counters, t0);
+            }
+            e_zu_ready = event_get();
+            cudaEventRecord(e_zu_ready, st);
+        } else if (strip_p1 && bi == 0) {
             // strip s: transpose (+ range check) on a side stream as soon as
             // its copy lands, pass 1 in strip order on the caller's stream
             // (stripe s waits for stripe s-1: a strip's blocks only wait for
@@ -2727,7 +2973,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
                 cudaEvent_t e = event_get();
                 cudaEventRecord(e, ts);
                 cudaStreamWaitEvent(st, e, 0);
-                p1.ticket = tickets + std::min<size_t>(s, P1_MAX_LAUNCHES - 1);
+                p1.ticket = tickets + std::min<size_t>(s, P1_MAX_LAUNCHES - 2);  // (the last is the zero unit's)
                 {
                     Prof pr(KK_PASS1, st);
                     launch_pass1(fold, p1_mode(L, p1), p1grid(p1.nst_run), p1smem, st, p1, s > 0);
@@ -2735,13 +2981,34 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             }
             p1.st0 = 0;
             p1.nst_run = L.nst;
-        } else {
+            if (zu) {  // the zero unit reads every strip: after the last transpose
+                cudaEvent_t e_t = event_get();
+                cudaEventRecord(e_t, ts);
+                cudaStreamWaitEvent(zs, e_t, 0);
+            }
+        } else if (nmain > 0) {
             p1.ticket = tickets;
             Prof pr(KK_PASS1, st);
             if (box)
                 k_pass1_box<G1, R_ANCHOR><<<gbox, P1_WARPS * 32, P1_SMEM, st>>>(p1, sp->radius);
             else
                 launch_pass1(fold, p1_mode(L, p1), p1grid(L.nst), p1smem, st, p1);
+        }
+        if (zu) {
+            cudaStreamWaitEvent(zs, e_zu_ready, 0);
+            Pass1Args pz = p1;
+            pz.term0 = 0;
+            pz.nterm = 1;
+            pz.st0 = 0;
+            pz.nst_run = L.nst;
+            pz.ticket = tickets + (P1_MAX_LAUNCHES - 1);
+            {
+                Prof pr(KK_PASS1, zs);
+                launch_pass1_zero(fold, dim3(L.nst * B * pz.zyc), p1smem, zs, pz);
+            }
+            cudaEvent_t e_z1 = event_get();
+            cudaEventRecord(e_z1, zs);
+            cudaStreamWaitEvent(st, e_z1, 0);  // joined before the edge kernel
         }
         if ((rc = check_cuda("pass1"))) return rc;
         if (s2 != st) {  // hand the batch to the second stream
@@ -2785,9 +3052,11 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.ntx = L.ntx;
         p2.k = kc;
         p2.t = td;
-        // pass 2: the block-summed variant (k_pass2_gr) for the Gaussian
-        const int npart = box ? -1 : (((n + G2 - 1) / G2 + P2R_GR - 1) / P2R_GR);
-        p2.ngroups = (n + G2 - 1) / G2;
+        // pass 2: the block-summed variant (k_pass2_gr) for the Gaussian, over
+        // the terms after the zero unit when it has its own pass 2
+        p2.term0 = term0;
+        const int npart = box ? -1 : (((nmain + G2 - 1) / G2 + P2R_GR - 1) / P2R_GR);
+        p2.ngroups = (nmain + G2 - 1) / G2;
         {
             const double g = sp->g1 * sp->g2;
             p2.wscale = box ? 1.f : (float)(fold ? g * g * g * g : g * g);
@@ -2810,9 +3079,49 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p2.xb2 = pp.xb2;
         p2.xord = pp.xord;
         if (pp.xlpt) p2.order = 4;
+        // the zero unit's pass 2 on its side stream, after the edge kernel;
+        // every reduce below waits for it
+        const size_t xpl = xm_plane(B, W, H);
+        cudaEvent_t e_z2 = nullptr;
+        if (zu) {
+            cudaEvent_t e_e = event_get();
+            cudaEventRecord(e_e, s2);
+            cudaStreamWaitEvent(zs, e_e, 0);
+            ZeroArgs za;
+            za.B = B;
+            za.H = H;
+            za.W = W;
+            za.ntx = L.ntx;
+            za.hq = L.zhq;
+            za.term = 0;
+            za.k = kc;
+            za.warm_tiles = pp.warm_tiles;
+            // x-chunks until ~2 waves of threads (warm-ups of >= K per chunk)
+            int zch = 1;
+            while ((long long)L.zhq * B * zch < 148LL * 12 * 32 * 2 && zch * 2 <= std::max(1, L.ntx / std::max(1, 2 * pp.warm_tiles)))
+                zch *= 2;
+            za.tiles_per_chunk = (L.ntx + zch - 1) / zch;
+            zch = (L.ntx + za.tiles_per_chunk - 1) / za.tiles_per_chunk;
+            za.wt = (float)terms->weight[tbeg] * p2.wscale;
+            za.floc = floc;
+            za.nHx = nHx;
+            za.Hx = p2.Hx;
+            za.s0 = s0;
+            za.bstate = bst;
+            za.num = part + (size_t)npart * 2 * xpl;
+            {
+                Prof pr(KK_PASS2, zs);
+                k_pass2_zero<<<dim3((L.zhq + 127) / 128, zch, B), 128, 0, zs>>>(za);
+            }
+            if ((rc = check_cuda("pass2 zero unit"))) return rc;
+            e_z2 = event_get();
+            cudaEventRecord(e_z2, zs);
+        }
         ReduceArgs ra;
         ra.part = part;
-        ra.ngroups = npart > 0 ? npart : p2.ngroups;
+        ra.ngroups = box ? p2.ngroups : npart;
+        ra.zpart = zu ? part + (size_t)npart * 2 * xpl : nullptr;
+        ra.den_add = zu ? (float)terms->weight[tbeg] : 0.f;
         ra.B = B;
         ra.H = H;
         ra.W = W;
@@ -2837,7 +3146,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             p2.rb0 = rb0;
             p2.nrb_run = nrun;
             dim3 g2(nrun * nchunk, p2.ngroups, B);
-            {
+            if (nmain > 0) {
                 Prof pr(KK_PASS2, q);
                 if (box)
                     k_pass2_box<G2, R_ANCHOR><<<g2, P2_THREADS, 0, q>>>(p2, sp->radius);
@@ -2851,6 +3160,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             int e;
             if ((e = check_cuda("pass2"))) return e;
             ra.i_base = rb0 * P2_THREADS;  // RED_I == P2_THREADS
+            if (e_z2) cudaStreamWaitEvent(q, e_z2, 0);
             {
                 const int rows = std::min(H - ra.i_base, nrun * P2_THREADS);
                 dim3 rgrid((W + TILE - 1) / TILE, (rows + RED_I - 1) / RED_I, B);
@@ -2982,6 +3292,9 @@ int tbf_set_option(int32_t option, int64_t value) {
             return TBF_OK;
         case TBF_OPT_LPT_SPLIT:
             g_lpt_split = (int)(value & 15);
+            return TBF_OK;
+        case TBF_OPT_ZERO_UNIT:
+            g_zero_unit = value != 0;
             return TBF_OK;
         case TBF_OPT_BATCHES:
             if (value < 1) return fail(TBF_ERR_PARAM, "batches must be >= 1");

@@ -911,3 +911,26 @@ def test_partial_row_bands_sum_to_full(tb):
         assert err_num < 2e-3 and err_den < 1e-5, (world, err_num, err_den)
     with pytest.raises(tb.ParameterError):
         tb.TrigFilter(tuple(f.shape), spec, k).partial(f, full[0], full[1], rows=(64, 700))
+
+
+@pytest.mark.parametrize("h,w,s,sr", [(300, 200, 4.0, 30.0), (517, 130, 8.0, 20.0), (200, 333, 3.0, 80.0)])
+def test_zero_unit_option_matches_oracle(tb, orc, h, w, s, sr):
+    """TBF_OPT_ZERO_UNIT=1 (the zero frequency of an even N as one packed
+    unit: f at four row quarters in the four lanes, its own pass 1 and pass 2,
+    den += w0 in the reduce): full images against the float64 oracle,
+    including the rows next to the quarter boundaries and the bottom edge."""
+    from paper_1105_4204_b200 import _native
+
+    lib = _native.load()
+    f = np.random.default_rng(h * w).uniform(0, 255, (h, w)).astype(np.float32)
+    k = tb.make_trig_kernel(sr, 255.0)
+    assert k.N % 2 == 0
+    ref, _ = orc.bilateral_trig(f.astype(np.float64), "gauss-recursive", s, orc.make_trig_kernel(sr, 255.0))
+    lib.tbf_set_option(_native.TBF_OPT_ZERO_UNIT, 1)
+    try:
+        got = tb.TrigFilter((1, h, w), tb.SpatialSpec.gaussian_recursive(s), k)(torch.from_numpy(f).cuda()[None])
+        torch.cuda.synchronize()
+    finally:
+        lib.tbf_set_option(_native.TBF_OPT_ZERO_UNIT, 0)
+    err = np.abs(got[0].cpu().numpy().astype(np.float64) - ref)
+    assert float(err.max()) <= TOL, (float(err.max()), np.unravel_index(err.argmax(), err.shape))
