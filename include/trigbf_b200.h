@@ -232,6 +232,10 @@ TBF_API int32_t tbf_profile_timeline(double* start_ms, double* dur_ms, int32_t* 
                                 are f at four row quarters (a quarter of a term's work and bytes;
                                 engines.py:265-271 filters f alone there), on a side stream;
                                 default 0 (a full term): measured 1-20% slower end to end */
+#define TBF_OPT_P1_CLUSTER 13 /* stripes per pass-1 thread-block cluster (default 1 = none; else the
+                                 largest of it, 2, 1 that divides the stripe count): the x hand-off
+                                 between a cluster's stripes goes through distributed shared memory
+                                 and mbarriers (bit-identical; measured 2-6% slower) */
 #define TBF_OPT_P1_FOLD 6   /* default 1: folds the y-sweep gain into the pass-2 weights
                                (skips 4 multiplies per pixel-term in pass 1 when T/g^4 is safe); 0 scales in pass 1 */
 TBF_API int tbf_set_option(int32_t option, int64_t value);

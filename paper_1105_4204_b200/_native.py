@@ -34,6 +34,7 @@ TBF_OPT_HOST_BANDS = 8
 TBF_OPT_P2_ORDER = 9
 TBF_OPT_LPT_SPLIT = 11  # bits 1/2: planned y-/x-chunks (device entry); 4/8: also in the host entry
 TBF_OPT_ZERO_UNIT = 12  # 1: the zero frequency as a packed 1-plane unit (default 0)
+TBF_OPT_P1_CLUSTER = 13  # stripes per pass-1 thread-block cluster (default 1 = none)
 TBF_LPT_DEFAULT = 3
 TBF_LAYOUT_INFO_N = 14
 LAYOUT_INFO_FIELDS = ("batches", "batch_terms", "y_chunks", "y_planned", "y_end0", "y_end1", "y_rows_max",

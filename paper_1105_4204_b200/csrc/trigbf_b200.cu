@@ -250,6 +250,61 @@ __device__ __forceinline__ float4 ld_relaxed4(const float4* p) {
     return v;
 }
 
+// Thread-block clusters (the pass-1 x hand-off between the stripes of a
+// cluster through distributed shared memory and mbarriers).
+__device__ __forceinline__ unsigned cluster_ctarank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t map_cluster(uint32_t saddr, unsigned rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_init_cta(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cbar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cbar) : "memory");
+}
+// wait for the phase with the given parity to complete (trap after ~10 s)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
+    const uint32_t a = smem_addr(bar);
+    unsigned spins = 0;
+    for (;;) {
+        uint32_t done;
+        asm volatile(
+            "{\n.reg .pred P;\n"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, P;\n}"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (++spins == (1u << 26)) __trap();
+    }
+}
+__device__ __forceinline__ void st_cluster4(uint32_t caddr, float4 v) {
+    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(caddr), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ unsigned ld_cluster_u32(uint32_t caddr) {
+    unsigned v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(caddr) : "memory");
+    return v;
+}
+
 // Named barriers between pairs of warps (the pass-1 x hand-off inside a
 // block): arrive does not wait; sync waits for `count` threads in total.
 // Barrier ids are immediates (ptxas then reserves ids 0..7 only, not all 16):
@@ -473,6 +528,7 @@ struct Pass1Args {
     int nst;           // stripes of P1_WARPS column tiles (one pass-1 block each, per term)
     int st0, nst_run;  // stripes [st0, st0 + nst_run) in this launch
     int term0, nterm;  // terms [term0, term0 + nterm) of the batch in this launch
+    int cs;            // stripes per thread-block cluster (1: no clusters; divides nst_run)
     int hq;            // zero unit (ZU launch): virtual rows = row quarters of 32-row segments
     int zyc, zrows;    // ... in y-chunks of zrows virtual rows
     Casc k;
@@ -633,7 +689,23 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     // stripe's f run together, and a wave spreads over many independent
     // chains (the hand-off lag of a wave grows with the stripes of one chain
     // in it).
-    if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1u);
+    // clusters of a.cs consecutive stripes (a.cs > 1): the cluster's first
+    // block takes the ticket, the others read it through DSMEM; each block's
+    // incoming hand-off slot and its FULL / EMPTY mbarriers are set up first
+    __shared__ __align__(8) uint64_t s_full, s_empty;
+    const unsigned crank = a.cs > 1 ? cluster_ctarank() : 0u;
+    if (threadIdx.x == 0) {
+        if (crank == 0) s_ticket = atomicAdd(a.ticket, 1u);
+        if (a.cs > 1) {
+            mbar_init_cta(&s_full, 32);
+            mbar_init_cta(&s_empty, 32);
+            fence_mbar_init();
+        }
+    }
+    if (a.cs > 1) {
+        cluster_sync_all();
+        if (threadIdx.x == 0 && crank != 0) s_ticket = ld_cluster_u32(map_cluster(smem_addr(&s_ticket), 0));
+    }
     __syncthreads();
     // a programmatically dependent next launch (the next host strip) may
     // start once every block of this one has got here
@@ -652,7 +724,7 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
             idx /= (unsigned)a.nyc;
         }
         b = (int)(idx % (unsigned)a.B);
-        stripe_r = (int)(idx / (unsigned)a.B);
+        stripe_r = (int)(idx / (unsigned)a.B) * a.cs + (int)crank;
     }
     const int H = a.H, W = a.W;
     const int stripe = a.st0 + stripe_r;
@@ -817,6 +889,14 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     // hand-off slots between the stripe's warps: slot w (warp w -> w+1) holds
     // one float4 per plane and row, after the P1_WARPS tiles
     float4* const hand = reinterpret_cast<float4*>(smem) + (size_t)P1_WARPS * TILE * BUF_LD;
+    // incoming slot of a cluster hand-off (written remotely by the previous
+    // stripe's last warp); in DSMEM terms, the next block's slot for ours
+    float4* const hand_in = hand + (size_t)(P1_WARPS - 1) * 4 * TILE;
+    const bool cl_in = a.cs > 1 && crank > 0;                    // hand-off in from the cluster
+    const bool cl_out = a.cs > 1 && crank + 1 < (unsigned)a.cs;  // hand-off out to the cluster
+    const uint32_t next_slot = cl_out ? map_cluster(smem_addr(hand_in), crank + 1) : 0u;
+    const uint32_t next_full = cl_out ? map_cluster(smem_addr(&s_full), crank + 1) : 0u;
+    const uint32_t prev_empty = cl_in ? map_cluster(smem_addr(&s_empty), crank - 1) : 0u;
     int nout = 0;  // output segments done (the hand-off barriers pair up per segment)
     const int nseg = (Bend - R0 + TILE - 1) / TILE;  // local segments of this chunk
     const int nsteps = 2 * nseg;
@@ -979,6 +1059,18 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
                 ly2[p] = c.w;
             }
             if (!last_out) named_bar_arrive(1 + P1_WARPS + (warp - 1), 64);
+        } else if (cl_in) {
+            // the previous stripe of the cluster wrote our slot (DSMEM)
+            mbar_wait_cluster(&s_full, (unsigned)nout & 1u);
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const float4 c = hand_in[p * TILE + lane];
+                lv1[p] = c.x;
+                lv2[p] = c.y;
+                ly1[p] = c.z;
+                ly2[p] = c.w;
+            }
+            if (!last_out) mbar_arrive_remote(prev_empty);  // slot free for its next segment
         } else if (stripe > 0) {
             // stripe s-1 hands its end state over: wait for its flag for this
             // segment (a hand-off never arrives only if the dispatch order
@@ -1050,6 +1142,14 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
 #pragma unroll
             for (int p = 0; p < 4; ++p) hs[p * TILE] = f4(lv1[p], lv2[p], ly1[p], ly2[p]);
             named_bar_arrive(1 + warp, 64);
+        } else if (cl_out) {
+            // to the next stripe of the cluster: its slot (DSMEM) once it read
+            // the previous segment's, then its FULL barrier (release)
+            if (nout > 0) mbar_wait_cluster(&s_empty, (unsigned)(nout - 1) & 1u);
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+                st_cluster4(next_slot + (uint32_t)((p * TILE + lane) * 16), f4(lv1[p], lv2[p], ly1[p], ly2[p]));
+            mbar_arrive_remote(next_full);
         } else {
             // the stripe's end state (clamped warps past the image edge pass
             // the state of its last column through unchanged) to mail slot
@@ -1064,6 +1164,9 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
         ++nout;
         __syncwarp();
     }
+    // a cluster's blocks keep their shared memory until every remote access
+    // to it is done
+    if (a.cs > 1) cluster_sync_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -2053,6 +2156,8 @@ int g_auto_batches = 2; // tbf_set_option(TBF_OPT_BATCHES): batches when batch_t
 int g_p2_order = 0;     // tbf_set_option(TBF_OPT_P2_ORDER): block order of the block-summed pass 2 (same-box A/B: orders 0 and 1 equal)
 int g_host_strips = 0;  // tbf_set_option(TBF_OPT_HOST_STRIPS): column strips of the host input (0 auto)
 int g_host_bands = 0;   // tbf_set_option(TBF_OPT_HOST_BANDS): row bands of the host output (0 auto)
+int g_p1_cluster = 1;   // tbf_set_option(TBF_OPT_P1_CLUSTER): stripes per pass-1 thread-block cluster
+                        // (1 = none, the default: clusters of 4 measured 2-6% slower)
 int g_zero_unit = 0;    // tbf_set_option(TBF_OPT_ZERO_UNIT): the zero frequency as a packed 1-plane unit
                         // (measured slower end to end: off by default)
 
@@ -2499,8 +2604,9 @@ int validate(const tbf_spatial* sp, const tbf_terms* terms, int tbeg, int tend) 
 
 constexpr int P1_SMEM = P1_WARPS * 4 * G1 * TILE * BUF_LD * 4;
 // Gaussian pass 1: the segment tiles plus the x hand-off slots between the
-// stripe's warps (73.7 KB: 3 blocks per SM still fit the 228 KB)
-constexpr int P1_SMEM_GAUSS = P1_SMEM + (P1_WARPS - 1) * 4 * TILE * 16;
+// stripe's warps and the incoming slot of a cluster hand-off (75.8 KB: 3
+// blocks per SM still fit the 228 KB)
+constexpr int P1_SMEM_GAUSS = P1_SMEM + P1_WARPS * 4 * TILE * 16;  // + the incoming cluster slot: 75.8 KB
 constexpr int P1_SMEM_OCC2 = 80 * 1024;  // padded request: at most 2 pass-1 blocks per SM
 
 // cudaFuncSetAttribute applies to the current device only: done once per
@@ -2636,11 +2742,22 @@ void launch_pass1(bool fold, int mode, dim3 grid, int smem, cudaStream_t st, con
     cfg.blockDim = dim3(P1_WARPS * 32);
     cfg.dynamicSmemBytes = (size_t)smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (p1.cs > 1) {  // clusters of p1.cs consecutive stripes (grid.x is a multiple)
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = (unsigned)p1.cs;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = na;
     switch (mode * 2 + (fold ? 1 : 0)) {
         case 0: cudaLaunchKernelEx(&cfg, k_pass1_gauss<false, 0>, p1); break;
         case 1: cudaLaunchKernelEx(&cfg, k_pass1_gauss<true, 0>, p1); break;
@@ -2805,6 +2922,16 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
     // first batch runs strip by strip as they land (columns are independent
     // in pass 1), the range check and transpose once the whole input is in
     const bool hpipe = hio && !box && L.nslot == 1 && out;
+    // pass-1 thread-block clusters: the largest of TBF_OPT_P1_CLUSTER, 2, 1
+    // stripes that divides the stripe count (cluster hand-offs go through
+    // DSMEM, only the hand-offs between clusters through L2)
+    int p1cs = 1;
+    if (!box)
+        for (int c = std::min(std::max(g_p1_cluster, 1), 8); c > 1; c /= 2)
+            if (L.nst % c == 0) {
+                p1cs = c;
+                break;
+            }
     std::vector<cudaEvent_t> ev_strip;
     std::vector<int> sb{0, L.nst};  // strip boundaries in stripes (P1_WARPS column tiles)
     cudaEvent_t e_ready = nullptr;
@@ -2814,7 +2941,10 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         e_ready = event_get();
         cudaEventRecord(e_ready, st);  // term table queued, earlier users of f done
         cudaStreamWaitEvent(sh, e_ready, 0);
-        if (hpipe) sb = quad_split(L.nst, hio->strips, true);
+        if (hpipe) {  // in whole clusters of stripes
+            sb = quad_split(L.nst / p1cs, hio->strips, true);
+            for (int& v : sb) v *= p1cs;
+        }
         float* df = const_cast<float*>(f);
         for (size_t s = 0; s + 1 < sb.size(); ++s) {
             const int x0 = sb[s] * STRIPE;
@@ -2914,6 +3044,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
         p1.nst_run = L.nst;
         p1.term0 = term0;
         p1.nterm = nmain;
+        p1.cs = p1cs;
         p1.hq = L.zhq;
         // the zero unit's virtual rows in chunks about as long as the main
         // ones (its blocks then run beside the main pass 1), at most nyc
@@ -3002,6 +3133,7 @@ int run_terms(const float* f, float* num, float* den, float* out, int B, int H, 
             pz.st0 = 0;
             pz.nst_run = L.nst;
             pz.ticket = tickets + (P1_MAX_LAUNCHES - 1);
+            pz.cs = 1;
             {
                 Prof pr(KK_PASS1, zs);
                 launch_pass1_zero(fold, dim3(L.nst * B * pz.zyc), p1smem, zs, pz);
@@ -3292,6 +3424,10 @@ int tbf_set_option(int32_t option, int64_t value) {
             return TBF_OK;
         case TBF_OPT_LPT_SPLIT:
             g_lpt_split = (int)(value & 15);
+            return TBF_OK;
+        case TBF_OPT_P1_CLUSTER:
+            if (value < 1 || value > 8) return fail(TBF_ERR_PARAM, "pass-1 cluster size must be in [1, 8]");
+            g_p1_cluster = (int)value;
             return TBF_OK;
         case TBF_OPT_ZERO_UNIT:
             g_zero_unit = value != 0;

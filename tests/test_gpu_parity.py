@@ -934,3 +934,25 @@ def test_zero_unit_option_matches_oracle(tb, orc, h, w, s, sr):
         lib.tbf_set_option(_native.TBF_OPT_ZERO_UNIT, 0)
     err = np.abs(got[0].cpu().numpy().astype(np.float64) - ref)
     assert float(err.max()) <= TOL, (float(err.max()), np.unravel_index(err.argmax(), err.shape))
+
+
+@pytest.mark.parametrize("cs", [2, 4])
+def test_cluster_handoff_option_bit_identical(tb, cs):
+    """TBF_OPT_P1_CLUSTER: the x hand-off between the stripes of a thread-block
+    cluster through distributed shared memory and mbarriers computes the
+    same bits as the L2 mailbox hand-off (same arithmetic, same order)."""
+    from paper_1105_4204_b200 import _native
+    from paper_1105_4204_b200.workloads import smooth_image
+
+    lib = _native.load()
+    f = torch.from_numpy(smooth_image(700, 1024, 12, seed=9)).cuda()[None]  # 8 stripes
+    k = tb.make_trig_kernel(20.0)
+    spec = tb.SpatialSpec.gaussian_recursive(6.0)
+    base = tb.TrigFilter(tuple(f.shape), spec, k)(f)
+    lib.tbf_set_option(_native.TBF_OPT_P1_CLUSTER, cs)
+    try:
+        got = tb.TrigFilter(tuple(f.shape), spec, k)(f)
+        torch.cuda.synchronize()
+    finally:
+        lib.tbf_set_option(_native.TBF_OPT_P1_CLUSTER, 1)
+    assert torch.equal(got, base)
