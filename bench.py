@@ -272,6 +272,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU baseline work")
     ap.add_argument("--flush-mb", type=int, default=512)
+    ap.add_argument("--shard-as", type=int, default=0,
+                    help="test aid: with --gpus 1, run this rank's share of a term/frame split over "
+                         "SHARD_AS ranks (the multi-GPU code path on one GPU, no collective partner)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -307,12 +310,13 @@ def main():
     mode = "replica"
     f0, f1 = 0, cfg.frames
     t0, t1 = 0, pairs.count
-    if world > 1 and args.config == 4:
+    split = world if world > 1 else args.shard_as  # ranks the work is split over
+    if split > 1 and args.config == 4:
         mode = "frames"
-        f0, f1 = frame_range(cfg.frames, world, rank)
-    elif world > 1 and args.config == 5:
+        f0, f1 = frame_range(cfg.frames, split, rank)
+    elif split > 1 and args.config == 5:
         mode = "terms"
-        shard = term_shard(pairs.count, world, rank, cfg.height)
+        shard = term_shard(pairs.count, split, rank, cfg.height)
         t0, t1 = shard.t0, shard.t1
     host = np.empty((f1 - f0, cfg.height, cfg.width), dtype=np.float32)
     for i in range(f0, f1):
@@ -340,7 +344,8 @@ def main():
                 numden.zero_()
             if left is not None:
                 left.partial(src, num, den, accumulate=True, rows=(shard.r0, shard.r1))
-            dist.reduce(numden, dst=0)  # one NCCL reduce of both planes
+            if world > 1:
+                dist.reduce(numden, dst=0)  # one NCCL reduce of both planes
             if rank == 0:
                 fin.finalize(num, den, src, out)
         counters_plan = fin
@@ -489,7 +494,8 @@ def main():
             torch.cuda.synchronize(dev)
             e2e_times.append(time.perf_counter() - t)
         tt = torch.tensor([sum(e2e_times[args.warmup:])], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": px_job * args.steps / float(tt.item()) / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": int(host.nbytes), "d2h_bytes_per_step": int(out.numel() * 4),
                "path": "pinned H2D on every rank, partial, NCCL reduce, finalize and D2H on rank 0"}
@@ -547,6 +553,8 @@ def main():
                        "N": kernel.N, "terms": pairs.count, "spatial_passes": pairs.spatial_passes,
                        "spatial": "gauss-recursive", "parallelism": f"{mode}x{world}",
                        "terms_per_batch": int(getattr(counters_plan, "batch_terms", 0)) or (t1 - t0),
+                       **({"shard_as": args.shard_as, "note": "test aid: one rank's share, no collective"}
+                          if world == 1 and args.shard_as > 1 else {}),
                        "l2": f"flushed before each timed step ({args.flush_mb} MiB write, outside the step events)"},
             "roofline": roofline,
             "pipeline_roofline": pipeline,
