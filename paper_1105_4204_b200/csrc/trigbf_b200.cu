@@ -2470,8 +2470,12 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
     if (!box) q = align_up(q + (size_t)tb * 16 * B * H * 4);
     L->s_bst = q;
     if (!box) q = align_up(q + (size_t)tb * 16 * B * H * 4);
-    L->s_part = q;  // the group blocks' (num, den) pairs, then the zero unit's num plane
-    q = align_up(q + ((size_t)L->ng2 + 1) * 2 * xm_plane(B, W, H) * 4);
+    // the (num, den) pairs of the pass-2 group blocks (box: one per G2-term
+    // group; Gaussian: k_pass2_gr sums P2R_GR groups per block), then the zero
+    // unit's num plane
+    L->s_part = q;
+    const size_t npairs = box ? (size_t)L->ng2 : (size_t)(L->ng2 + P2R_GR - 1) / P2R_GR;
+    q = align_up(q + (npairs + 1) * 2 * xm_plane(B, W, H) * 4);
     L->slot_bytes = q;
     L->off_slot = o;
     o += (size_t)L->nslot * q;
