@@ -2437,10 +2437,30 @@ int make_layout(int B, int H, int W, const tbf_spatial* sp, int nterms_range, in
             L->ych_lpt = n > 1;
         }
     }
-    L->nseg = (L->ych_rows + std::max(L->ywarm, L->Ey) + TILE - 1) / TILE + 1;
     // the zero unit's chunk: the virtual rows (row quarters) plus Ey both ways
     L->zhq = ((H + 3) / 4 + TILE - 1) / TILE * TILE;
-    if (!box) L->nseg = std::max(L->nseg, (L->zhq + 2 * L->Ey + TILE - 1) / TILE + 1);
+    auto seg_count = [&]() {
+        int ns = (L->ych_rows + std::max(L->ywarm, L->Ey) + TILE - 1) / TILE + 1;
+        if (!box) ns = std::max(ns, (L->zhq + 2 * L->Ey + TILE - 1) / TILE + 1);
+        return ns;
+    };
+    L->nseg = seg_count();
+    if (band && !box) {
+        // the workspace is sized for the whole image (tbf_workspace_bytes has no
+        // band): a band's chunks may not need more checkpoint segments than the
+        // whole image's equal chunks; fewer, longer chunks until they fit
+        Layout F;
+        if (make_layout(B, H, W, sp, nterms_range, batch_terms, &F, 0) == TBF_OK) {
+            const long long cap = (long long)F.nyc * F.nseg;
+            while (L->nyc > 1 && (long long)L->nyc * L->nseg > cap) {
+                const int nyc = L->nyc - 1;
+                L->ych_rows = ((Hb + nyc - 1) / nyc + TILE - 1) / TILE * TILE;
+                L->nyc = (Hb + L->ych_rows - 1) / L->ych_rows;
+                for (int c = 0; c <= L->nyc; ++c) L->ychb[c] = std::min(row1, row0 + c * L->ych_rows);
+                L->nseg = seg_count();
+            }
+        }
+    }
     const size_t px = (size_t)B * H * W;
     size_t o = 0;
     L->off_fT = o;

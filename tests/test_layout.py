@@ -104,3 +104,41 @@ def test_layout_info_rejects_bad_arguments(tb):
     shape, spec, k = _cfg(tb, 2)
     with pytest.raises(tb.ParameterError):
         tb.layout_info(shape, spec, k, term_range=(3, 3))
+
+
+@pytest.mark.parametrize("shape,sigma_s,sigma_r,world", [
+    ((1, 700, 300), 9.0, 12.0, 2),
+    ((1, 700, 300), 9.0, 12.0, 3),
+    ((1, 2048, 2048), 8.0, 20.0, 4),
+    ((1, 16384, 16384), 32.0, 15.0, 8),
+    ((1, 4096, 4096), 16.0, 10.0, 8),
+    ((2, 300, 260), 6.0, 15.0, 2),
+])
+def test_row_band_layout_fits_whole_image_workspace(tb, shape, sigma_s, sigma_r, world):
+    """The term-sharded path runs the leftover terms over a row band with a
+    plan (and workspace) sized by tbf_workspace_bytes for the whole image:
+    every rank's band layout must fit it (a band may pick other y-chunks).
+    The workspace check runs before any device work, so a fake device pointer
+    shows which error the call would return: anything but TBF_ERR_WORKSPACE."""
+    import ctypes
+
+    from paper_1105_4204_b200 import _native, engines
+    from paper_1105_4204_b200.distributed import term_shard
+    from paper_1105_4204_b200.kernels import term_pairs
+
+    lib = _native.load()
+    k = tb.make_trig_kernel(sigma_r, 255.0)
+    spec = tb.SpatialSpec.gaussian_recursive(sigma_s)
+    sp = engines.spatial_struct(spec)
+    terms = engines._TermsHolder(k)
+    B, H, W = shape
+    n = term_pairs(k).count
+    fake = ctypes.c_void_p(1 << 40)
+    for rank in range(world):
+        sh = term_shard(n, world, rank, H)
+        if sh.l1 <= sh.l0:
+            continue
+        ws = lib.tbf_workspace_bytes(B, H, W, ctypes.byref(sp), sh.l0, sh.l1, 0)
+        rc = lib.tbf_trig_partial_rows(fake, fake, fake, B, H, W, ctypes.byref(sp), ctypes.byref(terms.struct),
+                                       sh.l0, sh.l1, sh.r0, sh.r1, 0, 0, fake, ws, None)
+        assert rc != 5, (rank, sh, lib.tbf_last_error())  # TBF_ERR_WORKSPACE
