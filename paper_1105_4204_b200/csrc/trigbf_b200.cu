@@ -2720,6 +2720,31 @@ P2Plan p2_chunk_plan(const Layout& L, const tbf_spatial* sp, int ngroups, int np
             if (!ok) break;
             nchunk *= 2;
         }
+        // launches of several waves of k_pass2_gr blocks: the last wave runs
+        // partly empty, so a chunk count whose block count fills the waves
+        // better can pay for its warm-up tiles.  Cost = waves rounded up x
+        // tiles a block walks (its chunk plus the warm-up); a count wins by
+        // >= 3%.  Config 5 (1536 blocks, 3.46 waves): 2 chunks, pass 2 -5%
+        // measured (profiles/sweep_p2_chunks_r02.log)
+        if (npart > 0 && nchunk == 1 && threads >= wave) {
+            const long long blocks1 = (long long)nrb * (P2_THREADS / 32) * npart * B;
+            const long long slots = 148LL * TBF_P2_MINB;
+            auto cost = [&](int n) {
+                const int tpc = (L.ntx + n - 1) / n;
+                const long long waves = (blocks1 * n + slots - 1) / slots;
+                return (double)waves * (tpc + (n > 1 ? pp.warm_tiles : 0));
+            };
+            const double c1 = cost(1);
+            double best = c1;
+            for (int n = 2; n <= 4; ++n) {
+                if ((L.ntx + n - 1) / n < 4 * pp.warm_tiles) break;
+                const double c = cost(n);
+                if (c < best && c < 0.97 * c1) {
+                    best = c;
+                    nchunk = n;
+                }
+            }
+        }
     }
     pp.tiles_per_chunk = (L.ntx + nchunk - 1) / nchunk;
     nchunk = (L.ntx + pp.tiles_per_chunk - 1) / pp.tiles_per_chunk;
