@@ -60,6 +60,9 @@
 
 namespace {
 
+#ifndef TBF_P1_ASTORE
+#define TBF_P1_ASTORE 0  // 1: phase A also writes every segment tile (the round-1/2 code)
+#endif
 constexpr int TILE = 32;          // segment length along y == tile width along x == warp size
 constexpr int P1_WARPS = 4;       // warps per pass-1 block (each a different term group)
 constexpr int P2_THREADS = 128;   // rows per pass-2 block
@@ -642,7 +645,7 @@ __device__ __forceinline__ float4 f4(float a, float b, float c, float d) {
 template <bool STORE>
 __device__ __forceinline__ void p1_fwd8(const float (&fv)[8], float nu_hi, float nu_lo,
                                         const Casc& k, float (&v1)[4], float (&v2)[4],
-                                        float (&y1)[4], float (&y2)[4], float4* row) {
+                                        float (&y1)[4], float (&y2)[4], float4* row, bool st = true) {
     float cs[8], sn[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) sincos_fma(phase(nu_hi, nu_lo, fv[q]), &sn[q], &cs[q]);
@@ -652,7 +655,7 @@ __device__ __forceinline__ void p1_fwd8(const float (&fv)[8], float nu_hi, float
         float o[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) o[p] = cstep(u[p], v1[p], v2[p], y1[p], y2[p], k);
-        if (STORE) row[q * BUF_LD] = make_float4(o[0], o[1], o[2], o[3]);
+        if (STORE && st) row[q * BUF_LD] = make_float4(o[0], o[1], o[2], o[3]);
     }
 }
 
@@ -929,11 +932,15 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
         // (a whole step ahead of their use).  Measured 1-2% faster on configs
         // 1-4 than a separate prefetch array copied at the end of each step.
         const float* const fpn = MODE == 0 ? a.fY + ty_index(b, x0 + lane, nfast ? rn : 0, W, H) : frow(nfast ? rn : 0);
+        // phase A's forward outputs are not needed except on its last step
+        // (the first phase-B step reuses that tile): no shared-memory stores
+        // otherwise (the L1/shared pipe runs at ~80% of peak in this kernel)
+        const bool tile_st = TBF_P1_ASTORE || phaseB || step == nseg - 1;
         if (full) {
 #pragma unroll
             for (int q0 = 0; q0 < TILE; q0 += 8) {
                 p1_fwd8<true>(*reinterpret_cast<const float(*)[8]>(&seg_f[q0]), nu_hi, nu_lo, k, v1, v2,
-                              y1, y2, bl + q0 * BUF_LD);
+                              y1, y2, bl + q0 * BUF_LD, tile_st);
                 if (nfast) {
 #pragma unroll
                     for (int q = q0; q < q0 + 8; ++q) seg_f[q] = ldg_pinned(fpn + q * 32);
