@@ -877,8 +877,9 @@ __global__ void __launch_bounds__(P1_WARPS * 32, P1_BLOCKS_PER_SM) k_pass1_gauss
     // the forward sweep top->bottom (checkpoint stores), steps nseg..2nseg-1
     // revisit the segments bottom->top (restore, forward recompute into the
     // smem tile, backward, epilogue).  Both phases share one copy of the
-    // forward code (instruction-cache footprint); phase A also writes the
-    // tile, which is harmless.  f and checkpoints are prefetched one step ahead.
+    // forward code (instruction-cache footprint); phase A's tile stores are
+    // predicated off except on its last step (tile_st below).  f and
+    // checkpoints are prefetched one step ahead.
     float p1[4], p2[4], q1[4], q2[4];
     // F_loc layout: float4 [term][b][row block of 32][x][32 rows] (row-block
     // tiled so a pass-2 warp streams its rows contiguously along x)
