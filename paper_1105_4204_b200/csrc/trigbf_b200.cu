@@ -1853,26 +1853,25 @@ __global__ void __launch_bounds__(256) k_reduce(const __grid_constant__ ReduceAr
         if (gx < a.W && gi < a.H) {
             const float* pp = a.part + xm_index(b, gx, gi, a.W, a.H);
             if (vec) {
-                // 4 groups (8 float4 loads) in flight, summed in fixed group order
-                int g = 0;
-                for (; g + 4 <= a.ngroups; g += 4) {
+                // up to 4 groups (8 float4 loads) in flight, also for a partial
+                // block of groups (config 5 has 3 per batch), summed in fixed
+                // group order
+                for (int g = 0; g < a.ngroups; g += 4) {
                     float4 vn[4], vd[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        vn[q] = *reinterpret_cast<const float4*>(pp + (size_t)(2 * (g + q)) * plane);
-                        vd[q] = *reinterpret_cast<const float4*>(pp + (size_t)(2 * (g + q) + 1) * plane);
+                        if (g + q < a.ngroups) {
+                            vn[q] = __ldcs(reinterpret_cast<const float4*>(pp + (size_t)(2 * (g + q)) * plane));
+                            vd[q] = __ldcs(reinterpret_cast<const float4*>(pp + (size_t)(2 * (g + q) + 1) * plane));
+                        }
                     }
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        n[0] += vn[q].x; n[1] += vn[q].y; n[2] += vn[q].z; n[3] += vn[q].w;
-                        d[0] += vd[q].x; d[1] += vd[q].y; d[2] += vd[q].z; d[3] += vd[q].w;
+                        if (g + q < a.ngroups) {
+                            n[0] += vn[q].x; n[1] += vn[q].y; n[2] += vn[q].z; n[3] += vn[q].w;
+                            d[0] += vd[q].x; d[1] += vd[q].y; d[2] += vd[q].z; d[3] += vd[q].w;
+                        }
                     }
-                }
-                for (; g < a.ngroups; ++g) {
-                    const float4 vn = *reinterpret_cast<const float4*>(pp + (size_t)(2 * g) * plane);
-                    const float4 vd = *reinterpret_cast<const float4*>(pp + (size_t)(2 * g + 1) * plane);
-                    n[0] += vn.x; n[1] += vn.y; n[2] += vn.z; n[3] += vn.w;
-                    d[0] += vd.x; d[1] += vd.y; d[2] += vd.z; d[3] += vd.w;
                 }
                 if (a.zpart) {  // the zero unit last (fixed order)
                     const float4 vn = *reinterpret_cast<const float4*>(a.zpart + xm_index(b, gx, gi, a.W, a.H));

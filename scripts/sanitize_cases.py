@@ -40,6 +40,8 @@ lib.tbf_set_option(_native.TBF_OPT_ZERO_UNIT, 0)
 lib.tbf_set_option(_native.TBF_OPT_P1_CLUSTER, 4)
 out = tb.TrigFilter(tuple(g.shape), tb.SpatialSpec.gaussian_recursive(3.0), k)(g)
 lib.tbf_set_option(_native.TBF_OPT_P1_CLUSTER, 1)
+# several term batches (workspace num/den accumulation, x-chunks of a multi-batch launch)
+out = tb.TrigFilter(tuple(g.shape), tb.SpatialSpec.gaussian_recursive(3.0), k, batch_terms=4)(g)
 d = tb.bilateral_direct(rng.uniform(0, 255, (20, 23)), tb.SpatialSpec.box(2), k)
 torch.cuda.synchronize()
 print("sanitize cases done")
