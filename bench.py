@@ -248,9 +248,14 @@ def run_reference_arm(args, rank: int):
         "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
         "ms_per_step": cfg.pixels / (value * 1e6) * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        # the same workload keys as the B200 arm's line (its parallelism,
+        # batching and L2 keys describe the device run only)
         "config": {"workload": cfg.name, "shape": [cfg.frames, cfg.height, cfg.width],
-                   "sigma_s": cfg.sigma_s, "sigma_r": cfg.sigma_r,
-                   "N": make_trig_kernel(cfg.sigma_r, cfg.T).N},
+                   "sigma_s": cfg.sigma_s, "sigma_r": cfg.sigma_r, "T": cfg.T,
+                   "N": make_trig_kernel(cfg.sigma_r, cfg.T).N,
+                   "terms": term_pairs(make_trig_kernel(cfg.sigma_r, cfg.T)).count,
+                   "spatial_passes": term_pairs(make_trig_kernel(cfg.sigma_r, cfg.T)).spatial_passes,
+                   "spatial": "gauss-recursive"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
