@@ -142,3 +142,17 @@ def test_row_band_layout_fits_whole_image_workspace(tb, shape, sigma_s, sigma_r,
         rc = lib.tbf_trig_partial_rows(fake, fake, fake, B, H, W, ctypes.byref(sp), ctypes.byref(terms.struct),
                                        sh.l0, sh.l1, sh.r0, sh.r1, 0, 0, fake, ws, None)
         assert rc != 5, (rank, sh, lib.tbf_last_error())  # TBF_ERR_WORKSPACE
+
+
+def test_pass2_chunks_fill_the_last_wave(tb):
+    """Config 5 in 20-term batches: 1536 pass-2 group blocks per x-chunk are
+    3.46 waves of 444 slots; two equal chunks (6.92 waves, 12 warm-up tiles
+    each) cost less under the waves-rounded-up model and measured 5% faster
+    (profiles/sweep_p2_chunks_r02.log).  Configs 3 and 4 (4.9 and 15.6 waves)
+    keep one chunk."""
+    shape, spec, k = _cfg(tb, 5)
+    d = tb.layout_info(shape, spec, k, batch_terms=20)
+    assert d["batches"] == 3 and d["x_chunks"] == 2 and d["x_planned"] == 0 and d["x_tiles_equal"] == 256
+    for cid in (3, 4):
+        shape, spec, k = _cfg(tb, cid)
+        assert tb.layout_info(shape, spec, k)["x_chunks"] == 1
