@@ -321,7 +321,8 @@ def main():
         f0, f1 = frame_range(cfg.frames, split, rank)
     elif split > 1 and args.config == 5:
         mode = "terms"
-        shard = term_shard(pairs.count, split, rank, cfg.height)
+        shard = term_shard(pairs.count, split, rank, cfg.height,
+                           balance=os.environ.get("TBF_TERM_BALANCE") or None)  # development A/B
         t0, t1 = shard.t0, shard.t1
     host = np.empty((f1 - f0, cfg.height, cfg.width), dtype=np.float32)
     for i in range(f0, f1):
@@ -332,7 +333,8 @@ def main():
 
     if mode == "terms":
         # whole terms [t0, t1) plus the leftover terms on this rank's row band
-        # (distributed.term_shard): balanced to ~1.5% at 8 ranks on config 5
+        # (distributed.term_shard, balance="rows"; the default gives the
+        # leftover terms whole to the last ranks)
         plan = tb.TrigFilter(tuple(f.shape), spec, kernel, term_range=(t0, t1)) if t1 > t0 else None
         left = (tb.TrigFilter(tuple(f.shape), spec, kernel, term_range=(shard.l0, shard.l1))
                 if shard.l1 > shard.l0 else None)
@@ -537,7 +539,7 @@ def main():
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": repr(e)}
 
-    if rank == 0:
+    if rank == 0 or world == 1:  # (world 1 with RANK set: --shard-as timing of that rank's share)
         clocks = clk.summary()
         if issue is not None and clocks.get("sm_max_mhz"):
             # 148 SMs x 4 schedulers x 1 warp-instruction per clock

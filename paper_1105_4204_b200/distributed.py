@@ -8,9 +8,11 @@ Two ways the path shards:
   frequency terms (engines.py:264-300 accumulates num/den term by term), so
   each rank accumulates partial num/den planes for its share of the terms,
   the two planes are summed onto the root with one NCCL reduce over
-  NVLink/NVSwitch, and the root applies the guarded ratio.  Whole terms
-  would leave up to a term of imbalance, so the terms left over after an
-  even split go to every rank as a band of rows (term_shard).
+  NVLink/NVSwitch, and the root applies the guarded ratio.  The terms left
+  over after an even split go whole to the last ranks (the root finalizes);
+  splitting them by rows across all ranks balances the term count exactly but
+  costs a second call per rank (a full transpose and an under-filled band
+  launch), measured slower on one rank's share of 8 (term_shard).
 
 The reference has no distributed mode; its only parallelism is a thread pool
 over the 4 planes of one term (engines.py:262-303).
@@ -32,6 +34,14 @@ def frame_range(n_frames: int, world: int, rank: int) -> tuple[int, int]:
 
 ROW_BLOCK = 128  # band granularity of tbf_trig_partial_rows (pass-2 row blocks)
 PASS1_SHARE = 0.6  # share of a term's device time in pass 1 (the part with y warm-ups), measured on config 5
+# Fixed cost of a rank's leftover-band call in whole-term units (its own full
+# transpose and reduce, and a band launch far from filling the GPU): config 5
+# on one rank's share of 8, 7 whole terms + 4 terms x 1/8 of the rows took
+# 24.2 ms against 16.5 ms for the 7 terms (2.36 ms per term), i.e. ~1.6 terms
+# beyond the band's rows (profiles/ab_term_balance_r02.log)
+BAND_FIXED_TERMS = 1.6
+ROOT_FIXED_TERMS = 0.4  # the root's finalize + range check (0.94 ms on config 5)
+TERM_BALANCE = "terms"  # "terms": leftover terms whole to the last ranks; "rows": split by row bands
 
 
 @dataclass
@@ -47,19 +57,33 @@ class TermShard:
     r1: int
 
 
-def term_shard(n_terms: int, world: int, rank: int, height: int, warm_rows: int = 0) -> TermShard:
-    """Balanced split of n_terms pairs across `world` ranks.
+def term_shard(n_terms: int, world: int, rank: int, height: int, warm_rows: int = 0,
+               balance: str | None = None) -> TermShard:
+    """Split of n_terms pairs across `world` ranks.
 
-    Whole terms alone leave up to one term of imbalance (config 5: 60 terms on
-    8 ranks = 8 vs 7.5, +6.7%).  Here every rank takes floor(n/world)
-    consecutive terms over the whole image, and the n % world leftover terms
-    are split by rows instead: every rank filters them over its own band of
-    whole 128-row blocks (tbf_trig_partial_rows).  A band costs its rows plus
-    the y warm-ups on both sides in pass 1, so the bands are what balances.
+    balance="terms" (TERM_BALANCE, the default): contiguous whole terms,
+    floor(n/world) per rank and the n % world leftover ones one each to the
+    last ranks, never to the root while a rank is left (it also finalizes).
+    Up to one term of imbalance (config 5 on 8 ranks: 8 vs 7.5 terms).
+
+    balance="rows": every rank takes floor(n/world) consecutive terms over the
+    whole image, and the leftover terms are split by rows instead: every rank
+    filters them over its own band of whole 128-row blocks
+    (tbf_trig_partial_rows; a band costs its rows plus the y warm-ups on both
+    sides in pass 1).  Exact in term-rows, but each rank makes a second call
+    whose fixed cost (BAND_FIXED_TERMS) outweighs the term it saves.
     """
     if world < 1 or not (0 <= rank < world):
         raise ValueError(f"bad rank {rank} of {world}")
+    balance = balance or TERM_BALANCE
+    if balance not in ("terms", "rows"):
+        raise ValueError(f"unknown balance {balance!r}")
     q, r = divmod(n_terms, world)
+    if balance == "terms":
+        first_extra = world - r  # ranks [world - r, world) take q + 1 terms
+        t0 = rank * q + max(0, rank - first_extra)
+        t1 = t0 + q + (1 if rank >= first_extra else 0)
+        return TermShard(t0, t1, n_terms, n_terms, 0, 0)
     t0, t1 = rank * q, (rank + 1) * q
     l0, l1 = world * q, n_terms
     nrb = -(-height // ROW_BLOCK)
@@ -71,16 +95,17 @@ def term_shard(n_terms: int, world: int, rank: int, height: int, warm_rows: int 
     return TermShard(t0, t1, l0, l1, r0, r1)
 
 
-def shard_cost(sh: TermShard, height: int, warm_rows: int) -> float:
+def shard_cost(sh: TermShard, height: int, warm_rows: int, root: bool = False) -> float:
     """Model of a rank's device time in whole-image term units: pass 1 (the
     PASS1_SHARE of a term) sweeps a band's rows plus its warm-ups, pass 2
-    the band's rows."""
-    full = sh.t1 - sh.t0
+    the band's rows; a band call adds BAND_FIXED_TERMS, the root
+    ROOT_FIXED_TERMS."""
+    full = float(sh.t1 - sh.t0) + (ROOT_FIXED_TERMS if root else 0.0)
     if sh.l1 <= sh.l0:
-        return float(full)
+        return full
     ext = min(height, sh.r1 + warm_rows) - max(0, sh.r0 - warm_rows)
     frac = PASS1_SHARE * ext / height + (1.0 - PASS1_SHARE) * (sh.r1 - sh.r0) / height
-    return full + (sh.l1 - sh.l0) * frac
+    return full + (sh.l1 - sh.l0) * frac + BAND_FIXED_TERMS
 
 
 @dataclass
@@ -103,12 +128,13 @@ def reduce_numden(numden, dst: int = 0, group=None) -> None:
 
 
 def bilateral_trig_term_sharded(f, spatial, kernel, *, partial_fn=None, finalize_fn=None,
-                                group=None):
+                                group=None, balance: str | None = None):
     """Term-sharded filter of one image on every rank of the default group.
 
     Every rank holds the full input `f` ([B, H, W] float32).  Returns the
-    filtered image on rank 0 and None elsewhere.  The split is term_shard's:
-    whole terms plus a row band of the leftover terms per rank.
+    filtered image on rank 0 and None elsewhere.  The split is term_shard's
+    (`balance`: whole terms, or whole terms plus a row band of the leftover
+    terms per rank).
     `partial_fn(f, num, den, t0, t1, rows=None, accumulate=False)` /
     `finalize_fn(num, den, f, out)` default to the device path (TrigFilter);
     tests inject CPU implementations to exercise the partitioning and the
@@ -122,7 +148,7 @@ def bilateral_trig_term_sharded(f, spatial, kernel, *, partial_fn=None, finalize
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     pairs = term_pairs(kernel)
     H = int(f.shape[-2])
-    sh = term_shard(pairs.count, world, rank, H)
+    sh = term_shard(pairs.count, world, rank, H, balance=balance)
     numden = torch.zeros((2, *f.shape), dtype=f.dtype, device=f.device)
     num, den = numden[0], numden[1]
     plan_for_checks = None

@@ -25,14 +25,20 @@ def test_frame_range_partition():
             assert max(sizes) - min(sizes) <= 1
 
 
-def test_term_shard_partition():
+@pytest.mark.parametrize("balance", ["terms", "rows"])
+def test_term_shard_partition(balance):
     """Every (term, row) is covered exactly once: whole terms are contiguous
-    and disjoint across ranks, the leftover terms' row bands tile [0, H) in
-    whole 128-row blocks."""
+    and disjoint across ranks; with balance="rows" the leftover terms' row
+    bands tile [0, H) in whole 128-row blocks; with balance="terms" the
+    leftover terms go one each to the last ranks (the root keeps the fewest)."""
     for n_terms in (60, 22, 133, 16, 3, 34):
         for world in (1, 2, 3, 4, 8):
             for H in (16384, 2048, 300):
-                sh = [term_shard(n_terms, world, r, H) for r in range(world)]
+                sh = [term_shard(n_terms, world, r, H, balance=balance) for r in range(world)]
+                if balance == "terms":
+                    counts = [s.t1 - s.t0 for s in sh]
+                    assert max(counts) - min(counts) <= 1 and counts[0] == min(counts)
+                    assert counts == sorted(counts)
                 cover = np.zeros((n_terms, H), dtype=int)
                 for s in sh:
                     cover[s.t0:s.t1, :] += 1
@@ -41,17 +47,27 @@ def test_term_shard_partition():
                 assert np.all(cover == 1), (n_terms, world, H)
 
 
-def test_term_shard_imbalance_config5_8_ranks():
-    """Config 5 (60 terms, 16384 rows, y warm-up 384 rows) on 8 ranks: the
-    modelled max rank time is within 3% of the mean (whole terms alone: 8 vs
-    7.5 terms, +6.7%)."""
+def test_term_shard_balance_config5():
+    """Config 5 (60 terms, 16384 rows, y warm-up 384 rows): the row-band split
+    evens out the term-rows exactly (within 3% of the mean before its fixed
+    cost), but with the measured fixed cost of the band call (a full
+    transpose and an under-filled launch: one rank's share of 8 took 24.2 ms
+    vs 21.1 ms for the busiest whole-term rank, profiles/ab_term_balance_r02.log)
+    the whole-term split (the default) models and measures cheaper; 2 and 4
+    ranks divide 60 evenly."""
+    from paper_1105_4204_b200 import distributed as d
+
     H, warm = 16384, 384
     for world in (2, 4, 8):
-        costs = [shard_cost(term_shard(60, world, r, H), H, warm) for r in range(world)]
-        mean = 60.0 / world
-        assert max(costs) <= 1.03 * mean, (world, costs)
-    whole = max(len(range(r, 60, 8)) for r in range(8))
-    assert whole / 7.5 > 1.06  # what the band split removes
+        rows = [term_shard(60, world, r, H, balance="rows") for r in range(world)]
+        terms = [term_shard(60, world, r, H) for r in range(world)]
+        band_only = [shard_cost(s, H, warm) - (d.BAND_FIXED_TERMS if s.l1 > s.l0 else 0.0) for s in rows]
+        assert max(band_only) <= 1.03 * 60.0 / world, (world, band_only)
+        c_rows = max(shard_cost(s, H, warm, root=(r == 0)) for r, s in enumerate(rows))
+        c_terms = max(shard_cost(s, H, warm, root=(r == 0)) for r, s in enumerate(terms))
+        assert c_terms <= c_rows, (world, c_terms, c_rows)
+    counts = [s.t1 - s.t0 for s in (term_shard(60, 8, r, H) for r in range(8))]
+    assert counts == [7, 7, 7, 7, 8, 8, 8, 8]  # the root (finalize) among the 7s
 
 
 def _free_port():
@@ -76,7 +92,7 @@ def _partial_oracle(plane, sigma_s, kernel, t0, t1):
     return num, den
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, balance="rows"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -106,7 +122,7 @@ def _worker(rank, world, port, q):
             out.copy_(torch.from_numpy(o))
 
         out = bilateral_trig_term_sharded(f, SpatialSpec.gaussian_recursive(3.0), k,
-                                          partial_fn=partial_fn, finalize_fn=finalize_fn)
+                                          partial_fn=partial_fn, finalize_fn=finalize_fn, balance=balance)
         if rank == 0:
             ref, _ = orc.bilateral_trig(plane, "gauss-recursive", 3.0, okern)
             q.put(float(np.max(np.abs(out.numpy() - ref))))
@@ -116,11 +132,12 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_term_sharded_reduce_gloo_world2():
+@pytest.mark.parametrize("balance", ["rows", "terms"])
+def test_term_sharded_reduce_gloo_world2(balance):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, balance)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in procs]

@@ -25,7 +25,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _term_worker(rank, world, port, q):
+def _term_worker(rank, world, port, q, balance):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -60,8 +60,9 @@ def _term_worker(rank, world, port, q):
             plan.finalize(num.cuda(), den.cuda(), f_.cuda(), o)
             out.copy_(o.cpu())
 
-        sh = term_shard(term_pairs(k).count, world, rank, 700)
-        out = bilateral_trig_term_sharded(f, spec, k, partial_fn=partial_fn, finalize_fn=finalize_fn)
+        sh = term_shard(term_pairs(k).count, world, rank, 700, balance=balance)
+        out = bilateral_trig_term_sharded(f, spec, k, partial_fn=partial_fn, finalize_fn=finalize_fn,
+                                          balance=balance)
         if rank == 0:
             ref = tb.bilateral_trig(f.cuda(), spec, k).cpu()
             q.put((rank, (sh.t0, sh.t1, sh.l0, sh.l1, sh.r0, sh.r1), float((out - ref).abs().max())))
@@ -73,11 +74,12 @@ def _term_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_term_sharded_device_partials_world2():
+@pytest.mark.parametrize("balance", ["rows", "terms"])
+def test_term_sharded_device_partials_world2(balance):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_term_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_term_worker, args=(r, 2, port, q, balance)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=300) for _ in procs)
@@ -85,8 +87,11 @@ def test_term_sharded_device_partials_world2():
         p.join(timeout=60)
     (r0, sh0, e0), (r1, sh1, e1) = res
     assert sh0 is not None and sh1 is not None, res
-    # both ranks have whole terms and a band of the leftover term
-    assert sh0[1] > sh0[0] and sh1[1] > sh1[0] and sh0[3] > sh0[2] and sh0[5] > sh0[4] and sh1[5] > sh1[4], res
+    assert sh0[1] > sh0[0] and sh1[1] > sh1[0], res
+    if balance == "rows":  # both ranks also have a band of the leftover term
+        assert sh0[3] > sh0[2] and sh0[5] > sh0[4] and sh1[5] > sh1[4], res
+    else:  # the leftover term goes whole to the last rank
+        assert sh1[1] - sh1[0] == sh0[1] - sh0[0] + 1 and sh0[3] == sh0[2], res
     # fp32 partial num/den summed in another order than one process (93 pairs; tolerance 1e-3 T = 0.255)
     assert isinstance(e0, float) and e0 < 1e-2, res
     assert e1 is None, res

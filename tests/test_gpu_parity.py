@@ -897,7 +897,7 @@ def test_partial_row_bands_sum_to_full(tb):
     for world in (2, 3):
         acc = torch.zeros_like(full)
         for r in range(world):
-            sh = term_shard(n, world, r, 700)
+            sh = term_shard(n, world, r, 700, balance="rows")
             if sh.t1 > sh.t0:
                 part = torch.zeros_like(full)
                 tb.TrigFilter(tuple(f.shape), spec, k, term_range=(sh.t0, sh.t1)).partial(f, part[0], part[1])

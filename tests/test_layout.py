@@ -135,7 +135,7 @@ def test_row_band_layout_fits_whole_image_workspace(tb, shape, sigma_s, sigma_r,
     n = term_pairs(k).count
     fake = ctypes.c_void_p(1 << 40)
     for rank in range(world):
-        sh = term_shard(n, world, rank, H)
+        sh = term_shard(n, world, rank, H, balance="rows")
         if sh.l1 <= sh.l0:
             continue
         ws = lib.tbf_workspace_bytes(B, H, W, ctypes.byref(sp), sh.l0, sh.l1, 0)
