@@ -22,8 +22,9 @@ flush = torch.empty(128 << 20, device="cuda")
 for cid in [int(c) for c in sys.argv[1].split(",")]:
     cfg = workloads.CONFIGS[cid]
     f = torch.from_numpy(workloads.make_input(cfg, frames=cfg.frames)).cuda()
+    bt = os.environ.get("TBF_BT")  # terms per batch (default: the engine's pick)
     plan = tb.TrigFilter(tuple(f.shape), tb.SpatialSpec.gaussian_recursive(cfg.sigma_s),
-                         tb.make_trig_kernel(cfg.sigma_r, cfg.T))
+                         tb.make_trig_kernel(cfg.sigma_r, cfg.T), batch_terms=int(bt) if bt else None)
     out = torch.empty_like(f)
     plan(f, out)
     torch.cuda.synchronize()
@@ -45,7 +46,7 @@ for cid in [int(c) for c in sys.argv[1].split(",")]:
         for i in range(nk):
             if ln[i]:
                 per.setdefault(lib.tbf_kernel_name(i).decode(), []).append(ms[i])
-    print(f"{cfg.name} {os.path.basename(sys.argv[2]) if len(sys.argv) > 2 else 'default'} {os.environ.get('TBF_OPTS', '')}: "
+    print(f"{cfg.name} {os.path.basename(sys.argv[2]) if len(sys.argv) > 2 else 'default'} {os.environ.get('TBF_OPTS', '')} bt={plan.batch_terms}: "
           f"{np.median(tot):.3f} ms  " + "  ".join(f"{k} {np.median(v):.3f}" for k, v in per.items()), flush=True)
     del plan, f, out
     torch.cuda.empty_cache()
