@@ -35,11 +35,12 @@ def frame_range(n_frames: int, world: int, rank: int) -> tuple[int, int]:
 ROW_BLOCK = 128  # band granularity of tbf_trig_partial_rows (pass-2 row blocks)
 PASS1_SHARE = 0.6  # share of a term's device time in pass 1 (the part with y warm-ups), measured on config 5
 # Fixed cost of a rank's leftover-band call in whole-term units (its own full
-# transpose and reduce, and a band launch far from filling the GPU): config 5
-# on one rank's share of 8, 7 whole terms + 4 terms x 1/8 of the rows took
-# 24.2 ms against 16.5 ms for the 7 terms (2.36 ms per term), i.e. ~1.6 terms
-# beyond the band's rows (profiles/ab_term_balance_r02.log)
-BAND_FIXED_TERMS = 1.6
+# transpose and reduce, and a band launch far from filling the GPU): config 5,
+# the root's share of 8: 7 whole terms + the band of 4 leftover terms took
+# 24.2 ms against 20.0 ms for the 7 terms alone, i.e. 1.77 terms at 2.36 ms per
+# term, of which the model's band rows account for 0.61
+# (profiles/ab_term_balance_r02.log)
+BAND_FIXED_TERMS = 1.2
 ROOT_FIXED_TERMS = 0.4  # the root's finalize + range check (0.94 ms on config 5)
 TERM_BALANCE = "terms"  # "terms": leftover terms whole to the last ranks; "rows": split by row bands
 
